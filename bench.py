@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the KSE-Parareal hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1] = "c2", the config the headline metric
+"fine RK-3 fp64 cell-updates/s" is quoted on): 64 independent slice states
+on a 256x256 periodic grid (cs=1, U=0.1), seeded random-mode inputs, each
+advanced 200 RK3 steps at CFL 0.5.  One bench step = the whole batch x 200
+steps.  Unit of work: one cell's (u, v, p) advanced one RK3 step.
+
+  value      device throughput, inputs resident in HBM, L2 flushed between
+             timed steps (CUDA events on the launching stream, max over ranks)
+  e2e        the same through the public API (SlicePropagator.__call__ path:
+             pinned host input -> device -> 200 steps -> host), copies timed
+  roofline   48 algorithmic bytes per cell-update / avg launch duration vs
+             MEASURED_PEAKS.json hbm_gbs (burst: the kernel is timed alone)
+  cpu_baseline  the CPU oracle port (oracle/pw_oracle.c, reference operation
+             order, all host threads) on a bounded sample of the same workload
+  parareal   c3 KSE-Parareal window (512^2, P=64, K=5) iteration time and
+             phase split, when --parareal is given (default on at N=1)
+
+--impl reference times the reference's CPU implementation of the path: the
+oracle port (the reference itself is Python and is not on the GPU box).
+Multi-GPU (torchrun): each rank advances its own 64-state batch (weak
+scaling, no data-path collective -- slices are independent).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GRID = 256
+BATCH = 64
+STEPS_PER_SAMPLE = 200
+BYTES_PER_CELL_UPDATE = 48  # read (u,v,p) + write (u,v,p), fp64
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(seconds_target=12.0):
+    """Oracle port (reference operation order, C, all host threads) on a bounded c2 sample."""
+    from oracle import oracle as orc
+    from paper_1510_02237_b200 import harness
+
+    threads = orc.num_threads()
+    q0 = harness.fine_batch_states(n=N_GRID, batch=BATCH, seed=2001)
+    prop = orc.SlicePropagator(orc.RK3, 1, nx=N_GRID, ny=N_GRID, cs=harness.CS, order=6, nu=0.005,
+                               cfl=0.5, velocity=("constant", harness.VEL_U, harness.VEL_V),
+                               nthreads=threads)
+    t0 = time.perf_counter()
+    prop.batch(q0)  # one RK3 step on all 64 states: calibrate
+    one = time.perf_counter() - t0
+    nsteps = max(1, min(STEPS_PER_SAMPLE, int(seconds_target / max(one, 1e-3))))
+    prop.nsteps = nsteps
+    t0 = time.perf_counter()
+    prop.batch(q0)
+    el = time.perf_counter() - t0
+    cells = BATCH * N_GRID * N_GRID * nsteps
+    return {"value": cells / el, "unit": "cell-updates/s", "cores": threads, "kind": "port",
+            "sample": f"c2: {BATCH} states x {N_GRID}^2 x {nsteps} RK3 steps (of 200), "
+                      f"{el:.1f} s on {threads} host threads (oracle/pw_oracle.c, reference op order)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    per = max(2.0, min(8.0, 90.0 / max(1, args.steps)))
+    res = [cpu_baseline(seconds_target=per) for _ in range(max(1, args.steps))]
+    vals = [r["value"] for r in res]
+    v = statistics.median(vals)
+    cb = dict(res[-1])
+    cb["value"] = v
+    line = {"metric": "fine RK-3 fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "impl": "reference", "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2: 64 states x 256^2 x 200 RK3 steps, cs=1, U=0.1",
+                       "implementation": "CPU port of the reference kernels (oracle/pw_oracle.c)"},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "vs_baseline": None}
+    print(json.dumps(line), flush=True)
+
+
+def parareal_c3(dev_index):
+    """c3 KSE window: 512^2, P=64, K=5; per-iteration device time and phases."""
+    import numpy as np
+    import torch
+
+    from paper_1510_02237_b200 import harness
+    from paper_1510_02237_b200.integrators import RK3, SPLIT_FE_FB, SlicePropagator, make_propagator
+    from paper_1510_02237_b200.mesh import ACOUSTIC, ConstantVelocity, build_grid
+    from paper_1510_02237_b200.parareal import Timings, kse_sweep
+    from paper_1510_02237_b200.physics import ModelSpec
+
+    wl = harness.WORKLOADS["c3"]
+    g = build_grid(wl.n, wl.n)
+    vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
+    fine = SlicePropagator(make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), g, 0.5),
+                           wl.slice_span)
+    coarse = SlicePropagator(make_propagator(SPLIT_FE_FB, ModelSpec(ACOUSTIC, vel, 1, 1.0, 0.1, 1.0), g,
+                                             4.0, 16), wl.slice_span)
+    q0 = torch.as_tensor(harness.initial_state("c3")).cuda()
+    tm = Timings()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm, return_device=True)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"workload": "c3: 512^2, P=64, K=5 KSE-Parareal window", "window_s": wall,
+            "iteration_s": wall / wl.n_it,
+            "phases_s": {"coarse_and_correction": tm.coarse, "fine": tm.fine, "qr": tm.qr},
+            "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res]}
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_1510_02237_b200 import _lib, harness
+    from paper_1510_02237_b200.integrators import RK3, SlicePropagator, make_propagator
+    from paper_1510_02237_b200.mesh import ACOUSTIC, ConstantVelocity, build_grid
+    from paper_1510_02237_b200.physics import ModelSpec
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    g = build_grid(N_GRID, N_GRID)
+    vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
+    spec = make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, harness.CS, 0.005, 1.0), g, 0.5)
+    prop = SlicePropagator(spec, nsteps=STEPS_PER_SAMPLE)
+    ctx = prop.ctx
+    q_host = torch.as_tensor(harness.fine_batch_states(n=N_GRID, batch=BATCH, seed=2001 + rank))
+    x = q_host.cuda()
+    out = torch.empty_like(x)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    for _ in range(args.warmup):
+        prop.apply(x, out=out)
+    barrier()
+    # ---------------- device-resident timed region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for s in range(args.steps):
+            flush.zero_()
+            evs[s][0].record(stream)
+            prop.apply(x, out=out)
+            evs[s][1].record(stream)
+        barrier()
+    launches = ctx.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    cells_per_step = BATCH * N_GRID * N_GRID * STEPS_PER_SAMPLE
+    value = world * cells_per_step * args.steps / (tot_ms * 1e-3)
+    ms_per_step = tot_ms / args.steps
+
+    # ---------------- end-to-end through the public API (host buffers, copies timed)
+    pinned_in = q_host.pin_memory()
+    pinned_out = torch.empty_like(pinned_in).pin_memory()
+    e2e_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    prop.apply(pinned_in.cuda(non_blocking=True))
+    barrier()
+    e2e_ev[0].record(stream)
+    for _ in range(args.steps):
+        xd = pinned_in.to("cuda", non_blocking=True)
+        yd = prop.apply(xd)
+        pinned_out.copy_(yd, non_blocking=True)
+    e2e_ev[1].record(stream)
+    barrier()
+    e2e_ms = e2e_ev[0].elapsed_time(e2e_ev[1])
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * cells_per_step * args.steps / (e2e_ms * 1e-3)
+    ok = bool(torch.isfinite(pinned_out).all())
+
+    peak, peak_kind = load_peaks()
+    launch_s = (ms_per_step * 1e-3) / STEPS_PER_SAMPLE
+    algo_bytes = BYTES_PER_CELL_UPDATE * BATCH * N_GRID * N_GRID
+    achieved = algo_bytes / launch_s / 1e9
+
+    extra = {}
+    if rank == 0 and world == 1 and args.parareal:
+        extra["parareal"] = parareal_c3(local_rank)
+    if rank == 0:
+        line = {
+            "metric": "fine RK-3 fp64 cell-updates/s", "value": value, "unit": "cell-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "c2: 64 states x 256^2 periodic x 200 RK3 steps (CFL 0.5, order 6, "
+                                   "nu 0.005, cs=1, U=0.1), seeded random-mode fields",
+                       "global_batch_states": BATCH * world, "grid": N_GRID,
+                       "rk3_steps_per_state": STEPS_PER_SAMPLE, "parallelism": f"slice-sharded x{world}",
+                       "l2": "256 MiB flush between timed steps; the 200 chained RK3 launches inside a "
+                             "step keep their natural L2 reuse"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "algorithmic_bytes_per_launch": algo_bytes,
+                         "avg_launch_us": launch_s * 1e6,
+                         "kernel": "rk3_fused_kernel (one launch per RK3 step over all 64 states)"},
+            "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": int(q_host.numel() * 8),
+                    "d2h_bytes_per_step": int(q_host.numel() * 8), "finite": ok},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--parareal", dest="parareal", action="store_true", default=True)
+    ap.add_argument("--no-parareal", dest="parareal", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

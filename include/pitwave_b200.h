@@ -1,0 +1,146 @@
+/*
+ * pitwave_b200.h -- C ABI of the B200 (sm_100a) KSE-Parareal hot path.
+ *
+ * Drop-in boundary for the reference package `pitwave` (arXiv 1510.02237).
+ * The reference is pure Python; its FFI-free seam for this path is the set
+ * of propagator callables, the Subspace object and the sweep cores.  Every
+ * entry point below replaces one of them (reference file:line cited) and is
+ * bound from Python with ctypes (paper_1510_02237_b200/_lib.py; see
+ * INTEGRATION.md for the binding a pitwave maintainer would add).
+ *
+ * Conventions
+ *  - plain pointers and sizes, no torch or C++ types;
+ *  - `double*` arguments documented "device" are CUDA device pointers on
+ *    the context's device, "host" are host pointers;
+ *  - a state is (3, ny, nx) fp64, x fastest (mesh.State, mesh.py:74-138);
+ *    batches are `batch` states at a stride of `ld` doubles;
+ *  - every call returns PW_OK (0) or a negative status; the message of the
+ *    last failure on the calling thread is in pw_last_error().  Structural
+ *    errors map to the reference's ValueError, numerical blow-up is NOT an
+ *    error (the reference silences overflow, integrators.py:141-145).
+ *  - all work is enqueued on the context stream; calls return without
+ *    synchronising unless they return a host value (documented).
+ */
+#ifndef PITWAVE_B200_H
+#define PITWAVE_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PW_OK 0
+#define PW_ERR_VALUE (-1)     /* reference ValueError (bad shape, ratio, order ...) */
+#define PW_ERR_CUDA (-2)      /* CUDA / driver failure                             */
+#define PW_ERR_LIBRARY (-3)   /* cuBLAS / cuSOLVER failure                          */
+#define PW_ERR_MEMORY (-4)    /* device allocation failed                           */
+#define PW_ERR_STATE (-5)     /* object used in the wrong state                     */
+
+#define PW_SCHEME_RK3 0          /* integrators.rk3_step, integrators.py:79-85         */
+#define PW_SCHEME_SPLIT_FE_FB 1  /* integrators.split_fe_fb_step, integrators.py:103-106 */
+
+#define PW_MODE_ORIGINAL 0       /* parareal.parareal_sweep, parareal.py:68-97 */
+#define PW_MODE_KSE 1            /* parareal.kse_sweep,      parareal.py:100-138 */
+
+typedef struct pw_ctx pw_ctx;
+typedef struct pw_prop pw_prop;
+typedef struct pw_basis pw_basis;
+
+/* Propagator description: integrators.PropagatorSpec (integrators.py:26-61)
+ * + make_propagator (64-76) + the step count of one propagate() call
+ * (126-146).  h = PropagatorSpec.dt; a1/a2 = damping_coefficients
+ * (physics.py:54-58) of the step (RK3) or of one acoustic substep (FE-FB).
+ * uf/vf: host (ny*nx) face-velocity arrays (mesh.face_normal_velocities,
+ * mesh.py:232-247), copied to the device; if const_velocity != 0 they may be
+ * NULL and (vel_u, vel_v) is used (mesh.ConstantVelocity, mesh.py:162-176). */
+typedef struct pw_pde_desc {
+  int scheme;
+  int nx, ny;
+  double dx, dy;
+  double cs;
+  int order;        /* advective flux order 1..6 (stencils.VALID_ORDERS) */
+  double a1, a2;
+  double h;
+  int n_sound;
+  int nsteps;       /* fixed steps per apply */
+  int const_velocity;
+  double vel_u, vel_v;
+  const double* uf; /* host */
+  const double* vf; /* host */
+} pw_pde_desc;
+
+/* ---- library / context ------------------------------------------------ */
+const char* pw_last_error(void);
+int pw_version(void);
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int pw_ctx_create(int device, void* stream, pw_ctx** out);
+int pw_ctx_destroy(pw_ctx* ctx);
+int pw_ctx_set_stream(pw_ctx* ctx, void* stream);
+int pw_ctx_synchronize(pw_ctx* ctx);
+/* strict != 0: run the reference-operation-order kernels everywhere (bitwise
+ * parity mode); default uses the folded fused RK3 kernel for constant velocity. */
+int pw_ctx_set_strict(pw_ctx* ctx, int strict);
+/* number of kernels this library has launched on the context (host value). */
+long long pw_ctx_launch_count(pw_ctx* ctx);
+
+/* ---- propagators: the reference's fine/coarse callables -----------------
+ * replaces PitConfig.vector_propagators closures (parareal.py:182-194) and
+ * propagate() (integrators.py:126-146), batched over slices (_fine_all,
+ * parareal.py:62-65). */
+int pw_prop_create_pde(pw_ctx* ctx, const pw_pde_desc* desc, pw_prop** out);
+/* dense linear propagator q -> A q (the reference tests' matrix seam,
+ * tests/test_parareal.py:14-15); a: device, d x d, column-major. */
+int pw_prop_create_dense(pw_ctx* ctx, const double* a, int d, pw_prop** out);
+int pw_prop_destroy(pw_prop* prop);
+long long pw_prop_dim(const pw_prop* prop);
+/* out[b] = P(in[b]) for b < batch; in/out device, stride ld (>= dim); in == out allowed. */
+int pw_prop_apply(pw_prop* prop, const double* in, double* out, int batch, long long ld);
+
+/* ---- Krylov subspace: subspace.Subspace (subspace.py:31-98) ----------- */
+/* capacity: max snapshot columns kept (the reference keeps all). */
+int pw_basis_create(pw_ctx* ctx, long long dim, double rank_tol, int capacity, pw_basis** out);
+int pw_basis_destroy(pw_basis* basis);
+/* Subspace.update (subspace.py:46-80): append p snapshot/image pairs (device,
+ * column-major d x p, ld = dim) and refactor all columns (pivoted QR,
+ * rank_tol truncation, FQ = images * scatter(R^-1)).  Synchronises (rank). */
+int pw_basis_update(pw_basis* basis, const double* states, const double* images, int p);
+int pw_basis_rank(const pw_basis* basis);
+int pw_basis_ncols(const pw_basis* basis);
+/* device pointers (column-major, ld = dim) valid until the next update */
+int pw_basis_views(const pw_basis* basis, const double** q, const double** fq,
+                   const double** snapshots, const double** images);
+/* host copy of |R_jj| / |R_11| for j < ncols (rank diagnostics) and pivots */
+int pw_basis_diag(const pw_basis* basis, double* ratios_host, int* piv_host);
+/* Subspace.project (82-89): out = Q (Q^T v); v/out device (batch vectors, stride ld) */
+int pw_basis_project(pw_basis* basis, const double* v, double* out, int batch, long long ld);
+/* Subspace.fine_on_projection (91-98): out = FQ (Q^T v) */
+int pw_basis_fine_on_projection(pw_basis* basis, const double* v, double* out, int batch,
+                                long long ld);
+/* kse_coarse (subspace.py:105-111): out = G(v - Pv) + FQ (Q^T v) */
+int pw_kse_coarse(pw_basis* basis, pw_prop* coarse, const double* v, double* out, int batch,
+                  long long ld);
+
+/* ---- sweeps: parareal_sweep / kse_sweep (parareal.py:68-138) ------------
+ * q0: device (dim).  out_states: device, n_c x dim (endpoints q_1..q_{n_c}).
+ * residuals: host, n_it entries; *n_done = iterations run (tol early exit).
+ * tol < 0 disables the early exit (reference tol=None).
+ * timings: host [coarse, fine, qr] seconds (reference Timings, parareal.py:31-47), may be NULL.
+ * out_basis (KSE only, may be NULL): receives the final subspace (caller destroys).
+ * Synchronises once per iteration only when tol >= 0 or timings != NULL. */
+int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double* q0, int n_c,
+             int n_it, double tol, double rank_tol, double* out_states, double* residuals,
+             int* n_done, double* timings, int* ranks, pw_basis** out_basis);
+
+/* ---- memory helper ------------------------------------------------------
+ * stream-ordered copy of nbytes between any host/device pointers (UVA,
+ * cudaMemcpyDefault), synchronising the context stream afterwards. */
+int pw_copy(pw_ctx* ctx, void* dst, const void* src, long long nbytes);
+
+/* ---- diagnostics --------------------------------------------------------
+ * iteration_residual (parareal.py:50-59): max_i ||a_i - b_i||_2 (host result). */
+int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long dim,
+                double* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PITWAVE_B200_H */

@@ -1,0 +1,740 @@
+// C ABI of the B200 KSE-Parareal hot path (include/pitwave_b200.h).
+//
+// Objects: a context (device, stream, cuBLAS/cuSOLVER handles), propagators
+// (PDE over a slice, or a dense test matrix), the device-resident Krylov
+// basis, and the sweep driver.  Every sweep step is enqueued on the context
+// stream from this host loop; the only host round-trips are the rank read
+// after each subspace refactorisation and (optionally) the residual for a
+// tol early exit -- the reference's own per-iteration decisions.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "pw_internal.h"
+
+using pw::Ctx;
+using pw::Error;
+
+struct pw_ctx {
+  Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PW_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return PW_ERR_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PW_ERR_STATE;
+  }
+}
+
+#define PW_BLAS(call)                                                                     \
+  do {                                                                                    \
+    cublasStatus_t s_ = (call);                                                           \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                      \
+      throw Error{PW_ERR_LIBRARY, std::string(#call) + " -> cublas status " + std::to_string((int)s_)}; \
+  } while (0)
+#define PW_SOLVER(call)                                                                   \
+  do {                                                                                    \
+    cusolverStatus_t s_ = (call);                                                         \
+    if (s_ != CUSOLVER_STATUS_SUCCESS)                                                    \
+      throw Error{PW_ERR_LIBRARY, std::string(#call) + " -> cusolver status " + std::to_string((int)s_)}; \
+  } while (0)
+
+inline cublasHandle_t blas(Ctx& c) { return static_cast<cublasHandle_t>(c.cublas); }
+inline cusolverDnHandle_t solver(Ctx& c) { return static_cast<cusolverDnHandle_t>(c.cusolver); }
+
+// Stream-ordered device buffer.
+struct DBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  double* ensure(Ctx& c, size_t count) {
+    if (count <= n && p) return p;
+    release();
+    s = c.stream;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(double), s);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw Error{PW_ERR_MEMORY, "device allocation of " + std::to_string(count * 8) +
+                                     " bytes failed: " + cudaGetErrorString(e)};
+    }
+    n = count;
+    return p;
+  }
+};
+
+struct IBuf {
+  int* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  ~IBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  int* ensure(Ctx& c, size_t count) {
+    if (count <= n && p) return p;
+    if (p) cudaFreeAsync(p, s);
+    s = c.stream;
+    PW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(int), s));
+    n = count;
+    return p;
+  }
+};
+
+void copy_cols(Ctx& c, double* dst, long long ldd, const double* src, long long lds,
+               long long rows, long long cols) {
+  if (rows <= 0 || cols <= 0 || dst == src) return;
+  if (ldd == rows && lds == rows) {
+    PW_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * rows * cols, cudaMemcpyDeviceToDevice, c.stream));
+  } else {
+    PW_CUDA(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double),
+                              rows * sizeof(double), cols, cudaMemcpyDeviceToDevice, c.stream));
+  }
+}
+
+// C(m x n) = alpha * op(A) * op(B) + beta * C, column-major
+void gemm(Ctx& c, bool ta, bool tb, long long m, long long n, long long k, double alpha,
+          const double* A, long long lda, const double* B, long long ldb, double beta, double* C,
+          long long ldc) {
+  if (m <= 0 || n <= 0) return;
+  if (k <= 0) {
+    PW_CHECK(beta == 1.0 || beta == 0.0, PW_ERR_STATE, "gemm with k=0 and beta not in {0,1}");
+    if (beta == 0.0)
+      PW_CUDA(cudaMemset2DAsync(C, ldc * sizeof(double), 0, m * sizeof(double), n, c.stream));
+    return;
+  }
+  PW_BLAS(cublasDgemm_64(blas(c), ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N,
+                         m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc));
+}
+
+}  // namespace
+
+// ============================================================ propagators
+struct pw_prop {
+  pw_ctx* ctx = nullptr;
+  int kind = 0;  // 0 = PDE, 1 = dense
+  long long dim = 0;
+  pw_pde_desc desc{};
+  pw::ExactParams ex{};
+  DBuf uf, vf;
+  bool const_vel = false;
+  pw::FusedParams fp{};
+  bool vadv = false;
+  DBuf A;  // dense
+  DBuf t1, t2, work;
+};
+
+namespace {
+
+bool use_fused(const pw_prop* P) {
+  return P->kind == 0 && P->desc.scheme == PW_SCHEME_RK3 && P->const_vel && !P->ctx->c.strict &&
+         pw::fused_supported(P->desc.nx, P->desc.ny);
+}
+
+void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long ld) {
+  Ctx& c = P->ctx->c;
+  const long long d = P->dim;
+  PW_CHECK(batch >= 0, PW_ERR_VALUE, "batch must be non-negative");
+  PW_CHECK(ld >= d, PW_ERR_VALUE, "ld must be >= state dimension");
+  if (batch == 0) return;
+  if (P->kind == 1) {
+    const double* src = in;
+    if (in == out) {
+      double* t = P->t1.ensure(c, (size_t)d * batch);
+      copy_cols(c, t, d, in, ld, d, batch);
+      src = t;
+    }
+    gemm(c, false, false, d, batch, d, 1.0, P->A.p, d, src, src == in ? ld : d, 0.0, out, ld);
+    return;
+  }
+  const pw_pde_desc& D = P->desc;
+  const int nsteps = D.nsteps;
+  if (nsteps == 0) {
+    copy_cols(c, out, ld, in, ld, d, batch);
+    return;
+  }
+  if (use_fused(P)) {
+    // ping-pong so that the last step lands in `out`; in != dst always
+    const double* src = in;
+    long long ld_src = ld;
+    if (in == out) {
+      double* t = P->t1.ensure(c, (size_t)d * batch);
+      copy_cols(c, t, d, in, ld, d, batch);
+      src = t;
+      ld_src = d;
+    }
+    double* tmp = P->t2.ensure(c, (size_t)d * batch);
+    for (int s = 0; s < nsteps; ++s) {
+      const bool to_out = ((nsteps - 1 - s) % 2) == 0;
+      double* dst = to_out ? out : tmp;
+      const long long ld_dst = to_out ? ld : d;
+      pw::FusedParams fp = P->fp;
+      fp.ld_in = ld_src;
+      fp.ld_out = ld_dst;
+      pw::launch_rk3_fused(c, fp, src, dst, batch, P->vadv);
+      src = dst;
+      ld_src = ld_dst;
+    }
+    return;
+  }
+  // reference-order kernels, in place on `out`
+  copy_cols(c, out, ld, in, ld, d, batch);
+  if (D.scheme == PW_SCHEME_RK3) {
+    double* w = P->work.ensure(c, pw::rk3_exact_work_doubles(P->ex, batch));
+    pw::launch_rk3_exact(c, P->ex, out, batch, ld, nsteps, D.h, w);
+  } else {
+    double* w = P->work.ensure(c, pw::fefb_exact_work_doubles(P->ex, batch));
+    pw::launch_fefb_exact(c, P->ex, out, batch, ld, nsteps, D.h, D.n_sound, w);
+  }
+}
+
+}  // namespace
+
+// ============================================================ Krylov basis
+struct pw_basis {
+  pw_ctx* ctx = nullptr;
+  long long dim = 0;
+  double rank_tol = 1e-10;
+  int cap = 0;
+  int m = 0;
+  int r = 0;
+  bool diff_mode = false;  // M holds F(S)-G(S) (sweep) instead of F(S) (Subspace API)
+  pw_prop* coarse = nullptr;
+  DBuf S, M, W, Q, Y;      // d x cap (S, M, W); d x r (Q, Y)
+  DBuf Rs, tau1, tau2, diag, Q2, X, cs_work, lazy_fq, lazy_img, tmp, alpha;
+  IBuf piv, info;
+  std::vector<double> diag_h;
+  std::vector<int> piv_h;
+  bool fq_valid = false, img_valid = false;
+};
+
+namespace {
+
+void basis_refactor(pw_basis* B) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const int m = B->m;
+  B->fq_valid = B->img_valid = false;
+  B->r = 0;
+  if (m == 0) return;
+  PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
+           "snapshot block d*m exceeds the 32-bit cuSOLVER geqrf/orgqr range (TSQR path not built yet)");
+  const int mr = (int)std::min<long long>(d, m);  // rows of R1
+  // 1) Householder QR of the full d x m snapshot block (cuSOLVER dgeqrf)
+  double* W = B->W.ensure(c, (size_t)d * B->cap);
+  copy_cols(c, W, d, B->S.p, d, d, m);
+  double* tau1 = B->tau1.ensure(c, m);
+  int* info = B->info.ensure(c, 1);
+  int lw1 = 0, lw2 = 0;
+  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)d, m, W, (int)d, &lw1));
+  PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), (int)d, mr, mr, W, (int)d, tau1, &lw2));
+  double* work = B->cs_work.ensure(c, (size_t)std::max(lw1, lw2));
+  PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)d, m, W, (int)d, tau1, work, std::max(lw1, lw2), info));
+  // 2) column-pivoted QR of the mr x m factor R1 (same pivots as dgeqp3 on S)
+  double* Rs = B->Rs.ensure(c, (size_t)mr * m);
+  pw::launch_extract_upper(c, W, d, mr, m, Rs);
+  int* piv = B->piv.ensure(c, m);
+  double* tau2 = B->tau2.ensure(c, m);
+  double* diag = B->diag.ensure(c, m);
+  int r = 0;
+  pw::pivoted_qr_small(c, Rs, mr, m, B->rank_tol, piv, tau2, diag, &r);
+  B->diag_h.assign(mr, 0.0);
+  B->piv_h.assign(m, 0);
+  PW_CUDA(cudaMemcpyAsync(B->diag_h.data(), diag, sizeof(double) * mr, cudaMemcpyDeviceToHost, c.stream));
+  PW_CUDA(cudaMemcpyAsync(B->piv_h.data(), piv, sizeof(int) * m, cudaMemcpyDeviceToHost, c.stream));
+  B->r = r;
+  if (r == 0) {
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  // 3) explicit Q1 (d x mr), Q = Q1 Q2[:, :r]
+  PW_SOLVER(cusolverDnDorgqr(solver(c), (int)d, mr, mr, W, (int)d, tau1, work, std::max(lw1, lw2), info));
+  double* Q2 = B->Q2.ensure(c, (size_t)mr * r);
+  pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
+  double* Q = B->Q.ensure(c, (size_t)d * r);
+  gemm(c, false, false, d, r, mr, 1.0, W, d, Q2, mr, 0.0, Q, d);
+  // 4) Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep)
+  double* X = B->X.ensure(c, (size_t)m * r);
+  pw::tri_inverse_scatter(c, Rs, mr, m, piv, r, X);
+  double* Y = B->Y.ensure(c, (size_t)d * r);
+  gemm(c, false, false, d, r, m, 1.0, B->M.p, d, X, m, 0.0, Y, d);
+  PW_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void basis_append(pw_basis* B, const double* states, long long lds, const double* m_cols,
+                  long long ldm, int p) {
+  Ctx& c = B->ctx->c;
+  PW_CHECK(p >= 0, PW_ERR_VALUE, "negative column count");
+  PW_CHECK(B->m + p <= B->cap, PW_ERR_VALUE,
+           "subspace capacity exceeded (" + std::to_string(B->m + p) + " > " + std::to_string(B->cap) + ")");
+  const long long d = B->dim;
+  double* S = B->S.ensure(c, (size_t)d * B->cap);
+  double* M = B->M.ensure(c, (size_t)d * B->cap);
+  copy_cols(c, S + (size_t)B->m * d, d, states, lds, d, p);
+  copy_cols(c, M + (size_t)B->m * d, d, m_cols, ldm, d, p);
+  B->m += p;
+}
+
+// alpha (r x batch) = Q^T v
+double* basis_coeffs(pw_basis* B, const double* v, int batch, long long ld) {
+  Ctx& c = B->ctx->c;
+  double* a = B->alpha.ensure(c, (size_t)std::max(B->r, 1) * batch);
+  gemm(c, true, false, B->r, batch, B->dim, 1.0, B->Q.p, B->dim, v, ld, 0.0, a, std::max(B->r, 1));
+  return a;
+}
+
+const double* basis_fq(pw_basis* B) {
+  if (!B->diff_mode) return B->Y.p;
+  Ctx& c = B->ctx->c;
+  if (!B->fq_valid && B->r > 0) {
+    // FQ = D + G(Q)   (G linear: D = (F - G)(S) R^-1 and Q = S R^-1)
+    double* fq = B->lazy_fq.ensure(c, (size_t)B->dim * B->r);
+    prop_apply(B->coarse, B->Q.p, fq, B->r, B->dim);
+    pw::launch_axpby_cols(c, fq, fq, B->Y.p, 1.0, 1.0, (size_t)B->dim * B->r);
+    B->fq_valid = true;
+  }
+  return B->lazy_fq.p;
+}
+
+const double* basis_images(pw_basis* B) {
+  if (!B->diff_mode) return B->M.p;
+  Ctx& c = B->ctx->c;
+  if (!B->img_valid && B->m > 0) {
+    double* im = B->lazy_img.ensure(c, (size_t)B->dim * B->m);
+    prop_apply(B->coarse, B->S.p, im, B->m, B->dim);
+    pw::launch_axpby_cols(c, im, im, B->M.p, 1.0, 1.0, (size_t)B->dim * B->m);
+    B->img_valid = true;
+  }
+  return B->lazy_img.p;
+}
+
+pw_basis* basis_new(pw_ctx* ctx, long long dim, double rank_tol, int capacity) {
+  PW_CHECK(dim >= 1, PW_ERR_VALUE, "dimension must be positive");
+  PW_CHECK(capacity >= 1, PW_ERR_VALUE, "capacity must be positive");
+  auto* B = new pw_basis();
+  B->ctx = ctx;
+  B->dim = dim;
+  B->rank_tol = rank_tol;
+  B->cap = capacity;
+  return B;
+}
+
+}  // namespace
+
+// ============================================================ C ABI
+extern "C" {
+
+const char* pw_last_error(void) { return g_last_error.c_str(); }
+int pw_version(void) { return 100; }
+
+int pw_ctx_create(int device, void* stream, pw_ctx** out) {
+  return guarded([&] {
+    PW_CHECK(out != nullptr, PW_ERR_VALUE, "out is NULL");
+    int ndev = 0;
+    PW_CUDA(cudaGetDeviceCount(&ndev));
+    PW_CHECK(device >= 0 && device < ndev, PW_ERR_VALUE, "no such CUDA device");
+    PW_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    PW_CUDA(cudaGetDeviceProperties(&prop, device));
+    PW_CHECK(prop.major == 10, PW_ERR_CUDA,
+             std::string("this library is built for sm_100a (B200); device is ") + prop.name);
+    auto ctx = std::make_unique<pw_ctx>();
+    ctx->c.device = device;
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    ctx->c.num_sms = prop.multiProcessorCount;
+    cublasHandle_t h;
+    PW_BLAS(cublasCreate(&h));
+    PW_BLAS(cublasSetStream(h, ctx->c.stream));
+    PW_BLAS(cublasSetMathMode(h, CUBLAS_DEFAULT_MATH));
+    ctx->c.cublas = h;
+    cusolverDnHandle_t sh;
+    PW_SOLVER(cusolverDnCreate(&sh));
+    PW_SOLVER(cusolverDnSetStream(sh, ctx->c.stream));
+    ctx->c.cusolver = sh;
+    *out = ctx.release();
+  });
+}
+
+int pw_ctx_destroy(pw_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.red) cudaFree(ctx->c.red);
+    if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
+    if (ctx->c.cusolver) cusolverDnDestroy(solver(ctx->c));
+    delete ctx;
+  });
+}
+
+int pw_ctx_set_stream(pw_ctx* ctx, void* stream) {
+  return guarded([&] {
+    PW_CHECK(ctx, PW_ERR_VALUE, "ctx is NULL");
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    PW_BLAS(cublasSetStream(blas(ctx->c), ctx->c.stream));
+    PW_SOLVER(cusolverDnSetStream(solver(ctx->c), ctx->c.stream));
+  });
+}
+
+int pw_ctx_synchronize(pw_ctx* ctx) {
+  return guarded([&] { PW_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+int pw_ctx_set_strict(pw_ctx* ctx, int strict) {
+  return guarded([&] { ctx->c.strict = strict != 0; });
+}
+
+long long pw_ctx_launch_count(pw_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+int pw_prop_create_pde(pw_ctx* ctx, const pw_pde_desc* desc, pw_prop** out) {
+  return guarded([&] {
+    PW_CHECK(ctx && desc && out, PW_ERR_VALUE, "NULL argument");
+    const pw_pde_desc& D = *desc;
+    PW_CHECK(D.scheme == PW_SCHEME_RK3 || D.scheme == PW_SCHEME_SPLIT_FE_FB, PW_ERR_VALUE,
+             "scheme must be rk3 or split_fe_fb");
+    PW_CHECK(D.nx >= 8 && D.ny >= 8, PW_ERR_VALUE, "grid too small (need at least 8 cells per direction)");
+    PW_CHECK(D.order >= 1 && D.order <= 6, PW_ERR_VALUE, "flux order must be in 1..6");
+    PW_CHECK(D.nsteps >= 0, PW_ERR_VALUE, "nsteps must be non-negative");
+    PW_CHECK(D.scheme == PW_SCHEME_RK3 || D.n_sound >= 1, PW_ERR_VALUE, "n_sound must be at least 1");
+    PW_CHECK(D.h > 0 && D.dx > 0 && D.dy > 0 && D.cs > 0, PW_ERR_VALUE, "non-positive step/spacing/sound speed");
+    Ctx& c = ctx->c;
+    auto P = std::make_unique<pw_prop>();
+    P->ctx = ctx;
+    P->kind = 0;
+    P->desc = D;
+    P->desc.uf = P->desc.vf = nullptr;
+    P->dim = 3LL * D.nx * D.ny;
+    const size_t n = (size_t)D.nx * D.ny;
+    std::vector<double> hu(n), hv(n);
+    if (D.const_velocity) {
+      std::fill(hu.begin(), hu.end(), D.vel_u);
+      std::fill(hv.begin(), hv.end(), D.vel_v);
+    } else {
+      PW_CHECK(D.uf && D.vf, PW_ERR_VALUE, "face velocity arrays required");
+      std::memcpy(hu.data(), D.uf, n * sizeof(double));
+      std::memcpy(hv.data(), D.vf, n * sizeof(double));
+    }
+    // a velocity field that is constant on every face is handled by the folded kernel
+    bool cst = true;
+    for (size_t k = 1; k < n && cst; ++k) cst = (hu[k] == hu[0] && hv[k] == hv[0]);
+    P->const_vel = cst;
+    double* du = P->uf.ensure(c, n);
+    double* dv = P->vf.ensure(c, n);
+    PW_CUDA(cudaMemcpyAsync(du, hu.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    PW_CUDA(cudaMemcpyAsync(dv, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+    P->ex = pw::ExactParams{D.nx, D.ny, D.order, D.dx, D.dy, D.cs, D.a1, D.a2, du, dv};
+    if (D.scheme == PW_SCHEME_RK3 && cst) {
+      pw::make_fused_params(P->fp, D.nx, D.ny, D.dx, D.dy, D.cs, D.order, hu[0], hv[0], D.a1,
+                            D.a2, D.h);
+      P->vadv = hv[0] != 0.0;
+    }
+    *out = P.release();
+  });
+}
+
+int pw_prop_create_dense(pw_ctx* ctx, const double* a, int d, pw_prop** out) {
+  return guarded([&] {
+    PW_CHECK(ctx && a && out, PW_ERR_VALUE, "NULL argument");
+    PW_CHECK(d >= 1, PW_ERR_VALUE, "dimension must be positive");
+    auto P = std::make_unique<pw_prop>();
+    P->ctx = ctx;
+    P->kind = 1;
+    P->dim = d;
+    double* A = P->A.ensure(ctx->c, (size_t)d * d);
+    PW_CUDA(cudaMemcpyAsync(A, a, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, ctx->c.stream));
+    *out = P.release();
+  });
+}
+
+int pw_prop_destroy(pw_prop* prop) {
+  return guarded([&] {
+    if (!prop) return;
+    cudaStreamSynchronize(prop->ctx->c.stream);
+    delete prop;
+  });
+}
+
+long long pw_prop_dim(const pw_prop* prop) { return prop ? prop->dim : -1; }
+
+int pw_prop_apply(pw_prop* prop, const double* in, double* out, int batch, long long ld) {
+  return guarded([&] {
+    PW_CHECK(prop && in && out, PW_ERR_VALUE, "NULL argument");
+    prop_apply(prop, in, out, batch, ld);
+  });
+}
+
+int pw_basis_create(pw_ctx* ctx, long long dim, double rank_tol, int capacity, pw_basis** out) {
+  return guarded([&] {
+    PW_CHECK(ctx && out, PW_ERR_VALUE, "NULL argument");
+    *out = basis_new(ctx, dim, rank_tol, capacity);
+  });
+}
+
+int pw_basis_destroy(pw_basis* basis) {
+  return guarded([&] {
+    if (!basis) return;
+    cudaStreamSynchronize(basis->ctx->c.stream);
+    delete basis;
+  });
+}
+
+int pw_basis_update(pw_basis* basis, const double* states, const double* images, int p) {
+  return guarded([&] {
+    PW_CHECK(basis, PW_ERR_VALUE, "NULL basis");
+    PW_CHECK(!basis->diff_mode, PW_ERR_STATE, "sweep-internal subspace cannot be updated with images");
+    PW_CHECK(p == 0 || (states && images), PW_ERR_VALUE, "NULL snapshot/image pointer");
+    basis_append(basis, states, basis->dim, images, basis->dim, p);
+    basis_refactor(basis);
+  });
+}
+
+int pw_basis_rank(const pw_basis* basis) { return basis ? basis->r : -1; }
+int pw_basis_ncols(const pw_basis* basis) { return basis ? basis->m : -1; }
+
+int pw_basis_views(const pw_basis* basis, const double** q, const double** fq,
+                   const double** snapshots, const double** images) {
+  return guarded([&] {
+    PW_CHECK(basis, PW_ERR_VALUE, "NULL basis");
+    pw_basis* B = const_cast<pw_basis*>(basis);
+    if (q) *q = B->Q.p;
+    if (fq) *fq = B->r > 0 ? basis_fq(B) : nullptr;
+    if (snapshots) *snapshots = B->S.p;
+    if (images) *images = B->m > 0 ? basis_images(B) : nullptr;
+    PW_CUDA(cudaStreamSynchronize(B->ctx->c.stream));
+  });
+}
+
+int pw_basis_diag(const pw_basis* basis, double* ratios_host, int* piv_host) {
+  return guarded([&] {
+    PW_CHECK(basis, PW_ERR_VALUE, "NULL basis");
+    const int nd = (int)basis->diag_h.size();
+    for (int k = 0; k < nd && ratios_host; ++k)
+      ratios_host[k] = basis->diag_h[0] != 0.0 ? basis->diag_h[k] / basis->diag_h[0] : 0.0;
+    for (int k = 0; k < (int)basis->piv_h.size() && piv_host; ++k) piv_host[k] = basis->piv_h[k];
+  });
+}
+
+int pw_basis_project(pw_basis* basis, const double* v, double* out, int batch, long long ld) {
+  return guarded([&] {
+    PW_CHECK(basis && v && out, PW_ERR_VALUE, "NULL argument");
+    Ctx& c = basis->ctx->c;
+    if (basis->r == 0) {
+      PW_CUDA(cudaMemset2DAsync(out, ld * sizeof(double), 0, basis->dim * sizeof(double), batch, c.stream));
+      return;
+    }
+    double* a = basis_coeffs(basis, v, batch, ld);
+    gemm(c, false, false, basis->dim, batch, basis->r, 1.0, basis->Q.p, basis->dim, a, basis->r,
+         0.0, out, ld);
+  });
+}
+
+int pw_basis_fine_on_projection(pw_basis* basis, const double* v, double* out, int batch,
+                                long long ld) {
+  return guarded([&] {
+    PW_CHECK(basis && v && out, PW_ERR_VALUE, "NULL argument");
+    Ctx& c = basis->ctx->c;
+    if (basis->r == 0) {
+      PW_CUDA(cudaMemset2DAsync(out, ld * sizeof(double), 0, basis->dim * sizeof(double), batch, c.stream));
+      return;
+    }
+    const double* fq = basis_fq(basis);
+    double* a = basis_coeffs(basis, v, batch, ld);
+    gemm(c, false, false, basis->dim, batch, basis->r, 1.0, fq, basis->dim, a, basis->r, 0.0, out, ld);
+  });
+}
+
+int pw_kse_coarse(pw_basis* basis, pw_prop* coarse, const double* v, double* out, int batch,
+                  long long ld) {
+  return guarded([&] {
+    PW_CHECK(basis && coarse && v && out, PW_ERR_VALUE, "NULL argument");
+    PW_CHECK(coarse->dim == basis->dim, PW_ERR_VALUE, "coarse propagator dimension mismatch");
+    Ctx& c = basis->ctx->c;
+    const long long d = basis->dim;
+    if (basis->r == 0) {
+      prop_apply(coarse, v, out, batch, ld);
+      return;
+    }
+    // K(q) = G(q - Q Q^T q) + FQ Q^T q    (subspace.py:105-111)
+    const double* fq = basis_fq(basis);
+    double* a = basis_coeffs(basis, v, batch, ld);
+    double* w = basis->tmp.ensure(c, (size_t)d * batch);
+    copy_cols(c, w, d, v, ld, d, batch);
+    gemm(c, false, false, d, batch, basis->r, -1.0, basis->Q.p, d, a, basis->r, 1.0, w, d);
+    prop_apply(coarse, w, out, batch, ld);
+    // out is (d x batch) with stride ld; add FQ a
+    gemm(c, false, false, d, batch, basis->r, 1.0, fq, d, a, basis->r, 1.0, out, ld);
+  });
+}
+
+int pw_copy(pw_ctx* ctx, void* dst, const void* src, long long nbytes) {
+  return guarded([&] {
+    PW_CHECK(ctx && dst && src && nbytes >= 0, PW_ERR_VALUE, "bad pw_copy arguments");
+    if (nbytes == 0) return;
+    PW_CUDA(cudaMemcpyAsync(dst, src, (size_t)nbytes, cudaMemcpyDefault, ctx->c.stream));
+    PW_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long dim,
+                double* out_host) {
+  return guarded([&] {
+    PW_CHECK(ctx && out_host, PW_ERR_VALUE, "NULL argument");
+    Ctx& c = ctx->c;
+    DBuf scr;
+    double* s = scr.ensure(c, pw::residual_scratch_doubles(n, dim) + 1);
+    pw::launch_residual(c, a, dim, b, dim, n, dim, s + 1, s);
+    PW_CUDA(cudaMemcpyAsync(out_host, s, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// ------------------------------------------------------------ the sweep
+int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double* q0, int n_c,
+             int n_it, double tol, double rank_tol, double* out_states, double* residuals,
+             int* n_done, double* timings, int* ranks, pw_basis** out_basis) {
+  return guarded([&] {
+    PW_CHECK(ctx && fine && coarse && q0 && out_states && residuals && n_done, PW_ERR_VALUE,
+             "NULL argument");
+    PW_CHECK(mode == PW_MODE_ORIGINAL || mode == PW_MODE_KSE, PW_ERR_VALUE, "unknown mode");
+    PW_CHECK(n_c >= 1 && n_it >= 1, PW_ERR_VALUE, "n_c and n_it must be at least 1");
+    PW_CHECK(fine->dim == coarse->dim, PW_ERR_VALUE, "fine and coarse propagators must share the grid");
+    Ctx& c = ctx->c;
+    const long long d = fine->dim;
+    const bool kse = mode == PW_MODE_KSE;
+    // buffers (column-major, ld = d)
+    DBuf bQK, bQN, bPred, bGK, bGN, bRes, bScr, bAlpha, bPart;
+    double* QK = bQK.ensure(c, (size_t)d * (n_c + 1));
+    double* QN = bQN.ensure(c, (size_t)d * (n_c + 1));
+    double* PRED = bPred.ensure(c, (size_t)d * n_c);
+    double* GK = bGK.ensure(c, (size_t)d * n_c);
+    double* GN = bGN.ensure(c, (size_t)d * n_c);
+    double* res_dev = bRes.ensure(c, n_it);
+    double* scr = bScr.ensure(c, pw::residual_scratch_doubles(n_c, d));
+    std::unique_ptr<pw_basis> B;
+    if (kse) {
+      B.reset(basis_new(ctx, d, rank_tol, n_c * n_it));
+      B->diff_mode = true;
+      B->coarse = coarse;
+    }
+    cudaEvent_t ev[4];
+    const bool timed = timings != nullptr;
+    double t_coarse = 0, t_fine = 0, t_qr = 0;
+    if (timed) for (auto& e : ev) PW_CUDA(cudaEventCreate(&e));
+    auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
+      float ms = 0;
+      PW_CUDA(cudaEventSynchronize(b));
+      PW_CUDA(cudaEventElapsedTime(&ms, a, b));
+      return ms * 1e-3;
+    };
+
+    // serial coarse initialisation qk[i+1] = G(qk[i])  (parareal.py:112-116)
+    if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
+    copy_cols(c, QK, d, q0, d, d, 1);
+    for (int i = 0; i < n_c; ++i) prop_apply(coarse, QK + (size_t)i * d, QK + (size_t)(i + 1) * d, 1, d);
+    copy_cols(c, GK, d, QK + d, d, d, n_c);  // G(qk[i]) for the first correction
+    if (timed) {
+      PW_CUDA(cudaEventRecord(ev[1], c.stream));
+      t_coarse += elapsed(ev[0], ev[1]);
+    }
+    int k_done = 0;
+    for (int k = 0; k < n_it; ++k) {
+      if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
+      // fine predictor over all slices at once (_fine_all, parareal.py:62-65)
+      prop_apply(fine, QK, PRED, n_c, d);
+      if (timed) PW_CUDA(cudaEventRecord(ev[1], c.stream));
+      // c_i = F(qk[i]) - G(qk[i])  [- D Q^T qk[i] in KSE mode]
+      pw::launch_axpby_cols(c, PRED, PRED, GK, 1.0, -1.0, (size_t)d * n_c);
+      int r = 0;
+      double* alpha = nullptr;
+      double* alpha_next = nullptr;
+      if (kse) {
+        basis_append(B.get(), QK, d, PRED, d, n_c);
+        basis_refactor(B.get());
+        r = B->r;
+        if (ranks) ranks[k] = r;
+        if (r > 0) {
+          double* ab = bAlpha.ensure(c, (size_t)r * (n_c + 2));
+          gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
+          gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
+          alpha = ab;                             // column 0 = Q^T q0
+          alpha_next = ab + (size_t)r * n_c;      // scratch pair after the block
+        }
+      }
+      if (timed) PW_CUDA(cudaEventRecord(ev[2], c.stream));
+      // serial correction sweep (parareal.py:128-132)
+      copy_cols(c, QN, d, q0, d, d, 1);
+      double* part = bPart.ensure(c, pw::combine_part_doubles(d, r));
+      double* a_cur = alpha;
+      double* a_buf[2] = {alpha_next, alpha_next ? alpha_next + r : nullptr};
+      for (int i = 0; i < n_c; ++i) {
+        prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
+        double* a_nxt = (r > 0) ? a_buf[i % 2] : nullptr;
+        pw::launch_combine_gemv(c, GN + (size_t)i * d, B ? B->Y.p : nullptr, PRED + (size_t)i * d,
+                                a_cur, B ? B->Q.p : nullptr, r, d, QN + (size_t)(i + 1) * d, a_nxt,
+                                part);
+        a_cur = a_nxt;
+      }
+      pw::launch_residual(c, QK + d, d, QN + d, d, n_c, d, scr, res_dev + k);
+      if (timed) {
+        PW_CUDA(cudaEventRecord(ev[3], c.stream));
+        t_fine += elapsed(ev[0], ev[1]);
+        t_qr += elapsed(ev[1], ev[2]);
+        t_coarse += elapsed(ev[2], ev[3]);
+      }
+      std::swap(bQK.p, bQN.p);
+      std::swap(bQK.n, bQN.n);
+      std::swap(bGK.p, bGN.p);
+      std::swap(bGK.n, bGN.n);
+      QK = bQK.p;
+      QN = bQN.p;
+      GK = bGK.p;
+      GN = bGN.p;
+      k_done = k + 1;
+      if (tol >= 0.0) {
+        double rk = 0;
+        PW_CUDA(cudaMemcpyAsync(&rk, res_dev + k, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        PW_CUDA(cudaStreamSynchronize(c.stream));
+        if (rk <= tol) break;
+      }
+    }
+    copy_cols(c, out_states, d, QK + d, d, d, n_c);
+    PW_CUDA(cudaMemcpyAsync(residuals, res_dev, sizeof(double) * k_done, cudaMemcpyDeviceToHost, c.stream));
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+    *n_done = k_done;
+    if (timed) {
+      timings[0] = t_coarse;
+      timings[1] = t_fine;
+      timings[2] = t_qr;
+      for (auto& e : ev) cudaEventDestroy(e);
+    }
+    if (out_basis) *out_basis = B.release();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,505 @@
+// Krylov-subspace linear algebra for the KSE correction (sm_100a, fp64).
+//
+//  * pivoted_qr_small   -- column-pivoted Householder QR of the m x m triangular
+//                          factor R1 of the snapshot block (one cooperative
+//                          launch, 2 grid barriers per column).  Pivoted QR of
+//                          R1 has the pivots of dgeqp3 on the snapshots
+//                          themselves (subspace.py:67-68), see DESIGN.md.
+//  * form_q2            -- explicit Q2[:, :r] from the reflectors (dorgqr role)
+//  * tri_inverse_scatter-- scatter(R11^-1) of subspace.py:76-78
+//  * combine_gemv       -- the serial correction step of the KSE sweep,
+//                          qn[i+1] = G(qn[i]) + D alpha_i + c_i fused with the
+//                          next projection coefficients alpha_{i+1} = Q^T qn[i+1]
+//                          (one HBM pass over D and Q: 2 r d 8 bytes).
+//  * residual           -- iteration_residual (parareal.py:50-59)
+#include <cooperative_groups.h>
+
+#include "pw_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace pw {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+  return v;
+}
+
+// ---------------------------------------------------------------- small pivoted QR
+constexpr int kQrThreads = 256;
+constexpr int kQrWarps = kQrThreads / 32;
+
+// A: mr x m column-major (lda = mr), mr = min(d, m) rows of R1.  Steps j < min(mr, m).
+__global__ void __launch_bounds__(kQrThreads) pqr_kernel(double* A, int mr, int m, int* piv,
+                                                         double* tau, double* norms, double* diag) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned done[64];  // m <= 2048
+  __shared__ double red_v[kQrWarps];
+  __shared__ int red_i[kQrWarps];
+  __shared__ int s_p;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gwarp = blockIdx.x * kQrWarps + warp;
+  const int nwarps = gridDim.x * kQrWarps;
+  const int steps = mr < m ? mr : m;
+  for (int k = threadIdx.x; k < 64; k += blockDim.x) done[k] = 0u;
+  // initial column norms
+  for (int c = gwarp; c < m; c += nwarps) {
+    const double* col = A + (size_t)c * mr;
+    double s = 0.0;
+    for (int i = lane; i < mr; i += 32) s = fma(col[i], col[i], s);
+    s = warp_sum(s);
+    if (lane == 0) norms[c] = sqrt(s);
+  }
+  grid.sync();
+  for (int j = 0; j < steps; ++j) {
+    // pivot: max remaining norm, lowest index on ties (idamax semantics)
+    double best = -1.0;
+    int bi = m;
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      if (done[c >> 5] & (1u << (c & 31))) continue;
+      const double v = norms[c];
+      if (v > best || (v == best && c < bi)) { best = v; bi = c; }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const double ov = __shfl_xor_sync(FULL, best, off);
+      const int oi = __shfl_xor_sync(FULL, bi, off);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[warp] = best; red_i[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = red_v[0];
+      int bidx = red_i[0];
+      for (int w = 1; w < kQrWarps; ++w)
+        if (red_v[w] > b || (red_v[w] == b && red_i[w] < bidx)) { b = red_v[w]; bidx = red_i[w]; }
+      s_p = bidx;
+      done[bidx >> 5] |= (1u << (bidx & 31));
+    }
+    __syncthreads();
+    const int p = s_p;
+    // Householder reflector of column p, rows j..mr-1 (dlarfg)
+    if (gwarp == p % nwarps) {
+      double* col = A + (size_t)p * mr;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < mr; i += 32) s = fma(col[i], col[i], s);
+      s = warp_sum(s);
+      const double alpha = col[j];
+      double t = 0.0, beta = alpha;
+      if (s != 0.0) {
+        const double xnorm = sqrt(s);
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        t = (beta - alpha) / beta;
+        const double scal = 1.0 / (alpha - beta);
+        for (int i = j + 1 + lane; i < mr; i += 32) col[i] *= scal;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        col[j] = beta;
+        tau[j] = t;
+        piv[j] = p;
+        diag[j] = fabs(beta);
+      }
+    }
+    grid.sync();
+    // apply H_j to the remaining columns; recompute their trailing norms
+    const double t = tau[j];
+    const double* v = A + (size_t)p * mr;
+    for (int c = gwarp; c < m; c += nwarps) {
+      if (done[c >> 5] & (1u << (c & 31))) continue;
+      double* col = A + (size_t)c * mr;
+      double w = 0.0;
+      for (int i = j + 1 + lane; i < mr; i += 32) w = fma(v[i], col[i], w);
+      w = warp_sum(w) + col[j];
+      const double tw = t * w;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < mr; i += 32) {
+        const double x = col[i] - tw * v[i];
+        col[i] = x;
+        s = fma(x, x, s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        col[j] -= tw;
+        norms[c] = sqrt(s);
+      }
+    }
+    grid.sync();
+  }
+  // columns never pivoted (m > mr): record them after the pivoted ones
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int k = steps;
+    for (int c = 0; c < m && k < m; ++c)
+      if (!(done[c >> 5] & (1u << (c & 31)))) piv[k++] = c;
+  }
+}
+
+// Q2[:, c] = H_0 ... H_c e_c  (c < r), one warp per column, x staged in smem
+constexpr int kQ2Warps = 4;
+__global__ void __launch_bounds__(kQ2Warps * 32) form_q2_kernel(const double* A, int mr,
+                                                                 const int* piv, const double* tau,
+                                                                 int r, double* Q2) {
+  extern __shared__ double xs[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * kQ2Warps + warp;
+  if (c >= r) return;
+  double* x = xs + (size_t)warp * mr;
+  for (int i = lane; i < mr; i += 32) x[i] = (i == c) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int j = c; j >= 0; --j) {
+    const double* v = A + (size_t)piv[j] * mr;
+    double w = 0.0;
+    for (int i = j + 1 + lane; i < mr; i += 32) w = fma(v[i], x[i], w);
+    w = warp_sum(w) + x[j];
+    const double tw = tau[j] * w;
+    __syncwarp();
+    for (int i = j + 1 + lane; i < mr; i += 32) x[i] -= tw * v[i];
+    if (lane == 0) x[j] -= tw;
+    __syncwarp();
+  }
+  for (int i = lane; i < mr; i += 32) Q2[(size_t)c * mr + i] = x[i];
+}
+
+// X[piv[k], c] = (R11^-1)[k, c]; R11[i][k] = A[i, piv[k]] (i <= k < r).
+// Column-oriented back substitution, one warp per column, b staged in smem.
+__global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A, int mr, int m,
+                                                                 const int* piv, int r, double* X) {
+  extern __shared__ double bs[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * kQ2Warps + warp;
+  if (c >= r) return;
+  double* b = bs + (size_t)warp * mr;
+  for (int i = lane; i <= c; i += 32) b[i] = (i == c) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int l = c; l >= 0; --l) {
+    const double* col = A + (size_t)piv[l] * mr;  // R11[:, l]
+    const double yl = b[l] / col[l];
+    __syncwarp();
+    for (int i = lane; i < l; i += 32) b[i] -= yl * col[i];
+    if (lane == 0) b[l] = yl;
+    __syncwarp();
+  }
+  for (int k = lane; k <= c; k += 32) X[(size_t)c * m + piv[k]] = b[k];
+}
+
+// ---------------------------------------------------------------- fused serial step
+constexpr int kCgThreads = 256;
+constexpr int kCgRpt = 8;  // rows per thread
+constexpr int kCgRows = kCgThreads * kCgRpt;
+
+// 32 per-lane partials -> lane L holds the warp total of column L
+__device__ __forceinline__ double transpose_reduce32(double (&acc)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = upper ? acc[i] : acc[i + off];
+      const double keep = upper ? acc[i + off] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(FULL, send, off);
+    }
+  }
+  return acc[0];
+}
+
+// part[blk][k] = sum over this block's rows of Q[row, k] * y[row]
+__device__ __forceinline__ void block_qty(const double* __restrict__ Q, int r, long long d,
+                                          long long row0, const double (&y)[kCgRpt],
+                                          double* __restrict__ part, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kCgThreads / 32;
+  for (int k0 = 0; k0 < r; k0 += 32) {
+    double acc[32];
+#pragma unroll
+    for (int kk = 0; kk < 32; ++kk) acc[kk] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kCgRpt; ++s) {
+      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      if (row < d) {
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk)
+          if (k0 + kk < r) acc[kk] = fma(__ldg(Q + (long long)(k0 + kk) * d + row), y[s], acc[kk]);
+      }
+    }
+    const double tot = transpose_reduce32(acc);
+    red[warp * 32 + lane] = tot;
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += red[w * 32 + lane];
+      if (k0 + lane < r) part[(long long)blockIdx.x * r + k0 + lane] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kCgThreads) combine_gemv_kernel(
+    const double* __restrict__ g, const double* __restrict__ D, const double* __restrict__ cvec,
+    const double* __restrict__ alpha, const double* __restrict__ Q, int r, long long d,
+    double* __restrict__ y_out, double* __restrict__ part) {
+  extern __shared__ double sh[];
+  double* a_s = sh;            // r
+  double* red = sh + r;        // 8 warps x 32
+  for (int k = threadIdx.x; k < r; k += blockDim.x) a_s[k] = alpha[k];
+  __syncthreads();
+  const long long row0 = (long long)blockIdx.x * kCgRows;
+  double y[kCgRpt];
+#pragma unroll
+  for (int s = 0; s < kCgRpt; ++s) {
+    const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+    y[s] = row < d ? g[row] + cvec[row] : 0.0;
+  }
+  // y += D alpha   (column-major D: coalesced along rows for every k)
+  for (int k = 0; k < r; ++k) {
+    const double ak = a_s[k];
+    const double* Dk = D + (long long)k * d;
+#pragma unroll
+    for (int s = 0; s < kCgRpt; ++s) {
+      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      if (row < d) y[s] = fma(__ldg(Dk + row), ak, y[s]);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < kCgRpt; ++s) {
+    const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+    if (row < d) y_out[row] = y[s];
+  }
+  if (r > 0) block_qty(Q, r, d, row0, y, part, red);
+}
+
+__global__ void __launch_bounds__(kCgThreads) project_partial_kernel(
+    const double* __restrict__ Q, int r, long long d, const double* __restrict__ v,
+    double* __restrict__ part) {
+  __shared__ double red[kCgThreads];
+  const long long row0 = (long long)blockIdx.x * kCgRows;
+  double y[kCgRpt];
+#pragma unroll
+  for (int s = 0; s < kCgRpt; ++s) {
+    const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+    y[s] = row < d ? v[row] : 0.0;
+  }
+  block_qty(Q, r, d, row0, y, part, red);
+}
+
+// alpha[k] = sum_b part[b][k]  (fixed order: deterministic)
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int nblk, int r,
+                                    double* __restrict__ alpha) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= r) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[(long long)b * r + k];
+  alpha[k] = s;
+}
+
+// ---------------------------------------------------------------- elementwise / residual
+__global__ void axpby_kernel(double* __restrict__ y, const double* __restrict__ a,
+                             const double* __restrict__ b, double alpha, double beta, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = alpha * a[i] + beta * b[i];
+}
+
+constexpr int kResThreads = 256;
+__global__ void sqdiff_partial_kernel(const double* __restrict__ a, long long lda,
+                                      const double* __restrict__ b, long long ldb, long long nrows,
+                                      int chunks, double* __restrict__ part) {
+  __shared__ double red[kResThreads / 32];
+  const int col = blockIdx.y;
+  const long long per = (nrows + chunks - 1) / chunks;
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = lo + per < nrows ? lo + per : nrows;
+  const double* ac = a + col * lda;
+  const double* bc = b + col * ldb;
+  double s = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double df = bc[i] - ac[i];
+    s = fma(df, df, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kResThreads / 32; ++w) t += red[w];
+    part[(long long)col * chunks + blockIdx.x] = t;
+  }
+}
+
+__global__ void colmax_kernel(const double* __restrict__ part, int ncols, int chunks,
+                              double* __restrict__ out) {
+  __shared__ double red[256];
+  double best = 0.0;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < chunks; ++k) s += part[(long long)c * chunks + k];
+    const double nrm = sqrt(s);
+    best = fmax(best, nrm);  // fmax ignores NaN like max(r, nan)? see api docs
+  }
+  red[threadIdx.x] = best;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+__global__ void extract_upper_kernel(const double* __restrict__ W, long long ldw, int mr, int m,
+                                     double* __restrict__ R) {
+  const long long total = (long long)mr * m;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(idx / mr), row = (int)(idx % mr);
+    R[idx] = row <= col ? W[(long long)col * ldw + row] : 0.0;
+  }
+}
+
+int g_pqr_blocks_per_sm = -1;
+
+}  // namespace
+
+void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,
+                       double beta, size_t n) {
+  if (n == 0) return;
+  int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)c.num_sms * 8);
+  axpby_kernel<<<blocks, 256, 0, c.stream>>>(y, a, b, alpha, beta, n);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+static void ensure_red(Ctx& c, size_t n) {
+  if (c.red_cap >= n) return;
+  if (c.red) PW_CUDA(cudaFreeAsync(c.red, c.stream));
+  size_t cap = std::max<size_t>(n, 1 << 16);
+  PW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c.red), cap * sizeof(double), c.stream));
+  c.red_cap = cap;
+}
+
+void launch_extract_upper(Ctx& c, const double* W, long long ldw, int mr, int m, double* R) {
+  const long long total = (long long)mr * m;
+  int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c.num_sms * 8));
+  extract_upper_kernel<<<blocks, 256, 0, c.stream>>>(W, ldw, mr, m, R);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+size_t residual_scratch_doubles(int ncols, long long nrows) {
+  int chunks = (int)std::max<long long>(1, std::min<long long>((nrows + 8191) / 8192, 64));
+  return (size_t)ncols * chunks;
+}
+
+void launch_residual(Ctx& c, const double* a, long long lda, const double* b, long long ldb,
+                     int ncols, long long nrows, double* scratch, double* out_dev) {
+  if (ncols <= 0) {
+    PW_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), c.stream));
+    return;
+  }
+  int chunks = (int)std::max<long long>(1, std::min<long long>((nrows + 8191) / 8192, 64));
+  sqdiff_partial_kernel<<<dim3(chunks, ncols), kResThreads, 0, c.stream>>>(a, lda, b, ldb, nrows,
+                                                                          chunks, scratch);
+  colmax_kernel<<<1, 256, 0, c.stream>>>(scratch, ncols, chunks, out_dev);
+  c.launches += 2;
+  PW_LAUNCH_CHECK();
+}
+
+int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv_dev,
+                     double* tau_dev, double* diag_dev, int* rank_host) {
+  PW_CHECK(m >= 1 && m <= 2048, PW_ERR_VALUE, "pivoted QR supports 1..2048 snapshot columns");
+  const int steps = std::min(mr, m);
+  if (g_pqr_blocks_per_sm < 0) {
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_pqr_blocks_per_sm, pqr_kernel,
+                                                          kQrThreads, 0));
+    if (g_pqr_blocks_per_sm < 1) g_pqr_blocks_per_sm = 1;
+  }
+  ensure_red(c, (size_t)m);
+  double* norms = c.red;
+  int want = (m + kQrWarps - 1) / kQrWarps;
+  int blocks = std::max(1, std::min(want, c.num_sms * std::min(g_pqr_blocks_per_sm, 1)));
+  void* args[] = {&R, &mr, &m, &piv_dev, &tau_dev, &norms, &diag_dev};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)pqr_kernel, dim3(blocks), dim3(kQrThreads), args, 0,
+                                      c.stream));
+  c.launches += 1;
+  // rank = #{ |R_jj| > tol |R_11| } (subspace.py:69-72): host side from the m diagonal values
+  std::vector<double> dg(steps);
+  PW_CUDA(cudaMemcpyAsync(dg.data(), diag_dev, sizeof(double) * steps, cudaMemcpyDeviceToHost, c.stream));
+  PW_CUDA(cudaStreamSynchronize(c.stream));
+  int r = 0;
+  if (dg[0] != 0.0) {
+    for (int k = 0; k < steps; ++k)
+      if (dg[k] > rank_tol * dg[0]) ++r;
+  }
+  *rank_host = r;
+  return r;
+}
+
+void form_q2(Ctx& c, const double* R, int mr, const int* piv, const double* tau, int r,
+             double* Q2) {
+  if (r <= 0) return;
+  size_t smem = sizeof(double) * mr * kQ2Warps;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PW_CUDA(cudaFuncSetAttribute(form_q2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  form_q2_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, piv, tau,
+                                                                                   r, Q2);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv, int r,
+                         double* X) {
+  PW_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * (size_t)m * r, c.stream));
+  if (r <= 0) return;
+  size_t smem = sizeof(double) * mr * kQ2Warps;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PW_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, m, piv, r, X);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void launch_combine_gemv(Ctx& c, const double* g, const double* D, const double* cvec,
+                         const double* alpha, const double* Q, int r, long long d, double* y,
+                         double* alpha_next, double* part) {
+  const int nblk = (int)((d + kCgRows - 1) / kCgRows);
+  size_t smem = sizeof(double) * ((size_t)r + kCgThreads);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PW_CUDA(cudaFuncSetAttribute(combine_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  combine_gemv_kernel<<<nblk, kCgThreads, smem, c.stream>>>(g, D, cvec, alpha, Q, r, d, y, part);
+  c.launches += 1;
+  if (r > 0) {
+    reduce_parts_kernel<<<(r + 255) / 256, 256, 0, c.stream>>>(part, nblk, r, alpha_next);
+    c.launches += 1;
+  }
+  PW_LAUNCH_CHECK();
+}
+
+void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const double* v,
+                         double* alpha, double* part) {
+  if (r <= 0) return;
+  const int nblk = (int)((d + kCgRows - 1) / kCgRows);
+  project_partial_kernel<<<nblk, kCgThreads, 0, c.stream>>>(Q, r, d, v, part);
+  reduce_parts_kernel<<<(r + 255) / 256, 256, 0, c.stream>>>(part, nblk, r, alpha);
+  c.launches += 2;
+  PW_LAUNCH_CHECK();
+}
+
+size_t combine_part_doubles(long long d, int r) {
+  return (size_t)((d + kCgRows - 1) / kCgRows) * (size_t)std::max(r, 1);
+}
+
+}  // namespace pw

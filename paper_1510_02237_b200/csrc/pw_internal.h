@@ -1,0 +1,125 @@
+// Internal declarations of the sm_100a KSE-Parareal library (libpitwave_b200.so).
+// The public C ABI lives in include/pitwave_b200.h; nothing here crosses it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/pitwave_b200.h"
+
+namespace pw {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define PW_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      throw pw::Error{PW_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) +    \
+                                       " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+    }                                                                                       \
+  } while (0)
+
+#define PW_CHECK(cond, code, msg)                 \
+  do {                                            \
+    if (!(cond)) throw pw::Error{(code), (msg)};  \
+  } while (0)
+
+#define PW_LAUNCH_CHECK() PW_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- grid description
+// State layout (reference mesh.State, mesh.py:74-138): (3, ny, nx) fp64,
+// x fastest; a batch is B states at stride `ld` doubles.
+struct GridDesc {
+  int nx, ny;
+  double dx, dy;
+};
+
+// Exact-order (reference operation order, no FMA contraction) stencil
+// parameters: face-velocity arrays live on the device (mesh.face_normal_velocities).
+struct ExactParams {
+  int nx, ny, order;
+  double dx, dy, cs, a1, a2;
+  const double* uf;  // (ny, nx) x-face normal velocity
+  const double* vf;  // (ny, nx) y-face normal velocity
+};
+
+// Folded constant-velocity RK3 coefficients for one stage with factor beta
+// (s_out = q + beta * f(s_in)); see fine_fused.cu.
+struct StageCoef {
+  double cx[7];  // beta * x advection stencil, offsets -3..3
+  double cy[7];  // beta * y advection stencil (used only when V != 0)
+  double pgx;    // -beta*cs*sx
+  double pgy;    // -beta*cs*sy
+  double dmx;    // beta*a1*sx
+  double dmy;    // beta*a2*sy
+  double pdiv;   // -beta*cs
+};
+struct FusedParams {
+  int nx, ny;
+  long long ld_in, ld_out;
+  double sx, sy;  // 0.5/dx, 0.5/dy
+  StageCoef st[3];
+};
+
+// ---------------------------------------------------------------- context
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  void* cublas = nullptr;    // cublasHandle_t
+  void* cusolver = nullptr;  // cusolverDnHandle_t
+  // scratch for grid barriers / reductions
+  double* red = nullptr;     // reduction scratch (doubles)
+  size_t red_cap = 0;
+  int launches = 0;          // kernels launched by this library (bench gpu_launches)
+  bool strict = false;       // force reference-order kernels everywhere
+};
+
+// ---------------------------------------------------------------- kernels (launchers)
+// exact.cu  (compiled with -fmad=false: reference operation order, bitwise)
+void launch_rk3_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                      int nsteps, double h, double* work);
+void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                       int nsteps, double h, int nsub, double* work);
+size_t rk3_exact_work_doubles(const ExactParams& p, int batch);
+size_t fefb_exact_work_doubles(const ExactParams& p, int batch);
+
+// fine_fused.cu
+void make_fused_params(FusedParams& fp, int nx, int ny, double dx, double dy, double cs,
+                       int order, double U, double V, double a1, double a2, double h);
+void launch_rk3_fused(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch,
+                      bool vadv);
+bool fused_supported(int nx, int ny);
+
+// linalg.cu
+void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,
+                       double beta, size_t n);
+void launch_extract_upper(Ctx& c, const double* W, long long ldw, int mr, int m, double* R);
+size_t residual_scratch_doubles(int ncols, long long nrows);
+void launch_residual(Ctx& c, const double* a, long long lda, const double* b, long long ldb,
+                     int ncols, long long nrows, double* scratch, double* out_dev);
+size_t combine_part_doubles(long long d, int r);
+// R: mr x m (lda mr), mr = min(d, m); returns rank, fills piv (m), tau/diag (min(mr, m))
+int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv_dev,
+                     double* tau_dev, double* diag_dev, int* rank_host);
+void form_q2(Ctx& c, const double* R, int mr, const int* piv, const double* tau, int r,
+             double* Q2);
+void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv, int r,
+                         double* X);
+void launch_combine_gemv(Ctx& c, const double* g, const double* D, const double* cvec,
+                         const double* alpha, const double* Q, int r, long long d, double* y,
+                         double* alpha_next, double* part);
+void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const double* v,
+                         double* alpha, double* part);
+
+}  // namespace pw
