@@ -8,18 +8,28 @@
 // divergence telescopes into a fixed 7-point stencil per direction:
 //   -(F_{i+1}-F_i)/dx = sum_k c_k q_{i+k},  c_k = -(w_{k+2}-w_{k+3})/dx
 // with w the linear face-flux weights of _face_flux (numba_backend.py:13-30).
-// Each stage is folded into  s_out = q + beta*f(s_in)  with the stage
-// factor beta (h/3, h/2, h) pre-multiplied into every coefficient, so one
-// stage costs ~40 DP ops per cell instead of the reference form's ~106.
-// Results differ from the reference only by rounding (tests: <=1e-12 rel).
+// Each stage is folded into  s_out = q + beta*f(s_in)  with the stage factor
+// beta (h/3, h/2, h) and the expanded divergence damping pre-multiplied into
+// the coefficients (StageCoef): ~37 DP ops per cell and stage instead of the
+// reference form's ~106.  Results differ from the reference only by
+// rounding (tests: <= 1e-12 relative).
 //
-// Data movement (the roofline unit: 48 B per cell-update = read + write
-// (u,v,p) once).  A CTA owns an x-strip of TX output columns and a y-segment
-// of TY output rows.  It streams q rows top-to-bottom through shared-memory
-// rings (cp.async, asynchronous one tick ahead) and runs the three stages as
-// a row pipeline: stage k trails stage k-1 by RY rows, so all three stages
-// are fused per tile with halos only in x (3 cells per stage) and a
-// 6*RY-row warm-up per segment; q, s1, s2 never touch HBM.
+// Data movement (roofline unit: 48 B per cell-update = read + write (u,v,p)
+// once).  A CTA owns an x-strip of TX output columns and a y-segment of TY
+// rows.  It streams q rows top-to-bottom through shared-memory rings
+// (16-byte cp.async, one tick ahead) and runs the three RK stages as a
+// software pipeline: in tick t stage 1 produces rows of tick t, stage 2 the
+// rows stage 1 finished in tick t-1, stage 3 those stage 2 finished in t-1.
+// The three stages are therefore independent inside a tick: one barrier per
+// tick, and every thread owns exactly one (stage, column group, row block)
+// item, executed by one uniform code path (no divergence, no idle threads).
+// Halos are only in x (E = 4 columns per stage) plus a 6*RY-row warm-up per
+// segment; s1 and s2 never leave shared memory.
+//
+// On-chip traffic is what limits this kernel (shared memory moves ~128 B/clk
+// per SM, ~5.5x HBM), so each item is a BX x BY register block loaded as
+// aligned 16-byte chunks, and ring rows are XOR-swizzled per chunk so the
+// 32-byte per-thread stride of those chunks is bank-conflict free.
 #include <cuda_pipeline.h>
 
 #include "pw_internal.h"
@@ -27,111 +37,246 @@
 namespace pw {
 namespace {
 
-constexpr int H = 3;  // x radius of one stage (order-6 flux: 3; damping: 2)
+constexpr int E = 4;  // region growth per stage: >= the 3-cell x radius, keeps 16-B alignment
 
 __device__ __forceinline__ int wrapi(int k, int n) {
   k %= n;
   return k < 0 ? k + n : k;
 }
 
-template <int TX, int TY, int RY, int R, int NT, bool VADV>
+constexpr int pad4(int w) { return (w + 3) / 4 * 4; }  // whole chunk pairs per row
+
+template <int TX_, int TY_, int BX_, int BY_, int NRB_, int RY_, bool VADV_>
 struct Cfg {
-  static constexpr int WQ = TX + 6 * H;  // q ring row width (cols -3H .. TX+3H)
-  static constexpr int W1 = TX + 4 * H;  // s1 ring row width
-  static constexpr int W2 = TX + 2 * H;  // s2 ring row width
-  static constexpr int NQ = 3 * RY + 2 * R;
-  static constexpr int NS = 2 * RY + R;
-  static constexpr int NTICK = (TY + 6 * RY) / R;
-  static constexpr size_t SMEM = sizeof(double) * 3 * ((size_t)NQ * WQ + (size_t)NS * W1 + (size_t)NS * W2);
-  static_assert((TY + 6 * RY) % R == 0, "R must divide TY + 6 RY");
+  static constexpr int TX = TX_, TY = TY_, BX = BX_, BY = BY_, NRB = NRB_, RY = RY_;
+  static constexpr bool VADV = VADV_;
+  static constexpr int R = BY * NRB;            // rows per tick and stage
+  static constexpr int WQ = pad4(TX + 6 * E);   // q ring:  logical cols [-3E, TX+3E)
+  static constexpr int W1 = pad4(TX + 4 * E);   // s1 ring: logical cols [-2E, TX+2E)
+  static constexpr int W2 = pad4(TX + 2 * E);   // s2 ring: logical cols [-E,  TX+E)
+  static constexpr int G1 = (TX + 4 * E) / BX, G2 = (TX + 2 * E) / BX, G3 = TX / BX;
+  static constexpr int NT = (G1 + G2 + G3) * NRB;
+  static constexpr int NQ = 4 * R + 3 * RY;     // q rows live across the 3-tick pipeline + prefetch
+  static constexpr int NS = 2 * R + 2 * RY;
+  static constexpr int NTICK = (TY + 6 * RY + R - 1) / R + 2;
+  static constexpr size_t SMEM =
+      sizeof(double) * 3 * ((size_t)NQ * WQ + (size_t)NS * W1 + (size_t)NS * W2);
+  // CTAs per SM: shared memory (227 KB) and a ~200-register budget per thread
+  static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
+  static constexpr int MINB_REGS = 65536 / (NT * 200);
+  static constexpr int MINB = (MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS) < 1
+                                  ? 1 : (MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS);
+  static_assert(TX % BX == 0 && (2 * E) % BX == 0, "BX must divide TX and 2E");
+  static_assert(BX % 2 == 0 && BY >= 1, "BX must be even (16-byte chunks)");
 };
 
-// One stage over R rows of the output region of width WO.
-//   in ring  : rows of the stage input (width WI = WO + 2H), NI slots
-//   q ring   : step-start state (width WQ), column offset (WQ-WO)/2 to the output region
-//   rel0     : ring-relative row of the first output row this tick
-//   out      : ring (NO slots, width WO) or global (when GLOBAL)
-template <int WO, int RY, int R, int NT, bool VADV, bool GLOBAL>
-__device__ __forceinline__ void stage(const double* __restrict__ in_ring, int NI,
-                                      const double* __restrict__ q_ring, int NQ, int WQ,
-                                      int rel0, int rel_lo, int rel_hi, double* __restrict__ out,
-                                      int NO, const StageCoef& C, double sx, double sy,
-                                      // global-output addressing (stage 3)
-                                      double* __restrict__ gout, long long n, int nx, int ny,
-                                      int x0, int qs) {
-  constexpr int WI = WO + 2 * H;
-  const int qoff = (WQ - WO) / 2;
-  for (int item = threadIdx.x; item < R * WO; item += NT) {
-    const int rr = item / WO;
-    const int c = item - rr * WO;
-    const int rel = rel0 + rr;
-    if (rel < rel_lo || rel >= rel_hi) continue;
-    const int ci = c + H;
-    // ring row pointers for dy = -RY..RY (field-major inside a slot)
-    const double* row[2 * RY + 1];
+// Bank-conflict avoidance.  Work items are interleaved so that a quarter-warp
+// (8 threads of one 16-byte shared access) holds 4 column groups of one row
+// block and 4 of the next (row blocks are BY = 2 rows apart).  Same-row
+// threads touch chunks 2g+m -> 4 distinct even/odd bank quads; the other row
+// block lands on the complementary quads because every ring slot s stores its
+// 16-byte chunks pair-swapped (chunk j at j ^ flip(s), flip(s) = (s >> 1) & 1).
+__device__ __forceinline__ int slot_flip(int s) { return (s >> 1) & 1; }
+
+// A ring row seen from one thread: chunk k relative to its column group lives at
+// (k even ? e : o) + 2k  (e/o absorb the slot's pair swap)
+struct RowP {
+  const double* e;
+  const double* o;
+};
+__device__ __forceinline__ RowP rowp_of(const double* slot_base, int s, int c) {
+  const int f = slot_flip(s);
+  return RowP{slot_base + c + 2 * f, slot_base + c - 2 * f};
+}
+
+// dst[2i, 2i+1] = chunk k0 + i of the row (field offset foff, a multiple of 16 doubles)
+template <int N>
+__device__ __forceinline__ void ldrow(double (&dst)[N], const RowP& r, int foff, int k0) {
 #pragma unroll
-    for (int dy = -RY; dy <= RY; ++dy) row[dy + RY] = in_ring + (size_t)((rel + dy) % NI) * 3 * WI;
-    const double* u0 = row[RY];
-    const double* v0 = row[RY] + WI;
-    const double* p0 = row[RY] + 2 * WI;
-#define U(dy, dx) (row[RY + (dy)][ci + (dx)])
-#define V(dy, dx) (row[RY + (dy)][WI + ci + (dx)])
-#define P(dy, dx) (row[RY + (dy)][2 * WI + ci + (dx)])
-    const double* qrow = q_ring + (size_t)(rel % NQ) * 3 * WQ;
-    double au = qrow[qoff + c];
-    double av = qrow[WQ + qoff + c];
-    double ap = qrow[2 * WQ + qoff + c];
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-      au = fma(C.cx[k], u0[ci + k - 3], au);
-      av = fma(C.cx[k], v0[ci + k - 3], av);
-      ap = fma(C.cx[k], p0[ci + k - 3], ap);
-    }
-    if constexpr (VADV) {
-#pragma unroll
-      for (int k = 0; k < 7; ++k) {
-        if (k == 3) continue;
-        au = fma(C.cy[k], U(k - 3, 0), au);
-        av = fma(C.cy[k], V(k - 3, 0), av);
-        ap = fma(C.cy[k], P(k - 3, 0), ap);
-      }
-      au = fma(C.cy[3], U(0, 0), au);
-      av = fma(C.cy[3], V(0, 0), av);
-      ap = fma(C.cy[3], P(0, 0), ap);
-    }
-    // velocity divergence (unscaled by beta): div = sx (u_{i+1}-u_{i-1}) + sy (v_{j+1}-v_{j-1})
-    const double d_c = sx * (U(0, 1) - U(0, -1)) + sy * (V(1, 0) - V(-1, 0));
-    const double d_e = sx * (U(0, 2) - U(0, 0)) + sy * (V(1, 1) - V(-1, 1));
-    const double d_w = sx * (U(0, 0) - U(0, -2)) + sy * (V(1, -1) - V(-1, -1));
-    const double d_n = sx * (U(1, 1) - U(1, -1)) + sy * (V(2, 0) - V(0, 0));
-    const double d_s = sx * (U(-1, 1) - U(-1, -1)) + sy * (V(0, 0) - V(-2, 0));
-    au = fma(C.pgx, P(0, 1) - P(0, -1), au);
-    au = fma(C.dmx, d_e - d_w, au);
-    av = fma(C.pgy, P(1, 0) - P(-1, 0), av);
-    av = fma(C.dmy, d_n - d_s, av);
-    ap = fma(C.pdiv, d_c, ap);
-#undef U
-#undef V
-#undef P
-    if constexpr (GLOBAL) {
-      const int gy = wrapi(qs + rel, ny);
-      const long long off = (long long)gy * nx + x0 + c;
-      gout[off] = au;
-      gout[n + off] = av;
-      gout[2 * n + off] = ap;
-    } else {
-      double* orow = out + (size_t)(rel % NO) * 3 * WO;
-      orow[c] = au;
-      orow[WO + c] = av;
-      orow[2 * WO + c] = ap;
-    }
+  for (int i = 0; i < N / 2; ++i) {
+    const int k = k0 + i;
+    const double* p = ((k & 1) ? r.o : r.e) + foff + 2 * k;
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    dst[2 * i] = t.x;
+    dst[2 * i + 1] = t.y;
   }
 }
 
-template <int TX, int TY, int RY, int R, int NT, bool VADV>
-__global__ void __launch_bounds__(NT) rk3_fused_kernel(const double* __restrict__ in,
-                                                       double* __restrict__ out, FusedParams P) {
-  using K = Cfg<TX, TY, RY, R, NT, VADV>;
+struct Ring {
+  const double* base;
+  int n;      // slots
+  int pitch;  // doubles per slot (3 fields)
+  int w;      // doubles per field row
+};
+
+// One work item: output block rows [rel0, rel0+BY) x logical cols [c, c+BX) of
+// the stage region; input ring `in` holds the previous stage (q for stage 1),
+// whose column c+E.. corresponds to output col c -- the x-window of output col
+// c starts at input col c (x offset -4).  q base at q-ring col c + S*E.
+template <class K>
+__device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, int rel0, int c,
+                                           const StageCoef& C, double (&au)[K::BY][K::BX],
+                                           double (&av)[K::BY][K::BX], double (&ap)[K::BY][K::BX]) {
+  constexpr int BX = K::BX, BY = K::BY;
+  constexpr int WW = BX + 8;  // full window  x in [-4, BX+4)
+  constexpr int WH = BX + 4;  // halo window  x in [-2, BX+2)
+  // stage base q (q-ring col c + S*E = chunk S*E/2 relative to the group); stage 1 folds
+  // it into the stencil centre instead (its input ring is q itself)
+  double qb[3][BY][BX];
+  if (S != 1) {
+    int s = rel0 % qr.n;
+#pragma unroll
+    for (int r = 0; r < BY; ++r) {
+      const RowP q = rowp_of(qr.base + (size_t)s * qr.pitch, s, c);
+      s = (s + 1 == qr.n) ? 0 : s + 1;
+      ldrow(qb[0][r], q, 0, S * E / 2);
+      ldrow(qb[1][r], q, qr.w, S * E / 2);
+      ldrow(qb[2][r], q, 2 * qr.w, S * E / 2);
+    }
+  }
+  // row pointers of rel0 - RY .. rel0 + BY - 1 + RY, computed once (rel >= 0 always)
+  constexpr int NR = BY + 2 * K::RY;
+  RowP rows[NR];
+  {
+    int s = (rel0 - K::RY) % in.n;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      rows[k] = rowp_of(in.base + (size_t)s * in.pitch, s, c);
+      s = (s + 1 == in.n) ? 0 : s + 1;
+    }
+  }
+  auto rowp = [&](int dy) -> const RowP& { return rows[dy + K::RY]; };
+#pragma unroll
+  for (int r = 0; r < BY; ++r)
+#pragma unroll
+    for (int x = 0; x < BX; ++x) au[r][x] = av[r][x] = ap[r][x] = 0.0;
+  const int W = in.w;
+  // a[r][X] = v(r+1) - v(r-1), b[r][X] = u(r+1) - u(r-1) at x = X-1 in [-1, BX]
+  double A[BY][BX + 2], B[BY][BX + 2];
+  // ---- v rows -2 .. BY+1: x-advection on rows 0..BY-1, halo windows of rows -1..BY
+  {
+    double vh[BY + 2][WH];  // rows -1..BY on x in [-2, BX+2)
+    ldrow(vh[0], rowp(-1), W, 2 / 2);
+    ldrow(vh[BY + 1], rowp(BY), W, 2 / 2);
+#pragma unroll
+    for (int r = 0; r < BY; ++r) {
+      double w[WW];
+      ldrow(w, rowp(r), W, 0);
+#pragma unroll
+      for (int x = 0; x < BX; ++x)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) av[r][x] = fma(C.cxv[k], w[x + 1 + k], av[r][x]);
+#pragma unroll
+      for (int k = 0; k < WH; ++k) vh[r + 1][k] = w[k + 2];
+    }
+    double vm2[BX], vp2[BX];
+    ldrow(vm2, rowp(-2), W, 4 / 2);
+    ldrow(vp2, rowp(BY + 1), W, 4 / 2);
+#pragma unroll
+    for (int r = 0; r < BY; ++r) {
+#pragma unroll
+      for (int X = 0; X < BX + 2; ++X) A[r][X] = vh[r + 2][X + 1] - vh[r][X + 1];
+#pragma unroll
+      for (int x = 0; x < BX; ++x) {
+        const double up = (r + 2 <= BY) ? vh[r + 3][x + 2] : vp2[x];
+        const double dn = (r - 2 >= -1) ? vh[r - 1][x + 2] : vm2[x];
+        av[r][x] = fma(C.dv2, up + dn, av[r][x]);
+      }
+    }
+  }
+  // ---- u rows -1 .. BY
+  {
+    double uh[BY + 2][WH];
+    ldrow(uh[0], rowp(-1), 0, 2 / 2);
+    ldrow(uh[BY + 1], rowp(BY), 0, 2 / 2);
+#pragma unroll
+    for (int r = 0; r < BY; ++r) {
+      double w[WW];
+      ldrow(w, rowp(r), 0, 0);
+#pragma unroll
+      for (int x = 0; x < BX; ++x) {
+#pragma unroll
+        for (int k = 0; k < 7; ++k) au[r][x] = fma(C.cxu[k], w[x + 1 + k], au[r][x]);
+        ap[r][x] = fma(C.pu, w[x + 5] - w[x + 3], ap[r][x]);
+      }
+#pragma unroll
+      for (int k = 0; k < WH; ++k) uh[r + 1][k] = w[k + 2];
+    }
+#pragma unroll
+    for (int r = 0; r < BY; ++r)
+#pragma unroll
+      for (int X = 0; X < BX + 2; ++X) B[r][X] = uh[r + 2][X + 1] - uh[r][X + 1];
+  }
+  // ---- p rows -1 .. BY
+  {
+    double plo[BX], phi[BX];
+    ldrow(plo, rowp(-1), 2 * W, 4 / 2);
+    ldrow(phi, rowp(BY), 2 * W, 4 / 2);
+    double pc[BY][BX];
+#pragma unroll
+    for (int r = 0; r < BY; ++r) {
+      double w[WW];
+      ldrow(w, rowp(r), 2 * W, 0);
+#pragma unroll
+      for (int x = 0; x < BX; ++x) {
+#pragma unroll
+        for (int k = 0; k < 7; ++k) ap[r][x] = fma(C.cxp[k], w[x + 1 + k], ap[r][x]);
+        au[r][x] = fma(C.pgx, w[x + 5] - w[x + 3], au[r][x]);
+        pc[r][x] = w[x + 4];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < BY; ++r)
+#pragma unroll
+      for (int x = 0; x < BX; ++x) {
+        const double up = (r + 1 < BY) ? pc[r + 1][x] : phi[x];
+        const double dn = (r - 1 >= 0) ? pc[r - 1][x] : plo[x];
+        av[r][x] = fma(C.pgy, up - dn, av[r][x]);
+      }
+  }
+  // ---- y advection (V != 0): rows r-3 .. r+3 on x in [0, BX)
+  if constexpr (K::VADV) {
+#pragma unroll
+    for (int r = 0; r < BY; ++r)
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        const RowP& yr = rowp(r + k - 3);
+        double a[BX], b[BX], d[BX];
+        ldrow(a, yr, 0, 4 / 2);
+        ldrow(b, yr, W, 4 / 2);
+        ldrow(d, yr, 2 * W, 4 / 2);
+#pragma unroll
+        for (int x = 0; x < BX; ++x) {
+          au[r][x] = fma(C.cy[k], a[x], au[r][x]);
+          av[r][x] = fma(C.cy[k], b[x], av[r][x]);
+          ap[r][x] = fma(C.cy[k], d[x], ap[r][x]);
+        }
+      }
+  }
+  // ---- mixed damping differences and the pressure divergence's y part
+#pragma unroll
+  for (int r = 0; r < BY; ++r)
+#pragma unroll
+    for (int x = 0; x < BX; ++x) {
+      au[r][x] = fma(C.cuv, A[r][x + 2] - A[r][x], au[r][x]);
+      av[r][x] = fma(C.cvu, B[r][x + 2] - B[r][x], av[r][x]);
+      ap[r][x] = fma(C.pv, A[r][x + 1], ap[r][x]);
+    }
+  if (S != 1) {
+#pragma unroll
+    for (int r = 0; r < BY; ++r)
+#pragma unroll
+      for (int x = 0; x < BX; ++x) {
+        au[r][x] += qb[0][r][x];
+        av[r][x] += qb[1][r][x];
+        ap[r][x] += qb[2][r][x];
+      }
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::NT, 1) rk3_fused_kernel(const double* __restrict__ in,
+                                                          double* __restrict__ out, FusedParams P) {
   extern __shared__ __align__(16) double smem[];
   double* q_ring = smem;
   double* s1_ring = q_ring + (size_t)K::NQ * 3 * K::WQ;
@@ -139,25 +284,74 @@ __global__ void __launch_bounds__(NT) rk3_fused_kernel(const double* __restrict_
 
   const int nx = P.nx, ny = P.ny;
   const long long n = (long long)nx * ny;
-  const int x0 = blockIdx.x * TX;
-  const int y0 = blockIdx.y * TY;
+  const int x0 = blockIdx.x * K::TX;
+  const int y0 = blockIdx.y * K::TY;
   const double* src = in + (long long)blockIdx.z * P.ld_in;
   double* dst = out + (long long)blockIdx.z * P.ld_out;
-  const int qs = y0 - 3 * RY;  // ring-relative row 0
+  const int qs = y0 - 3 * K::RY;  // ring-relative row 0
+  const int tid = threadIdx.x;
 
+  // this thread's item: stage S (1..3), column group g, row block rb
+  int S, g, rb;
+  {
+    const int n1 = K::G1 * K::NRB, n2 = K::G2 * K::NRB;
+    int t = tid;
+    if (t < n1) {
+      S = 1;
+    } else if (t < n1 + n2) {
+      S = 2;
+      t -= n1;
+    } else {
+      S = 3;
+      t -= n1 + n2;
+    }
+    rb = t % K::NRB;  // interleaved: see the bank-conflict note above
+    g = t / K::NRB;
+  }
+  const int c = g * K::BX;
+  const Ring qring{q_ring, K::NQ, 3 * K::WQ, K::WQ};
+  const Ring inring = (S == 1) ? qring
+                    : (S == 2) ? Ring{s1_ring, K::NS, 3 * K::W1, K::W1}
+                               : Ring{s2_ring, K::NS, 3 * K::W2, K::W2};
+  double* out_ring = (S == 1) ? s1_ring : s2_ring;
+  const int out_pitch = (S == 1) ? 3 * K::W1 : 3 * K::W2;
+  const int out_w = (S == 1) ? K::W1 : K::W2;
+  const StageCoef& C = P.st[S - 1];
+  // stage row offset inside a tick and validity window (ring-relative rows)
+  const int lag = (S == 1) ? K::RY : (S == 2) ? K::R + 2 * K::RY : 2 * K::R + 3 * K::RY;
+  const int lo = S * K::RY, hi = K::TY + (6 - S) * K::RY;
+
+  // q-row loads: R rows x 3 fields x (TX+6E)/2 chunks of 16 B per tick (chunks never
+  // straddle the x wrap).  The (row-in-tick, field, chunk) set of each thread is the
+  // same every tick, so its smem/global offsets are computed once here.
+  constexpr int CH = (K::TX + 6 * E) / 2;
+  constexpr int PER_ROW = 3 * CH;
+  constexpr int NLD = (K::R * PER_ROW + K::NT - 1) / K::NT;
+  int ld_rr[NLD], ld_soff[NLD];
+  long long ld_goff[NLD];
+#pragma unroll
+  for (int k = 0; k < NLD; ++k) {
+    const int e = tid + k * K::NT;
+    const int rr = e / PER_ROW;
+    const int rem = e - rr * PER_ROW;
+    const int f = rem / CH;
+    const int col = 2 * (rem - f * CH);
+    int gx = x0 - 3 * E + col;
+    if (gx < 0 || gx >= nx) gx = wrapi(gx, nx);
+    ld_rr[k] = (e < K::R * PER_ROW) ? rr : -1;
+    ld_soff[k] = f * K::WQ + col;  // chunk pair swap of the slot applied per tick
+    ld_goff[k] = f * n + gx;
+  }
   auto load_rows = [&](int rel_first) {
-    // R rows x 3 fields x WQ columns, 8-byte cp.async (LDGSTS), wrapped indices
-    constexpr int PER_ROW = 3 * K::WQ;
-    for (int e = threadIdx.x; e < R * PER_ROW; e += NT) {
-      const int rr = e / PER_ROW;
-      const int rem = e - rr * PER_ROW;
-      const int f = rem / K::WQ;
-      const int col = rem - f * K::WQ;
-      const int rel = rel_first + rr;
-      const int gy = wrapi(qs + rel, ny);
-      const int gx = wrapi(x0 - 3 * H + col, nx);
-      double* d = q_ring + (size_t)(rel % K::NQ) * 3 * K::WQ + f * K::WQ + col;
-      __pipeline_memcpy_async(d, src + f * n + (long long)gy * nx + gx, sizeof(double));
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      if (ld_rr[k] < 0) continue;
+      const int rel = rel_first + ld_rr[k];
+      int gy = qs + rel;
+      if (gy < 0 || gy >= ny) gy = wrapi(gy, ny);
+      const int slot = rel % K::NQ;
+      double* d = q_ring + (size_t)slot * (3 * K::WQ) + (ld_soff[k] ^ (2 * slot_flip(slot)));
+      __pipeline_memcpy_async(d, src + ld_goff[k] + (long long)gy * nx, 16);
     }
     __pipeline_commit();
   };
@@ -166,51 +360,89 @@ __global__ void __launch_bounds__(NT) rk3_fused_kernel(const double* __restrict_
   for (int t = 0; t < K::NTICK; ++t) {
     __pipeline_wait_prior(0);
     __syncthreads();
-    if (t + 1 < K::NTICK) load_rows((t + 1) * R);
-    // stage 1: s1 = q + (h/3) f(q)    rows rel [tR-RY, tR-RY+R), valid [RY, TY+5RY)
-    stage<K::W1, RY, R, NT, VADV, false>(q_ring, K::NQ, q_ring, K::NQ, K::WQ, t * R - RY, RY,
-                                         TY + 5 * RY, s1_ring, K::NS, P.st[0], P.sx, P.sy,
-                                         nullptr, n, nx, ny, x0, qs);
-    __syncthreads();
-    // stage 2: s2 = q + (h/2) f(s1)   valid [2RY, TY+4RY)
-    stage<K::W2, RY, R, NT, VADV, false>(s1_ring, K::NS, q_ring, K::NQ, K::WQ, t * R - 2 * RY,
-                                         2 * RY, TY + 4 * RY, s2_ring, K::NS, P.st[1], P.sx,
-                                         P.sy, nullptr, n, nx, ny, x0, qs);
-    __syncthreads();
-    // stage 3: q+ = q + h f(s2)       valid [3RY, TY+3RY) -> global
-    stage<TX, RY, R, NT, VADV, true>(s2_ring, K::NS, q_ring, K::NQ, K::WQ, t * R - 3 * RY,
-                                     3 * RY, TY + 3 * RY, nullptr, 0, P.st[2], P.sx, P.sy, dst, n,
-                                     nx, ny, x0, qs);
+    if (t + 1 < K::NTICK) load_rows((t + 1) * K::R);
+    const int rel0 = t * K::R - lag + rb * K::BY;
+    if (rel0 >= lo && rel0 < hi) {
+      double au[K::BY][K::BX], av[K::BY][K::BX], ap[K::BY][K::BX];
+      stage_item<K>(inring, qring, S, rel0, c, C, au, av, ap);
+      if (S == 3) {
+#pragma unroll
+        for (int r = 0; r < K::BY; ++r) {
+          int gy = qs + rel0 + r;
+          if (gy < 0 || gy >= ny) gy = wrapi(gy, ny);
+          double* gp = dst + (long long)gy * nx + x0 + c;
+#pragma unroll
+          for (int x = 0; x < K::BX; x += 2) {
+            *reinterpret_cast<double2*>(gp + x) = make_double2(au[r][x], au[r][x + 1]);
+            *reinterpret_cast<double2*>(gp + n + x) = make_double2(av[r][x], av[r][x + 1]);
+            *reinterpret_cast<double2*>(gp + 2 * n + x) = make_double2(ap[r][x], ap[r][x + 1]);
+          }
+        }
+      } else {
+        int so = rel0 % K::NS;
+#pragma unroll
+        for (int r = 0; r < K::BY; ++r) {
+          int s = so + r;
+          s -= (s >= K::NS) ? K::NS : 0;
+          double* o = out_ring + (size_t)s * out_pitch;
+#pragma unroll
+          for (int x = 0; x < K::BX; x += 2) {
+            const int p = (c + x) ^ (2 * slot_flip(s));
+            *reinterpret_cast<double2*>(o + p) = make_double2(au[r][x], au[r][x + 1]);
+            *reinterpret_cast<double2*>(o + out_w + p) = make_double2(av[r][x], av[r][x + 1]);
+            *reinterpret_cast<double2*>(o + 2 * out_w + p) = make_double2(ap[r][x], ap[r][x + 1]);
+          }
+        }
+      }
+    }
   }
 }
 
-template <int TX, int TY, int RY, bool VADV>
+template <class K>
 void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
-  constexpr int R = 2, NT = 128;
-  using K = Cfg<TX, TY, RY, R, NT, VADV>;
-  auto kern = rk3_fused_kernel<TX, TY, RY, R, NT, VADV>;
+  auto kern = rk3_fused_kernel<K>;
   static bool attr_set = false;
   if (!attr_set) {
     PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
     attr_set = true;
   }
-  dim3 grid(fp.nx / TX, fp.ny / TY, batch);
-  kern<<<grid, NT, K::SMEM, c.stream>>>(in, out, fp);
+  dim3 grid(fp.nx / K::TX, fp.ny / K::TY, batch);
+  kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp);
   c.launches += 1;
   PW_LAUNCH_CHECK();
+}
+
+int tile_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("PW_FUSED_VARIANT");  // tuning hook (scripts/microbench.py)
+    v = (s && *s) ? atoi(s) : 0;
+  }
+  return v;
 }
 
 template <int RY, bool VADV>
 void launch_ry(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
   const int nx = fp.nx, ny = fp.ny;
-  // x strip 64 (or 32/16/8 for small grids); y segment 128 (or the grid height)
-  if (nx % 64 == 0) {
-    if (ny % 128 == 0) return launch_cfg<64, 128, RY, VADV>(c, fp, in, out, batch);
-    if (ny % 64 == 0) return launch_cfg<64, 64, RY, VADV>(c, fp, in, out, batch);
+  if (nx % 128 == 0 && ny % 256 == 0) {
+    switch (tile_variant()) {
+      case 1: return launch_cfg<Cfg<64, 128, 4, 2, 2, RY, VADV>>(c, fp, in, out, batch);
+      case 2: return launch_cfg<Cfg<64, 256, 4, 2, 1, RY, VADV>>(c, fp, in, out, batch);
+      case 3: return launch_cfg<Cfg<32, 256, 4, 2, 2, RY, VADV>>(c, fp, in, out, batch);
+      case 4: return launch_cfg<Cfg<64, 256, 4, 1, 2, RY, VADV>>(c, fp, in, out, batch);
+      case 5: return launch_cfg<Cfg<128, 256, 4, 2, 1, RY, VADV>>(c, fp, in, out, batch);
+      case 6: return launch_cfg<Cfg<64, 256, 4, 4, 1, RY, VADV>>(c, fp, in, out, batch);
+      case 7: return launch_cfg<Cfg<32, 128, 4, 2, 2, RY, VADV>>(c, fp, in, out, batch);
+      default: break;
+    }
   }
-  if (nx % 32 == 0 && ny % 32 == 0) return launch_cfg<32, 32, RY, VADV>(c, fp, in, out, batch);
-  if (nx % 16 == 0 && ny % 16 == 0) return launch_cfg<16, 16, RY, VADV>(c, fp, in, out, batch);
-  if (nx % 8 == 0 && ny % 8 == 0) return launch_cfg<8, 8, RY, VADV>(c, fp, in, out, batch);
+  if (nx % 64 == 0 && ny % 64 == 0) {
+    if (ny % 256 == 0) return launch_cfg<Cfg<64, 256, 4, 2, 2, RY, VADV>>(c, fp, in, out, batch);
+    return launch_cfg<Cfg<64, 64, 4, 2, 2, RY, VADV>>(c, fp, in, out, batch);
+  }
+  if (nx % 32 == 0 && ny % 32 == 0) return launch_cfg<Cfg<32, 32, 4, 2, 2, RY, VADV>>(c, fp, in, out, batch);
+  if (nx % 16 == 0 && ny % 16 == 0) return launch_cfg<Cfg<16, 16, 4, 2, 1, RY, VADV>>(c, fp, in, out, batch);
+  if (nx % 8 == 0 && ny % 8 == 0) return launch_cfg<Cfg<8, 8, 4, 2, 1, RY, VADV>>(c, fp, in, out, batch);
   throw Error{PW_ERR_VALUE, "fused RK3 needs nx, ny multiples of 8"};
 }
 
@@ -266,19 +498,37 @@ void make_fused_params(FusedParams& fp, int nx, int ny, double dx, double dy, do
     const double by = (k + 3 >= 0 && k + 3 < 6) ? wy[k + 3] : 0.0;
     cy[k + 3] = -(ay - by) / dy;
   }
+  // expanded divergence damping: a1 sx (D_{i+1} - D_{i-1}) with D = sx dx(u) + sy dy(v)
+  //   = a1 sx^2 (u_{i+2} - 2 u_i + u_{i-2}) + a1 sx sy (a_{i+1} - a_{i-1}),  a = v_{j+1} - v_{j-1}
+  // and a2 sy (D_{j+1} - D_{j-1}) = a2 sy^2 (v_{j+2} - 2 v_j + v_{j-2}) + a2 sx sy (b_{i+1} - b_{i-1})
+  const double sx = fp.sx, sy = fp.sy;
   const double betas[3] = {h / 3.0, h / 2.0, h};
   for (int s = 0; s < 3; ++s) {
     const double b = betas[s];
     StageCoef& C = fp.st[s];
     for (int k = 0; k < 7; ++k) {
-      C.cx[k] = b * cx[k];
+      C.cxu[k] = b * cx[k];
+      C.cxv[k] = b * cx[k];
+      C.cxp[k] = b * cx[k];
       C.cy[k] = b * cy[k];
     }
-    C.pgx = -b * cs * fp.sx;
-    C.pgy = -b * cs * fp.sy;
-    C.dmx = b * a1 * fp.sx;
-    C.dmy = b * a2 * fp.sy;
-    C.pdiv = -b * cs;
+    const double du2 = b * a1 * sx * sx;
+    C.cxu[1] += du2;
+    C.cxu[3] -= 2.0 * du2;
+    C.cxu[5] += du2;
+    C.dv2 = b * a2 * sy * sy;
+    C.cxv[3] -= 2.0 * C.dv2;
+    C.pgx = -b * cs * sx;
+    C.pgy = -b * cs * sy;
+    C.cuv = b * a1 * sx * sy;
+    C.cvu = b * a2 * sx * sy;
+    C.pu = -b * cs * sx;
+    C.pv = -b * cs * sy;
+    if (s == 0) {  // stage 1 reads q itself: s1 = (I + beta L) q, the identity joins the centre
+      C.cxu[3] += 1.0;
+      C.cxv[3] += 1.0;
+      C.cxp[3] += 1.0;
+    }
   }
 }
 

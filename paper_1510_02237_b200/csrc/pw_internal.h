@@ -55,14 +55,21 @@ struct ExactParams {
 
 // Folded constant-velocity RK3 coefficients for one stage with factor beta
 // (s_out = q + beta * f(s_in)); see fine_fused.cu.
+// Divergence damping is expanded and folded (a1 dx(div) = a1 sx^2 dxx(u) +
+// a1 sx sy dx dy(v), a2 dy(div) likewise), so per cell only x stencils, a
+// few y differences and two mixed differences remain.
 struct StageCoef {
-  double cx[7];  // beta * x advection stencil, offsets -3..3
-  double cy[7];  // beta * y advection stencil (used only when V != 0)
-  double pgx;    // -beta*cs*sx
-  double pgy;    // -beta*cs*sy
-  double dmx;    // beta*a1*sx
-  double dmy;    // beta*a2*sy
-  double pdiv;   // -beta*cs
+  double cxu[7];  // beta * (x advection + a1 sx^2 [1,0,-2,0,1]) on u, offsets -3..3
+  double cxv[7];  // beta * x advection on v, centre - 2 beta a2 sy^2
+  double cxp[7];  // beta * x advection on p
+  double cy[7];   // beta * y advection stencil (used only when V != 0)
+  double pgx;     // -beta cs sx     du += pgx (p_{i+1} - p_{i-1})
+  double pgy;     // -beta cs sy     dv += pgy (p_{j+1} - p_{j-1})
+  double cuv;     // beta a1 sx sy   du += cuv (a_{i+1} - a_{i-1}),  a = v_{j+1} - v_{j-1}
+  double cvu;     // beta a2 sx sy   dv += cvu (b_{i+1} - b_{i-1}),  b = u_{j+1} - u_{j-1}
+  double dv2;     // beta a2 sy^2    dv += dv2 (v_{j+2} + v_{j-2})
+  double pu;      // -beta cs sx     dp += pu (u_{i+1} - u_{i-1})
+  double pv;      // -beta cs sy     dp += pv a_i
 };
 struct FusedParams {
   int nx, ny;
