@@ -236,8 +236,40 @@ struct pw_basis {
 
 namespace {
 
+// PW_QR_TIMING=1 prints the refactorisation phase times (CUDA events) to stderr
+struct PhaseClock {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  explicit PhaseClock(cudaStream_t st) : s(st) {
+    const char* e = getenv("PW_QR_TIMING");
+    on = e && *e == '1';
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  ~PhaseClock() {
+    if (!on || ev.size() < 2) return;
+    cudaEventSynchronize(ev.back().second);
+    fprintf(stderr, "[pw qr]");
+    for (size_t k = 1; k < ev.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[k - 1].second, ev[k].second);
+      fprintf(stderr, " %s=%.3fms", ev[k].first, ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto& x : ev) cudaEventDestroy(x.second);
+  }
+};
+
 void basis_refactor(pw_basis* B) {
   Ctx& c = B->ctx->c;
+  PhaseClock clk(c.stream);
+  clk.mark("start");
   const long long d = B->dim;
   const int m = B->m;
   B->fq_valid = B->img_valid = false;
@@ -255,7 +287,9 @@ void basis_refactor(pw_basis* B) {
   PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)d, m, W, (int)d, &lw1));
   PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), (int)d, mr, mr, W, (int)d, tau1, &lw2));
   double* work = B->cs_work.ensure(c, (size_t)std::max(lw1, lw2));
+  clk.mark("copy");
   PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)d, m, W, (int)d, tau1, work, std::max(lw1, lw2), info));
+  clk.mark("geqrf");
   // 2) column-pivoted QR of the mr x m factor R1 (same pivots as dgeqp3 on S)
   double* Rs = B->Rs.ensure(c, (size_t)mr * m);
   pw::launch_extract_upper(c, W, d, mr, m, Rs);
@@ -264,6 +298,7 @@ void basis_refactor(pw_basis* B) {
   double* diag = B->diag.ensure(c, m);
   int r = 0;
   pw::pivoted_qr_small(c, Rs, mr, m, B->rank_tol, piv, tau2, diag, &r);
+  clk.mark("pivqr+rank");
   B->diag_h.assign(mr, 0.0);
   B->piv_h.assign(m, 0);
   PW_CUDA(cudaMemcpyAsync(B->diag_h.data(), diag, sizeof(double) * mr, cudaMemcpyDeviceToHost, c.stream));
@@ -275,15 +310,18 @@ void basis_refactor(pw_basis* B) {
   }
   // 3) explicit Q1 (d x mr), Q = Q1 Q2[:, :r]
   PW_SOLVER(cusolverDnDorgqr(solver(c), (int)d, mr, mr, W, (int)d, tau1, work, std::max(lw1, lw2), info));
+  clk.mark("orgqr");
   double* Q2 = B->Q2.ensure(c, (size_t)mr * r);
   pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
   double* Q = B->Q.ensure(c, (size_t)d * r);
   gemm(c, false, false, d, r, mr, 1.0, W, d, Q2, mr, 0.0, Q, d);
+  clk.mark("Q=Q1Q2");
   // 4) Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep)
   double* X = B->X.ensure(c, (size_t)m * r);
   pw::tri_inverse_scatter(c, Rs, mr, m, piv, r, X);
   double* Y = B->Y.ensure(c, (size_t)d * r);
   gemm(c, false, false, d, r, m, 1.0, B->M.p, d, X, m, 0.0, Y, d);
+  clk.mark("Rinv+Y");
   PW_CUDA(cudaStreamSynchronize(c.stream));
 }
 
@@ -364,6 +402,12 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     PW_CUDA(cudaGetDeviceProperties(&prop, device));
     PW_CHECK(prop.major == 10, PW_ERR_CUDA,
              std::string("this library is built for sm_100a (B200); device is ") + prop.name);
+    // keep freed device memory in the stream-ordered pool: sweeps re-allocate their
+    // (multi-GB) basis buffers every window, and re-mapping them costs ~100 ms
+    cudaMemPool_t pool;
+    PW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    PW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     auto ctx = std::make_unique<pw_ctx>();
     ctx->c.device = device;
     ctx->c.stream = static_cast<cudaStream_t>(stream);

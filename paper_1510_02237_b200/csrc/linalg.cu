@@ -188,15 +188,22 @@ __global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A,
 }
 
 // ---------------------------------------------------------------- fused serial step
+// One HBM pass over D and Q per serial correction step (2 r d 8 bytes).  A
+// persistent grid of 2 CTAs per SM walks 1024-row tiles: 4 rows per thread and
+// 4 columns of D in flight per iteration (16 independent 8-byte loads per
+// thread), then 8 columns of Q at a time, reduced inside the warp by an 8-way
+// transpose (9 shuffles per 8 columns) and accumulated per warp in shared
+// memory; one fixed-order cross-warp sum per CTA, one fixed-order cross-CTA
+// sum in reduce_parts_kernel -> deterministic alpha.
 constexpr int kCgThreads = 256;
-constexpr int kCgRpt = 8;  // rows per thread
+constexpr int kCgWarps = kCgThreads / 32;
+constexpr int kCgRpt = 4;  // rows per thread
 constexpr int kCgRows = kCgThreads * kCgRpt;
 
-// 32 per-lane partials -> lane L holds the warp total of column L
-__device__ __forceinline__ double transpose_reduce32(double (&acc)[32]) {
+__device__ __forceinline__ double transpose_reduce8(double (&acc)[8]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
+  for (int off = 4; off >= 1; off >>= 1) {
     const bool upper = (lane & off) != 0;
 #pragma unroll
     for (int i = 0; i < off; ++i) {
@@ -205,97 +212,136 @@ __device__ __forceinline__ double transpose_reduce32(double (&acc)[32]) {
       acc[i] = keep + __shfl_xor_sync(FULL, send, off);
     }
   }
-  return acc[0];
+  double v = acc[0];  // column lane & 7, summed over the lane's group of 8
+  v += __shfl_xor_sync(FULL, v, 8);
+  v += __shfl_xor_sync(FULL, v, 16);
+  return v;
 }
 
-// part[blk][k] = sum over this block's rows of Q[row, k] * y[row]
-__device__ __forceinline__ void block_qty(const double* __restrict__ Q, int r, long long d,
-                                          long long row0, const double (&y)[kCgRpt],
-                                          double* __restrict__ part, double* red) {
+// wpart[warp][k] += sum over this tile's rows of Q[row, k] * y[row]
+__device__ __forceinline__ void tile_qty(const double* __restrict__ Q, int r, long long d,
+                                         long long row0, const double (&y)[kCgRpt],
+                                         double* __restrict__ wpart) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = kCgThreads / 32;
-  for (int k0 = 0; k0 < r; k0 += 32) {
-    double acc[32];
+  for (int k0 = 0; k0 < r; k0 += 8) {
+    double acc[8];
 #pragma unroll
-    for (int kk = 0; kk < 32; ++kk) acc[kk] = 0.0;
+    for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.0;
 #pragma unroll
-    for (int s = 0; s < kCgRpt; ++s) {
-      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-      if (row < d) {
+    for (int kk = 0; kk < 8; ++kk) {
+      if (k0 + kk < r) {
+        const double* Qk = Q + (long long)(k0 + kk) * d;
 #pragma unroll
-        for (int kk = 0; kk < 32; ++kk)
-          if (k0 + kk < r) acc[kk] = fma(__ldg(Q + (long long)(k0 + kk) * d + row), y[s], acc[kk]);
+        for (int s = 0; s < kCgRpt; ++s) {
+          const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+          if (row < d) acc[kk] = fma(__ldcs(Qk + row), y[s], acc[kk]);
+        }
       }
     }
-    const double tot = transpose_reduce32(acc);
-    red[warp * 32 + lane] = tot;
-    __syncthreads();
-    if (warp == 0) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += red[w * 32 + lane];
-      if (k0 + lane < r) part[(long long)blockIdx.x * r + k0 + lane] = s;
-    }
-    __syncthreads();
+    const double v = transpose_reduce8(acc);
+    if (lane < 8 && k0 + lane < r) wpart[warp * r + k0 + lane] += v;
   }
 }
 
-__global__ void __launch_bounds__(kCgThreads) combine_gemv_kernel(
+__device__ __forceinline__ void flush_wpart(const double* wpart, int r, double* __restrict__ part) {
+  __syncthreads();
+  for (int k = threadIdx.x; k < r; k += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kCgWarps; ++w) s += wpart[w * r + k];
+    part[(long long)blockIdx.x * r + k] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
     const double* __restrict__ g, const double* __restrict__ D, const double* __restrict__ cvec,
     const double* __restrict__ alpha, const double* __restrict__ Q, int r, long long d,
     double* __restrict__ y_out, double* __restrict__ part) {
   extern __shared__ double sh[];
   double* a_s = sh;            // r
-  double* red = sh + r;        // 8 warps x 32
+  double* wpart = sh + r;      // kCgWarps x r
   for (int k = threadIdx.x; k < r; k += blockDim.x) a_s[k] = alpha[k];
+  for (int k = threadIdx.x; k < kCgWarps * r; k += blockDim.x) wpart[k] = 0.0;
   __syncthreads();
-  const long long row0 = (long long)blockIdx.x * kCgRows;
-  double y[kCgRpt];
-#pragma unroll
-  for (int s = 0; s < kCgRpt; ++s) {
-    const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-    y[s] = row < d ? g[row] + cvec[row] : 0.0;
-  }
-  // y += D alpha   (column-major D: coalesced along rows for every k)
-  for (int k = 0; k < r; ++k) {
-    const double ak = a_s[k];
-    const double* Dk = D + (long long)k * d;
+  const long long ntiles = (d + kCgRows - 1) / kCgRows;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row0 = tile * kCgRows;
+    double y[kCgRpt];
 #pragma unroll
     for (int s = 0; s < kCgRpt; ++s) {
       const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-      if (row < d) y[s] = fma(__ldg(Dk + row), ak, y[s]);
+      y[s] = row < d ? g[row] + cvec[row] : 0.0;
     }
-  }
+    // y += D alpha  (column-major D: every column read as one coalesced 8 KB run)
+    int k = 0;
+    for (; k + 4 <= r; k += 4) {
+      double t[4][kCgRpt];
 #pragma unroll
-  for (int s = 0; s < kCgRpt; ++s) {
-    const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-    if (row < d) y_out[row] = y[s];
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int s = 0; s < kCgRpt; ++s) {
+          const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+          t[kk][s] = row < d ? __ldcs(D + (long long)(k + kk) * d + row) : 0.0;
+        }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int s = 0; s < kCgRpt; ++s) y[s] = fma(t[kk][s], a_s[k + kk], y[s]);
+    }
+    for (; k < r; ++k) {
+#pragma unroll
+      for (int s = 0; s < kCgRpt; ++s) {
+        const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+        if (row < d) y[s] = fma(__ldcs(D + (long long)k * d + row), a_s[k], y[s]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kCgRpt; ++s) {
+      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      if (row < d) y_out[row] = y[s];
+    }
+    if (r > 0) tile_qty(Q, r, d, row0, y, wpart);
   }
-  if (r > 0) block_qty(Q, r, d, row0, y, part, red);
+  if (r > 0) flush_wpart(wpart, r, part);
 }
 
-__global__ void __launch_bounds__(kCgThreads) project_partial_kernel(
+__global__ void __launch_bounds__(kCgThreads, 2) project_partial_kernel(
     const double* __restrict__ Q, int r, long long d, const double* __restrict__ v,
     double* __restrict__ part) {
-  __shared__ double red[kCgThreads];
-  const long long row0 = (long long)blockIdx.x * kCgRows;
-  double y[kCgRpt];
+  extern __shared__ double wpart[];
+  for (int k = threadIdx.x; k < kCgWarps * r; k += blockDim.x) wpart[k] = 0.0;
+  __syncthreads();
+  const long long ntiles = (d + kCgRows - 1) / kCgRows;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row0 = tile * kCgRows;
+    double y[kCgRpt];
 #pragma unroll
-  for (int s = 0; s < kCgRpt; ++s) {
-    const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-    y[s] = row < d ? v[row] : 0.0;
+    for (int s = 0; s < kCgRpt; ++s) {
+      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      y[s] = row < d ? v[row] : 0.0;
+    }
+    tile_qty(Q, r, d, row0, y, wpart);
   }
-  block_qty(Q, r, d, row0, y, part, red);
+  flush_wpart(wpart, r, part);
 }
 
-// alpha[k] = sum_b part[b][k]  (fixed order: deterministic)
-__global__ void reduce_parts_kernel(const double* __restrict__ part, int nblk, int r,
-                                    double* __restrict__ alpha) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= r) return;
+// alpha[k] = sum_b part[b][k]  (fixed order: deterministic); 32 columns x 8 partial streams per CTA
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nblk,
+                                                           int r, double* __restrict__ alpha) {
+  __shared__ double red[8][32];
+  const int kk = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + kk;
   double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += part[(long long)b * r + k];
-  alpha[k] = s;
+  if (k < r)
+    for (int b = grp; b < nblk; b += 8) s += part[(long long)b * r + k];
+  red[grp][kk] = s;
+  __syncthreads();
+  if (grp == 0 && k < r) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][kk];
+    alpha[k] = t;
+  }
 }
 
 // ---------------------------------------------------------------- elementwise / residual
@@ -469,11 +515,16 @@ void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv,
   PW_LAUNCH_CHECK();
 }
 
+static int combine_grid(const Ctx& c, long long d) {
+  const long long ntiles = (d + kCgRows - 1) / kCgRows;
+  return (int)std::max<long long>(1, std::min<long long>(ntiles, 2LL * c.num_sms));
+}
+
 void launch_combine_gemv(Ctx& c, const double* g, const double* D, const double* cvec,
                          const double* alpha, const double* Q, int r, long long d, double* y,
                          double* alpha_next, double* part) {
-  const int nblk = (int)((d + kCgRows - 1) / kCgRows);
-  size_t smem = sizeof(double) * ((size_t)r + kCgThreads);
+  const int nblk = combine_grid(c, d);
+  size_t smem = sizeof(double) * ((size_t)r * (1 + kCgWarps) + 1);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     PW_CUDA(cudaFuncSetAttribute(combine_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -482,7 +533,7 @@ void launch_combine_gemv(Ctx& c, const double* g, const double* D, const double*
   combine_gemv_kernel<<<nblk, kCgThreads, smem, c.stream>>>(g, D, cvec, alpha, Q, r, d, y, part);
   c.launches += 1;
   if (r > 0) {
-    reduce_parts_kernel<<<(r + 255) / 256, 256, 0, c.stream>>>(part, nblk, r, alpha_next);
+    reduce_parts_kernel<<<(r + 31) / 32, 256, 0, c.stream>>>(part, nblk, r, alpha_next);
     c.launches += 1;
   }
   PW_LAUNCH_CHECK();
@@ -491,15 +542,21 @@ void launch_combine_gemv(Ctx& c, const double* g, const double* D, const double*
 void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const double* v,
                          double* alpha, double* part) {
   if (r <= 0) return;
-  const int nblk = (int)((d + kCgRows - 1) / kCgRows);
-  project_partial_kernel<<<nblk, kCgThreads, 0, c.stream>>>(Q, r, d, v, part);
-  reduce_parts_kernel<<<(r + 255) / 256, 256, 0, c.stream>>>(part, nblk, r, alpha);
+  const int nblk = combine_grid(c, d);
+  size_t smem = sizeof(double) * (size_t)r * kCgWarps;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PW_CUDA(cudaFuncSetAttribute(project_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  project_partial_kernel<<<nblk, kCgThreads, smem, c.stream>>>(Q, r, d, v, part);
+  reduce_parts_kernel<<<(r + 31) / 32, 256, 0, c.stream>>>(part, nblk, r, alpha);
   c.launches += 2;
   PW_LAUNCH_CHECK();
 }
 
 size_t combine_part_doubles(long long d, int r) {
-  return (size_t)((d + kCgRows - 1) / kCgRows) * (size_t)std::max(r, 1);
+  return (size_t)((d + kCgRows - 1) / kCgRows) * (size_t)std::max(r, 1);  // >= grid x r
 }
 
 }  // namespace pw

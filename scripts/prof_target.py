@@ -33,11 +33,17 @@ if what == "fine":
     y = p.apply(x)
     torch.cuda.synchronize()
     print("fine ok", bool(torch.isfinite(y).all()))
-elif what == "c3k2":
+elif what == "coarse":
+    _, c = specs(512)
+    x = torch.as_tensor(harness.initial_state("c3")).cuda()[None, :].contiguous()
+    y = SlicePropagator(c, nsteps=1).apply(x)
+    torch.cuda.synchronize()
+    print("coarse ok", bool(torch.isfinite(y).all()))
+elif what in ("c3k2", "c3k5"):
     wl = harness.WORKLOADS["c3"]
     f, c = specs(wl.n)
     fine, coarse = SlicePropagator(f, wl.slice_span), SlicePropagator(c, wl.slice_span)
     q0 = torch.as_tensor(harness.initial_state("c3")).cuda()
-    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, 2, return_device=True)
+    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, 2 if what == "c3k2" else 5, return_device=True)
     torch.cuda.synchronize()
     print("c3k2 ok", res, sub.rank)
