@@ -130,6 +130,18 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
              int n_it, double tol, double rank_tol, double* out_states, double* residuals,
              int* n_done, double* timings, int* ranks, pw_basis** out_basis);
 
+/* ---- slice-sharded fine predictor (multi-GPU) ----------------------------
+ * If set, pw_sweep calls hook(user, qk, pred, n_c, dim) instead of applying
+ * the fine propagator itself: qk = the n_c predictor inputs, pred = where the
+ * n_c fine images must land (both device, column-major, ld = dim).  The hook
+ * runs on the calling thread and must leave its work ordered on the context
+ * stream; it returns 0 on success.  Used to shard the P independent fine
+ * propagations over GPUs (each rank propagates P/N slices, then an NCCL
+ * all-gather over NVLink): the reference's _fine_all pool (parareal.py:62-65)
+ * spread over devices.  hook = NULL restores the local fine propagator. */
+typedef int (*pw_fine_hook)(void* user, const double* qk, double* pred, int n_c, long long dim);
+int pw_ctx_set_fine_hook(pw_ctx* ctx, pw_fine_hook hook, void* user);
+
 /* ---- memory helper ------------------------------------------------------
  * stream-ordered copy of nbytes between any host/device pointers (UVA,
  * cudaMemcpyDefault), synchronising the context stream afterwards. */

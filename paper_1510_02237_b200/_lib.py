@@ -25,6 +25,7 @@ MODE_KSE = 1
 c_dp = ctypes.POINTER(ctypes.c_double)
 c_ip = ctypes.POINTER(ctypes.c_int)
 c_vp = ctypes.c_void_p
+FINE_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong)
 
 
 class PdeDesc(ctypes.Structure):
@@ -75,6 +76,7 @@ SIGNATURES = [
     ("pw_sweep", ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_double, ctypes.c_double, c_vp, c_dp, c_ip, c_dp, c_ip,
                                 ctypes.POINTER(c_vp)]),
+    ("pw_ctx_set_fine_hook", ctypes.c_int, [c_vp, FINE_HOOK, c_vp]),
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
 ]

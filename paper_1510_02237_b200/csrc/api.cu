@@ -449,6 +449,14 @@ int pw_ctx_synchronize(pw_ctx* ctx) {
   return guarded([&] { PW_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
 }
 
+int pw_ctx_set_fine_hook(pw_ctx* ctx, pw_fine_hook hook, void* user) {
+  return guarded([&] {
+    PW_CHECK(ctx, PW_ERR_VALUE, "ctx is NULL");
+    ctx->c.fine_hook = hook;
+    ctx->c.fine_hook_user = user;
+  });
+}
+
 int pw_ctx_set_strict(pw_ctx* ctx, int strict) {
   return guarded([&] { ctx->c.strict = strict != 0; });
 }
@@ -710,7 +718,12 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     for (int k = 0; k < n_it; ++k) {
       if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
       // fine predictor over all slices at once (_fine_all, parareal.py:62-65)
-      prop_apply(fine, QK, PRED, n_c, d);
+      if (c.fine_hook) {
+        const int rc = c.fine_hook(c.fine_hook_user, QK, PRED, n_c, d);
+        PW_CHECK(rc == 0, PW_ERR_STATE, "fine hook failed (rc=" + std::to_string(rc) + ")");
+      } else {
+        prop_apply(fine, QK, PRED, n_c, d);
+      }
       if (timed) PW_CUDA(cudaEventRecord(ev[1], c.stream));
       // c_i = F(qk[i]) - G(qk[i])  [- D Q^T qk[i] in KSE mode]
       pw::launch_axpby_cols(c, PRED, PRED, GK, 1.0, -1.0, (size_t)d * n_c);

@@ -90,6 +90,8 @@ struct Ctx {
   size_t red_cap = 0;
   int launches = 0;          // kernels launched by this library (bench gpu_launches)
   bool strict = false;       // force reference-order kernels everywhere
+  pw_fine_hook fine_hook = nullptr;  // slice-sharded fine predictor (multi-GPU), see header
+  void* fine_hook_user = nullptr;
 };
 
 // ---------------------------------------------------------------- kernels (launchers)

@@ -1,0 +1,70 @@
+"""Multi-GPU plumbing for the Parareal window (host side, torch.distributed).
+
+Slice sharding of the fine predictor: the P fine propagations of one
+iteration are independent (the reference's ``_fine_all`` thread pool,
+parareal.py:62-65).  Rank r propagates the contiguous block of slices
+``shard_range(P, r, N)`` on its own GPU, and one all-gather (NCCL over
+NVLink, or gloo on CPU in the tests) gives every rank all P fine images.
+The rest of the window -- subspace refactorisation and serial correction
+sweep -- runs replicated on every rank with identical inputs and
+deterministic kernels, so all ranks hold bitwise-identical iterates.
+
+The row-sharded basis of SURVEY.md 8(e) (distributed TSQR, allreduce of the
+r inner products per serial step) is the next step and is not built yet.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as tdist
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous [lo, hi) block of n items for `rank` of `world` (sizes differ by <= 1)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class ShardedFine:
+    """Fine predictor over a batch of slices, sharded over a process group.
+
+    ``apply_fn(states)`` maps a (b, d) tensor of slice states to their fine
+    images (same device).  ``__call__(qk)`` takes all n (n, d) states on
+    every rank and returns all n images on every rank.
+    """
+
+    def __init__(self, apply_fn, group=None):
+        self.apply_fn = apply_fn
+        self.group = group
+
+    @property
+    def world(self):
+        return tdist.get_world_size(self.group) if tdist.is_initialized() else 1
+
+    @property
+    def rank(self):
+        return tdist.get_rank(self.group) if tdist.is_initialized() else 0
+
+    def __call__(self, qk: torch.Tensor) -> torch.Tensor:
+        world, rank = self.world, self.rank
+        n = qk.shape[0]
+        if world == 1:
+            return self.apply_fn(qk)
+        lo, hi = shard_range(n, rank, world)
+        width = (n + world - 1) // world  # all_gather needs equal blocks: pad
+        local = torch.zeros((width, qk.shape[1]), dtype=qk.dtype, device=qk.device)
+        if hi > lo:
+            local[: hi - lo] = self.apply_fn(qk[lo:hi].contiguous())
+        blocks = [torch.empty_like(local) for _ in range(world)]
+        tdist.all_gather(blocks, local, group=self.group)
+        out = torch.empty_like(qk)
+        for r in range(world):
+            rlo, rhi = shard_range(n, r, world)
+            if rhi > rlo:
+                out[rlo:rhi] = blocks[r][: rhi - rlo]
+        return out
+
+    # the oracle sweeps (tests) call fine.batch(states) on numpy arrays
+    def batch(self, states):
+        t = torch.as_tensor(states)
+        return self(t).cpu().numpy()

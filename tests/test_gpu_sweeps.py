@@ -289,3 +289,29 @@ def test_kse_residual_and_ranks_against_oracle_c1_shape_p16():
     worst = max(rel(a, b) for a, b in zip(ends, o_ends))
     assert worst <= 1e-9, worst
     np.testing.assert_allclose(res, o_res, rtol=1e-8)
+
+
+def test_sharded_fine_hook_single_rank_group():
+    """The multi-GPU fine hook (pw_ctx_set_fine_hook + dist.ShardedFine) on a 1-rank NCCL group."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    g = golden("c1_kse.npz")
+    wl, fine, coarse = c1_props()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ends_g, res_g, _ = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it, group=dist.group.WORLD)
+    finally:
+        dist.destroy_process_group()
+    ends, res, _ = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    np.testing.assert_array_equal(np.array(ends_g), np.array(ends))
+    assert res_g == res
