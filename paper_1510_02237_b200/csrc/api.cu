@@ -501,6 +501,13 @@ int pw_prop_create_pde(pw_ctx* ctx, const pw_pde_desc* desc, pw_prop** out) {
     PW_CUDA(cudaMemcpyAsync(dv, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     PW_CUDA(cudaStreamSynchronize(c.stream));
     P->ex = pw::ExactParams{D.nx, D.ny, D.order, D.dx, D.dy, D.cs, D.a1, D.a2, du, dv};
+    auto pow2_inv = [](double x) {  // 1/x if x is an exact power of two, else 0
+      int e = 0;
+      const double m = std::frexp(x, &e);
+      return (m == 0.5) ? std::ldexp(1.0, 1 - e) : 0.0;
+    };
+    P->ex.inv_dx = pow2_inv(D.dx);
+    P->ex.inv_dy = pow2_inv(D.dy);
     if (D.scheme == PW_SCHEME_RK3 && cst) {
       pw::make_fused_params(P->fp, D.nx, D.ny, D.dx, D.dy, D.cs, D.order, hu[0], hv[0], D.a1,
                             D.a2, D.h);

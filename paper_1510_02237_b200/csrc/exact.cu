@@ -19,6 +19,7 @@
 // (latency-bound serial work: no per-substep launches); (2) the fine RK3 for
 // spatially varying velocity or when the context is in strict mode.
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 
 #include "pw_internal.h"
 
@@ -68,7 +69,8 @@ __device__ __forceinline__ double adv_at(const ExactParams& p, const double* __r
   const int jp = j + 1 < p.ny ? j + 1 : 0;
   const double fxi = fx_at(p, q, j, i), fxp = fx_at(p, q, j, ip);
   const double gyj = gy_at(p, q, j, i), gyp = gy_at(p, q, jp, i);
-  return -(fxp - fxi) / p.dx - (gyp - gyj) / p.dy;
+  const double tx = -(fxp - fxi), ty = (gyp - gyj);
+  return (p.inv_dx != 0.0 ? tx * p.inv_dx : tx / p.dx) - (p.inv_dy != 0.0 ? ty * p.inv_dy : ty / p.dy);
 }
 
 __device__ __forceinline__ double cdx(const ExactParams& p, const double* __restrict__ f, int j,
@@ -124,34 +126,6 @@ __global__ void rk3_stage_exact(const double* q, const double* __restrict__ s, d
 // which each thread recomputes from the old state with the same expression
 // (bitwise identical to storing them), reading a ping-pong copy of (u, v, p).
 // work per state: [au, av, ap, u', v', p'] (6 planes).
-__device__ __forceinline__ double u_new(const ExactParams& p, const double* cu, const double* cv,
-                                        const double* pp, const double* au, int j, int i,
-                                        double sx, double sy, double tau, bool damp) {
-  const size_t c = (size_t)j * p.nx + i;
-  double du = au[c] - p.cs * cdx(p, pp, j, i, sx);
-  if (damp) {
-    const int im = wrapi(i - 1, p.nx), ipp = wrapi(i + 1, p.nx);
-    const double div_ip = cdx(p, cu, j, ipp, sx) + cdy(p, cv, j, ipp, sy);
-    const double div_im = cdx(p, cu, j, im, sx) + cdy(p, cv, j, im, sy);
-    du = du + p.a1 * ((div_ip - div_im) * sx);
-  }
-  return cu[c] + tau * du;
-}
-
-__device__ __forceinline__ double v_new(const ExactParams& p, const double* cu, const double* cv,
-                                        const double* pp, const double* av, int j, int i,
-                                        double sx, double sy, double tau, bool damp) {
-  const size_t c = (size_t)j * p.nx + i;
-  double dv = av[c] - p.cs * cdy(p, pp, j, i, sy);
-  if (damp) {
-    const int jm = wrapi(j - 1, p.ny), jpp = wrapi(j + 1, p.ny);
-    const double div_jp = cdx(p, cu, jpp, i, sx) + cdy(p, cv, jpp, i, sy);
-    const double div_jm = cdx(p, cu, jm, i, sx) + cdy(p, cv, jm, i, sy);
-    dv = dv + p.a2 * ((div_jp - div_jm) * sy);
-  }
-  return cv[c] + tau * dv;
-}
-
 // 7x7 neighbourhood of a cell, wrapped once: rows j-3..j+3, cols i-3..i+3
 struct Nbr {
   int ro[7];
@@ -171,34 +145,78 @@ __device__ __forceinline__ void make_nbr(Nbr& N, int j, int i, int nx, int ny) {
     N.co[k + 3] = ii;
   }
 }
-// u' and v' of one FB substep at (j+DY, i+DX), reference operation order (fb_substeps)
-template <int DY, int DX>
-__device__ __forceinline__ double un_at(const Nbr& N, const ExactParams& p, const double* cu,
-                                        const double* cv, const double* cp, const double* au,
-                                        double sx, double sy, double tau, bool damp) {
-  double du = N.at(au, DY, DX) - p.cs * ((N.at(cp, DY, DX + 1) - N.at(cp, DY, DX - 1)) * sx);
+// Field access for the FB substep: global memory through a wrapped 7x7 neighbourhood ...
+struct GAcc {
+  Nbr N;
+  const double* __restrict__ cu;
+  const double* __restrict__ cv;
+  const double* __restrict__ cp;
+  const double* __restrict__ au;
+  const double* __restrict__ av;
+  __device__ __forceinline__ double u(int dy, int dx) const { return N.at(cu, dy, dx); }
+  __device__ __forceinline__ double v(int dy, int dx) const { return N.at(cv, dy, dx); }
+  __device__ __forceinline__ double p(int dy, int dx) const { return N.at(cp, dy, dx); }
+  __device__ __forceinline__ double a_u(int dy, int dx) const { return N.at(au, dy, dx); }
+  __device__ __forceinline__ double a_v(int dy, int dx) const { return N.at(av, dy, dx); }
+};
+// ... or a shared-memory tile (pointers at the cell, row pitch W; a-tiles pitch WA)
+struct SAcc {
+  const double* su;
+  const double* sv;
+  const double* sp;
+  int W;
+  const double* sau;
+  const double* sav;
+  int WA;
+  __device__ __forceinline__ double u(int dy, int dx) const { return su[dy * W + dx]; }
+  __device__ __forceinline__ double v(int dy, int dx) const { return sv[dy * W + dx]; }
+  __device__ __forceinline__ double p(int dy, int dx) const { return sp[dy * W + dx]; }
+  __device__ __forceinline__ double a_u(int dy, int dx) const { return sau[dy * WA + dx]; }
+  __device__ __forceinline__ double a_v(int dy, int dx) const { return sav[dy * WA + dx]; }
+};
+
+// u' and v' of one FB substep at (j+DY, i+DX), reference operation order (fb_substeps,
+// numba_backend.py:137-143): du = au - cs dx(p) [+ a1 dx(div)], u' = u + tau du
+template <int DY, int DX, class A>
+__device__ __forceinline__ double un_at(const A& a, const ExactParams& p, double sx, double sy,
+                                        double tau, bool damp) {
+  double du = a.a_u(DY, DX) - p.cs * ((a.p(DY, DX + 1) - a.p(DY, DX - 1)) * sx);
   if (damp) {
-    const double div_ip = (N.at(cu, DY, DX + 2) - N.at(cu, DY, DX)) * sx +
-                          (N.at(cv, DY + 1, DX + 1) - N.at(cv, DY - 1, DX + 1)) * sy;
-    const double div_im = (N.at(cu, DY, DX) - N.at(cu, DY, DX - 2)) * sx +
-                          (N.at(cv, DY + 1, DX - 1) - N.at(cv, DY - 1, DX - 1)) * sy;
+    const double div_ip = (a.u(DY, DX + 2) - a.u(DY, DX)) * sx +
+                          (a.v(DY + 1, DX + 1) - a.v(DY - 1, DX + 1)) * sy;
+    const double div_im = (a.u(DY, DX) - a.u(DY, DX - 2)) * sx +
+                          (a.v(DY + 1, DX - 1) - a.v(DY - 1, DX - 1)) * sy;
     du = du + p.a1 * ((div_ip - div_im) * sx);
   }
-  return N.at(cu, DY, DX) + tau * du;
+  return a.u(DY, DX) + tau * du;
 }
-template <int DY, int DX>
-__device__ __forceinline__ double vn_at(const Nbr& N, const ExactParams& p, const double* cu,
-                                        const double* cv, const double* cp, const double* av,
-                                        double sx, double sy, double tau, bool damp) {
-  double dv = N.at(av, DY, DX) - p.cs * ((N.at(cp, DY + 1, DX) - N.at(cp, DY - 1, DX)) * sy);
+template <int DY, int DX, class A>
+__device__ __forceinline__ double vn_at(const A& a, const ExactParams& p, double sx, double sy,
+                                        double tau, bool damp) {
+  double dv = a.a_v(DY, DX) - p.cs * ((a.p(DY + 1, DX) - a.p(DY - 1, DX)) * sy);
   if (damp) {
-    const double div_jp = (N.at(cu, DY + 1, DX + 1) - N.at(cu, DY + 1, DX - 1)) * sx +
-                          (N.at(cv, DY + 2, DX) - N.at(cv, DY, DX)) * sy;
-    const double div_jm = (N.at(cu, DY - 1, DX + 1) - N.at(cu, DY - 1, DX - 1)) * sx +
-                          (N.at(cv, DY, DX) - N.at(cv, DY - 2, DX)) * sy;
+    const double div_jp = (a.u(DY + 1, DX + 1) - a.u(DY + 1, DX - 1)) * sx +
+                          (a.v(DY + 2, DX) - a.v(DY, DX)) * sy;
+    const double div_jm = (a.u(DY - 1, DX + 1) - a.u(DY - 1, DX - 1)) * sx +
+                          (a.v(DY, DX) - a.v(DY - 2, DX)) * sy;
     dv = dv + p.a2 * ((div_jp - div_jm) * sy);
   }
-  return N.at(cv, DY, DX) + tau * dv;
+  return a.v(DY, DX) + tau * dv;
+}
+
+// one cell's substep: new (u, v, p), p from the recomputed neighbour velocities
+template <class A>
+__device__ __forceinline__ void fb_cell(const A& a, const ExactParams& p, double sx, double sy,
+                                        double tau, bool damp, double ap_c, double p_c,
+                                        double& un, double& vn, double& pn) {
+  un = un_at<0, 0>(a, p, sx, sy, tau, damp);
+  vn = vn_at<0, 0>(a, p, sx, sy, tau, damp);
+  const double u_e = un_at<0, 1>(a, p, sx, sy, tau, damp);
+  const double u_w = un_at<0, -1>(a, p, sx, sy, tau, damp);
+  const double v_n = vn_at<1, 0>(a, p, sx, sy, tau, damp);
+  const double v_s = vn_at<-1, 0>(a, p, sx, sy, tau, damp);
+  const double divn = (u_e - u_w) * sx + (v_n - v_s) * sy;
+  pn = p_c + tau * (ap_c - p.cs * divn);
 }
 
 __global__ void __launch_bounds__(128) fefb_coop(double* st, int batch, long long ld, ExactParams p,
@@ -228,24 +246,22 @@ __global__ void __launch_bounds__(128) fefb_coop(double* st, int batch, long lon
         const int j = cell / p.nx, i = cell - j * p.nx;
         double* w = work + b * 6 * n;
         double* sb = st + b * ld;
-        const double* cu = from_state ? sb : w + 3 * n;
-        const double* cv = cu + n;
-        const double* cp = cu + 2 * n;
-        double* nu = from_state ? w + 3 * n : sb;
-        Nbr N;
-        make_nbr(N, j, i, p.nx, p.ny);
-        // momentum: current p gradient + current-velocity damping
-        const double un = un_at<0, 0>(N, p, cu, cv, cp, w, sx, sy, tau, damp);
-        const double vn = vn_at<0, 0>(N, p, cu, cv, cp, w + n, sx, sy, tau, damp);
-        // pressure from the freshly updated velocity divergence (neighbour velocities recomputed)
-        const double u_e = un_at<0, 1>(N, p, cu, cv, cp, w, sx, sy, tau, damp);
-        const double u_w = un_at<0, -1>(N, p, cu, cv, cp, w, sx, sy, tau, damp);
-        const double v_n = vn_at<1, 0>(N, p, cu, cv, cp, w + n, sx, sy, tau, damp);
-        const double v_s = vn_at<-1, 0>(N, p, cu, cv, cp, w + n, sx, sy, tau, damp);
-        const double divn = (u_e - u_w) * sx + (v_n - v_s) * sy;
+        const double* __restrict__ cu = from_state ? sb : w + 3 * n;
+        const double* __restrict__ cv = cu + n;
+        const double* __restrict__ cp = cu + 2 * n;
+        double* __restrict__ nu = from_state ? w + 3 * n : sb;
+        GAcc acc;
+        make_nbr(acc.N, j, i, p.nx, p.ny);
+        acc.cu = cu;
+        acc.cv = cv;
+        acc.cp = cp;
+        acc.au = w;
+        acc.av = w + n;
+        double un, vn, pn;
+        fb_cell(acc, p, sx, sy, tau, damp, w[2 * n + cell], cp[cell], un, vn, pn);
         nu[cell] = un;
         nu[n + cell] = vn;
-        nu[2 * n + cell] = cp[cell] + tau * (w[2 * n + cell] - cs * divn);
+        nu[2 * n + cell] = pn;
       }
       grid.sync();
     }
@@ -261,6 +277,120 @@ __global__ void __launch_bounds__(128) fefb_coop(double* st, int batch, long lon
       grid.sync();
     }
   }
+}
+
+// Tiled variant for grids divisible by T: per substep every CTA stages its
+// T x T tile of (u, v, p) with a 3-cell halo and (au, av) with a 1-cell halo in
+// shared memory, then computes T*T/256 cells per thread from the tile with
+// compile-time offsets (same expressions as the global variant: bitwise equal).
+template <int T>
+__global__ void __launch_bounds__(256, 2) fefb_tiled_coop(double* st, int batch, long long ld,
+                                                       ExactParams p, int nsteps, double tau,
+                                                       int nsub, double* work) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr int W = T + 6, WA = T + 2;
+  extern __shared__ double sm[];
+  double* su = sm;
+  double* sv = su + W * W;
+  double* sp = sv + W * W;
+  double* sau = sp + W * W;
+  double* sav = sau + WA * WA;
+  const int nx = p.nx, ny = p.ny;
+  const int n = nx * ny;
+  const double sx = 0.5 / p.dx, sy = 0.5 / p.dy;
+  const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
+  const int tiles_x = nx / T, tiles = tiles_x * (ny / T);
+  const long long work_items = (long long)tiles * batch;
+  const int stride = gridDim.x * blockDim.x;
+  const int first = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int step = 0; step < nsteps; ++step) {
+    for (long long b = 0; b < batch; ++b)
+      for (int cell = first; cell < n; cell += stride) {
+        const int j = cell / nx, i = cell - j * nx;
+        const double* q = st + b * ld;
+        double* w = work + b * 6 * n;
+        w[cell] = adv_at(p, q, j, i);
+        w[n + cell] = adv_at(p, q + n, j, i);
+        w[2 * n + cell] = adv_at(p, q + 2 * n, j, i);
+      }
+    grid.sync();
+    for (int sub = 0; sub < nsub; ++sub) {
+      const bool from_state = (sub % 2 == 0);
+      for (long long it = blockIdx.x; it < work_items; it += gridDim.x) {
+        const long long b = it / tiles;
+        const int t = (int)(it - b * tiles);
+        const int ty0 = (t / tiles_x) * T, tx0 = (t % tiles_x) * T;
+        double* w = work + b * 6 * n;
+        double* sb = st + b * ld;
+        const double* __restrict__ cu = from_state ? sb : w + 3 * n;
+        double* __restrict__ nu = from_state ? w + 3 * n : sb;
+        // stage (u, v, p) with halo 3 and (au, av) with halo 1: warp w stages rows
+        // w, w+8, ...; lanes cover x and x+32 (column wraps computed once per tile)
+        {
+          const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+          auto wrapx = [&](int x) { return x < 0 ? x + nx : (x >= nx ? x - nx : x); };
+          auto wrapy = [&](int y) { return y < 0 ? y + ny : (y >= ny ? y - ny : y); };
+          const int gx0 = wrapx(lane < W ? tx0 - 3 + lane : 0);
+          const int gx1 = wrapx(tx0 - 3 + lane + 32 < nx + 3 ? tx0 - 3 + lane + 32 : 0);
+          for (int y = warp; y < W; y += 8) {
+            const double* row = cu + wrapy(ty0 - 3 + y) * nx;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+              if (lane < W) __pipeline_memcpy_async(&sm[f * W * W + y * W + lane], row + f * n + gx0, 8);
+              if (lane + 32 < W)
+                __pipeline_memcpy_async(&sm[f * W * W + y * W + lane + 32], row + f * n + gx1, 8);
+            }
+          }
+          const int ga0 = wrapx(lane < WA ? tx0 - 1 + lane : 0);
+          const int ga1 = wrapx(tx0 - 1 + lane + 32 < nx + 1 ? tx0 - 1 + lane + 32 : 0);
+          for (int y = warp; y < WA; y += 8) {
+            const double* row = w + wrapy(ty0 - 1 + y) * nx;
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+              if (lane < WA) __pipeline_memcpy_async(&sau[f * WA * WA + y * WA + lane], row + f * n + ga0, 8);
+              if (lane + 32 < WA)
+                __pipeline_memcpy_async(&sau[f * WA * WA + y * WA + lane + 32], row + f * n + ga1, 8);
+            }
+          }
+          __pipeline_commit();
+          __pipeline_wait_prior(0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < T * T / 256; ++k) {
+          const int c = threadIdx.x + k * 256;
+          const int ly = c / T, lx = c - ly * T;
+          const int off = (ly + 3) * W + (lx + 3);
+          const int offa = (ly + 1) * WA + (lx + 1);
+          SAcc acc{su + off, sv + off, sp + off, W, sau + offa, sav + offa, WA};
+          const int cell = (ty0 + ly) * nx + tx0 + lx;
+          double un, vn, pn;
+          fb_cell(acc, p, sx, sy, tau, damp, w[2 * n + cell], sp[off], un, vn, pn);
+          nu[cell] = un;
+          nu[n + cell] = vn;
+          nu[2 * n + cell] = pn;
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+    if (nsub % 2 == 1) {
+      for (long long b = 0; b < batch; ++b)
+        for (int cell = first; cell < n; cell += stride) {
+          double* w = work + b * 6 * n;
+          double* sb = st + b * ld;
+          sb[cell] = w[3 * n + cell];
+          sb[n + cell] = w[4 * n + cell];
+          sb[2 * n + cell] = w[5 * n + cell];
+        }
+      grid.sync();
+    }
+  }
+}
+
+template <int T>
+constexpr size_t tiled_smem() {
+  return sizeof(double) * (3 * (T + 6) * (T + 6) + 2 * (T + 2) * (T + 2));
 }
 
 constexpr int kThreads = 256;
@@ -297,9 +427,35 @@ void launch_rk3_exact(Ctx& c, const ExactParams& p, double* states, int batch, l
   PW_LAUNCH_CHECK();
 }
 
+template <int T>
+static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                         int nsteps, double h, int nsub, double* work) {
+  static int per_sm = -1;
+  constexpr size_t smem = tiled_smem<T>();
+  if (per_sm < 0) {
+    PW_CUDA(cudaFuncSetAttribute(fefb_tiled_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fefb_tiled_coop<T>, 256, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long items = (long long)(p.nx / T) * (p.ny / T) * batch;
+  int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * per_sm));
+  double tau = h / nsub;
+  ExactParams pp = p;
+  void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)fefb_tiled_coop<T>, dim3(blocks), dim3(256), args, smem,
+                                      c.stream));
+  c.launches += 1;
+}
+
 void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                        int nsteps, double h, int nsub, double* work) {
   if (nsteps <= 0 || batch <= 0) return;
+  PW_CHECK((long long)p.nx * p.ny < (1LL << 31), PW_ERR_VALUE, "grid too large");
+  if (!c.strict && p.nx % 32 == 0 && p.ny % 32 == 0 && (long long)p.nx * p.ny >= 65536)
+    return launch_tiled<32>(c, p, states, batch, ld, nsteps, h, nsub, work);
+  if (!c.strict && p.nx % 16 == 0 && p.ny % 16 == 0)
+    return launch_tiled<16>(c, p, states, batch, ld, nsteps, h, nsub, work);
   static int max_per_sm = -1;
   if (max_per_sm < 0) {
     PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, fefb_coop, kCoopThreads, 0));
@@ -307,7 +463,6 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
   }
   const long long total = (long long)p.nx * p.ny * batch;
   long long want = (total + kCoopThreads - 1) / kCoopThreads;
-  PW_CHECK((long long)p.nx * p.ny < (1LL << 31), PW_ERR_VALUE, "grid too large");
   long long cap = (long long)c.num_sms * max_per_sm;
   int blocks = (int)std::max<long long>(1, std::min(want, cap));
   double tau = h / nsub;

@@ -51,6 +51,9 @@ struct ExactParams {
   double dx, dy, cs, a1, a2;
   const double* uf;  // (ny, nx) x-face normal velocity
   const double* vf;  // (ny, nx) y-face normal velocity
+  // 1/dx, 1/dy when dx, dy are powers of two: x/dx == x*(1/dx) exactly then,
+  // so the divisions of flux_divergence become multiplies without changing a bit
+  double inv_dx = 0.0, inv_dy = 0.0;
 };
 
 // Folded constant-velocity RK3 coefficients for one stage with factor beta

@@ -172,6 +172,22 @@ def test_propagate_api_and_composition_bitwise(dev):
         propagate(fspec, st, 0.0, 2.5 * h)
 
 
+@pytest.mark.parametrize("n", [256, 512])
+def test_tiled_coarse_bitwise_with_global_variant(dev, n):
+    """Shared-memory tiled FE-FB (T=32) == per-cell global variant (strict mode), bitwise."""
+    from paper_1510_02237_b200.integrators import SlicePropagator
+
+    _, cspec = make_specs(n)
+    q0 = torch.as_tensor(harness.fine_batch_states(n=n, batch=2, seed=13)).cuda()
+    tiled = SlicePropagator(cspec, nsteps=2).apply(q0)
+    dev.set_strict(True)
+    try:
+        ref = SlicePropagator(cspec, nsteps=2).apply(q0)
+    finally:
+        dev.set_strict(False)
+    assert torch.equal(tiled, ref)
+
+
 def test_blowup_is_not_an_error(dev):
     """Unstable coarse steps overflow quietly (integrators.py:141-145)."""
     from paper_1510_02237_b200.integrators import SlicePropagator
