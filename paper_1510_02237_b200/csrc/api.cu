@@ -228,6 +228,9 @@ struct pw_basis {
   pw_prop* coarse = nullptr;
   DBuf S, M, W, Q, Y;      // d x cap (S, M, W); d x r (Q, Y)
   DBuf Rs, tau1, tau2, diag, Q2, X, cs_work, lazy_fq, lazy_img, tmp, alpha;
+  DBuf R1;                 // unpivoted R of all snapshots (cap x cap)
+  DBuf Q1;                 // explicit orthonormal Q1 (d x cap), built column block by column block
+  int q1_cols = 0;         // snapshot columns already factored into W (incremental path)
   IBuf piv, info;
   std::vector<double> diag_h;
   std::vector<int> piv_h;
@@ -266,7 +269,100 @@ struct PhaseClock {
   }
 };
 
-void basis_refactor(pw_basis* B) {
+// Unpivoted Householder QR  S = Q1 R1  of all m snapshots, kept in factored form:
+// W holds dgeqrf's reflectors (below the diagonal) and tau1 their scales; R1 is
+// copied to a cap x cap buffer.  When the sweep appends p columns N, only they
+// are processed -- N <- Q1^T N with the stored reflectors (dormqr, BLAS3), then
+// dgeqrf of the trailing (d - m_old) x p block -- which is exactly what a blocked
+// Householder QR of the whole d x m block computes (no orthogonality loss on
+// the near-duplicate snapshots Parareal produces).  The pivoted QR of R1 below
+// then picks dgeqp3's pivots on S.
+static int solver_ws(pw_basis* B, int lw) {
+  B->cs_work.ensure(B->ctx->c, (size_t)std::max(lw, 1));
+  return (int)B->cs_work.n;
+}
+
+static void factor_full(pw_basis* B, int mr) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const int m = B->m;
+  PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
+           "snapshot block d*m exceeds the 32-bit cuSOLVER geqrf range");
+  double* W = B->W.ensure(c, (size_t)d * B->cap);
+  copy_cols(c, W, d, B->S.p, d, d, m);
+  double* tau1 = B->tau1.ensure(c, B->cap);
+  int* info = B->info.ensure(c, 1);
+  int lw = 0;
+  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)d, m, W, (int)d, &lw));
+  const int lwork = solver_ws(B, lw);
+  PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)d, m, W, (int)d, tau1, B->cs_work.p, lwork, info));
+  const size_t capc = (size_t)B->cap;
+  double* R1 = B->R1.ensure(c, capc * capc);
+  double* tmp = B->Rs.ensure(c, capc * capc);
+  pw::launch_extract_upper(c, W, d, mr, m, tmp);  // mr x m, ld mr
+  PW_CUDA(cudaMemcpy2DAsync(R1, capc * sizeof(double), tmp, mr * sizeof(double), mr * sizeof(double),
+                            m, cudaMemcpyDeviceToDevice, c.stream));
+  // explicit orthonormal Q1 (d x mr) next to the reflectors
+  double* Q1 = B->Q1.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
+  copy_cols(c, Q1, d, W, d, d, mr);
+  PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), (int)d, mr, mr, Q1, (int)d, tau1, &lw));
+  const int lwork2 = solver_ws(B, lw);
+  PW_SOLVER(cusolverDnDorgqr(solver(c), (int)d, mr, mr, Q1, (int)d, tau1, B->cs_work.p, lwork2, info));
+  B->q1_cols = mr;
+}
+
+static PhaseClock* g_clk = nullptr;  // optional fine-grained marks (PW_QR_TIMING=1)
+static void mark(const char* n) { if (g_clk) g_clk->mark(n); }
+
+static void factor_append(pw_basis* B, int m_old) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const int m = B->m, p = m - m_old;
+  const size_t capc = (size_t)B->cap;
+  PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
+           "snapshot block d*m exceeds the 32-bit cuSOLVER ormqr range");
+  double* W = B->W.p;
+  double* Wn = W + (size_t)m_old * d;
+  double* tau1 = B->tau1.p;
+  int* info = B->info.ensure(c, 1);
+  copy_cols(c, Wn, d, B->S.p + (size_t)m_old * d, d, d, p);
+  // N <- Q1^T N  (the m_old stored reflectors, applied as blocked WY updates)
+  int lw = 0;
+  PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)d, p, m_old, W,
+                                        (int)d, tau1, Wn, (int)d, &lw));
+  int lwork = solver_ws(B, lw);
+  mark("a.copy");
+  PW_SOLVER(cusolverDnDormqr(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)d, p, m_old, W, (int)d,
+                             tau1, Wn, (int)d, B->cs_work.p, lwork, info));
+  mark("a.ormqrT");
+  // Householder QR of the trailing rows m_old..d-1 of the new block
+  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)(d - m_old), p, Wn + m_old, (int)d, &lw));
+  lwork = solver_ws(B, lw);
+  PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)(d - m_old), p, Wn + m_old, (int)d, tau1 + m_old,
+                             B->cs_work.p, lwork, info));
+  mark("a.geqrf");
+  // R1[:, m_old:m] = [ (Q1^T N)[0:m_old] ; upper(R_N) ]
+  double* R1 = B->R1.p;
+  double* tmp = B->Rs.ensure(c, capc * capc);
+  PW_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Wn, d * sizeof(double), m * sizeof(double), p,
+                            cudaMemcpyDeviceToDevice, c.stream));
+  pw::launch_zero_strict_lower_block(c, tmp + m_old, m, p, p);
+  PW_CUDA(cudaMemcpy2DAsync(R1 + (size_t)m_old * capc, capc * sizeof(double), tmp, m * sizeof(double),
+                            m * sizeof(double), p, cudaMemcpyDeviceToDevice, c.stream));
+  // new explicit Q1 columns: Q_full [0; I_p; 0] with all m reflectors
+  double* Q1n = B->Q1.p + (size_t)m_old * d;
+  PW_CUDA(cudaMemsetAsync(Q1n, 0, sizeof(double) * (size_t)d * p, c.stream));
+  pw::launch_set_diag_block(c, Q1n + m_old, d, p, 1.0);
+  PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_N, (int)d, p, m, W,
+                                        (int)d, tau1, Q1n, (int)d, &lw));
+  lwork = solver_ws(B, lw);
+  mark("a.R1");
+  PW_SOLVER(cusolverDnDormqr(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_N, (int)d, p, m, W, (int)d, tau1,
+                             Q1n, (int)d, B->cs_work.p, lwork, info));
+  B->q1_cols = m;
+}
+
+void basis_refactor(pw_basis* B, int m_old) {
   Ctx& c = B->ctx->c;
   PhaseClock clk(c.stream);
   clk.mark("start");
@@ -275,27 +371,24 @@ void basis_refactor(pw_basis* B) {
   B->fq_valid = B->img_valid = false;
   B->r = 0;
   if (m == 0) return;
-  PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
-           "snapshot block d*m exceeds the 32-bit cuSOLVER geqrf/orgqr range (TSQR path not built yet)");
   const int mr = (int)std::min<long long>(d, m);  // rows of R1
-  // 1) Householder QR of the full d x m snapshot block (cuSOLVER dgeqrf)
-  double* W = B->W.ensure(c, (size_t)d * B->cap);
-  copy_cols(c, W, d, B->S.p, d, d, m);
-  double* tau1 = B->tau1.ensure(c, m);
-  int* info = B->info.ensure(c, 1);
-  int lw1 = 0, lw2 = 0;
-  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)d, m, W, (int)d, &lw1));
-  PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), (int)d, mr, mr, W, (int)d, tau1, &lw2));
-  double* work = B->cs_work.ensure(c, (size_t)std::max(lw1, lw2));
-  clk.mark("copy");
-  PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)d, m, W, (int)d, tau1, work, std::max(lw1, lw2), info));
-  clk.mark("geqrf");
-  // 2) column-pivoted QR of the mr x m factor R1 (same pivots as dgeqp3 on S)
-  double* Rs = B->Rs.ensure(c, (size_t)mr * m);
-  pw::launch_extract_upper(c, W, d, mr, m, Rs);
-  int* piv = B->piv.ensure(c, m);
-  double* tau2 = B->tau2.ensure(c, m);
-  double* diag = B->diag.ensure(c, m);
+  const size_t capc = (size_t)B->cap;
+  if (B->R1.p == nullptr) {  // R1 starts zero: its strict lower part is never written
+    B->R1.ensure(c, capc * capc);
+    PW_CUDA(cudaMemsetAsync(B->R1.p, 0, capc * capc * sizeof(double), c.stream));
+  }
+  const bool incremental = B->diff_mode && m <= d && m_old > 0 && B->q1_cols == m_old;
+  g_clk = clk.on ? &clk : nullptr;
+  if (incremental) factor_append(B, m_old);
+  else factor_full(B, mr);
+  clk.mark(incremental ? "ormqr+geqrf(new)" : "geqrf(all)");
+  // column-pivoted QR of the mr x m factor R1 (same pivots as dgeqp3 on S)
+  double* Rs = B->Rs.ensure(c, capc * capc);
+  PW_CUDA(cudaMemcpy2DAsync(Rs, mr * sizeof(double), B->R1.p, capc * sizeof(double), mr * sizeof(double),
+                            m, cudaMemcpyDeviceToDevice, c.stream));
+  int* piv = B->piv.ensure(c, capc);
+  double* tau2 = B->tau2.ensure(c, capc);
+  double* diag = B->diag.ensure(c, capc);
   int r = 0;
   pw::pivoted_qr_small(c, Rs, mr, m, B->rank_tol, piv, tau2, diag, &r);
   clk.mark("pivqr+rank");
@@ -308,18 +401,16 @@ void basis_refactor(pw_basis* B) {
     PW_CUDA(cudaStreamSynchronize(c.stream));
     return;
   }
-  // 3) explicit Q1 (d x mr), Q = Q1 Q2[:, :r]
-  PW_SOLVER(cusolverDnDorgqr(solver(c), (int)d, mr, mr, W, (int)d, tau1, work, std::max(lw1, lw2), info));
-  clk.mark("orgqr");
-  double* Q2 = B->Q2.ensure(c, (size_t)mr * r);
+  // Q = Q1 Q2[:, :r]
+  double* Q2 = B->Q2.ensure(c, capc * capc);
   pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
-  double* Q = B->Q.ensure(c, (size_t)d * r);
-  gemm(c, false, false, d, r, mr, 1.0, W, d, Q2, mr, 0.0, Q, d);
+  double* Q = B->Q.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
+  gemm(c, false, false, d, r, mr, 1.0, B->Q1.p, d, Q2, mr, 0.0, Q, d);
   clk.mark("Q=Q1Q2");
-  // 4) Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep)
-  double* X = B->X.ensure(c, (size_t)m * r);
+  // Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep)
+  double* X = B->X.ensure(c, capc * capc);
   pw::tri_inverse_scatter(c, Rs, mr, m, piv, r, X);
-  double* Y = B->Y.ensure(c, (size_t)d * r);
+  double* Y = B->Y.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
   gemm(c, false, false, d, r, m, 1.0, B->M.p, d, X, m, 0.0, Y, d);
   clk.mark("Rinv+Y");
   PW_CUDA(cudaStreamSynchronize(c.stream));
@@ -416,6 +507,13 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     PW_BLAS(cublasCreate(&h));
     PW_BLAS(cublasSetStream(h, ctx->c.stream));
     PW_BLAS(cublasSetMathMode(h, CUBLAS_DEFAULT_MATH));
+    {
+      const size_t ws = 64u << 20;  // fixed cuBLAS workspace: no allocations inside GEMM calls
+      void* wp = nullptr;
+      PW_CUDA(cudaMalloc(&wp, ws));
+      ctx->c.blas_ws = wp;
+      PW_BLAS(cublasSetWorkspace(h, wp, ws));
+    }
     ctx->c.cublas = h;
     cusolverDnHandle_t sh;
     PW_SOLVER(cusolverDnCreate(&sh));
@@ -430,6 +528,7 @@ int pw_ctx_destroy(pw_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.red) cudaFree(ctx->c.red);
+    if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
     if (ctx->c.cusolver) cusolverDnDestroy(solver(ctx->c));
     delete ctx;
@@ -568,8 +667,9 @@ int pw_basis_update(pw_basis* basis, const double* states, const double* images,
     PW_CHECK(basis, PW_ERR_VALUE, "NULL basis");
     PW_CHECK(!basis->diff_mode, PW_ERR_STATE, "sweep-internal subspace cannot be updated with images");
     PW_CHECK(p == 0 || (states && images), PW_ERR_VALUE, "NULL snapshot/image pointer");
+    const int m_old = basis->m;
     basis_append(basis, states, basis->dim, images, basis->dim, p);
-    basis_refactor(basis);
+    basis_refactor(basis, m_old);
   });
 }
 
@@ -738,12 +838,13 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       double* alpha = nullptr;
       double* alpha_next = nullptr;
       if (kse) {
+        const int m_old = B->m;
         basis_append(B.get(), QK, d, PRED, d, n_c);
-        basis_refactor(B.get());
+        basis_refactor(B.get(), m_old);
         r = B->r;
         if (ranks) ranks[k] = r;
         if (r > 0) {
-          double* ab = bAlpha.ensure(c, (size_t)r * (n_c + 2));
+          double* ab = bAlpha.ensure(c, (size_t)std::min<long long>(B->cap, d) * (n_c + 2));
           gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
           gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           alpha = ab;                             // column 0 = Q^T q0
@@ -753,7 +854,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       if (timed) PW_CUDA(cudaEventRecord(ev[2], c.stream));
       // serial correction sweep (parareal.py:128-132)
       copy_cols(c, QN, d, q0, d, d, 1);
-      double* part = bPart.ensure(c, pw::combine_part_doubles(d, r));
+      double* part = bPart.ensure(c, pw::combine_part_doubles(d, kse ? (int)std::min<long long>(B->cap, d) : 1));
       double* a_cur = alpha;
       double* a_buf[2] = {alpha_next, alpha_next ? alpha_next + r : nullptr};
       for (int i = 0; i < n_c; ++i) {

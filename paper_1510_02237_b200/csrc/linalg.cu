@@ -407,6 +407,21 @@ __global__ void extract_upper_kernel(const double* __restrict__ W, long long ldw
   }
 }
 
+// zero the strict lower triangle of a rows x cols block (leading dim ld)
+__global__ void zero_strict_lower_kernel(double* __restrict__ A, long long ld, int rows, int cols) {
+  const long long total = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(idx / rows), row = (int)(idx % rows);
+    if (row > col) A[(long long)col * ld + row] = 0.0;
+  }
+}
+
+__global__ void set_diag_kernel(double* __restrict__ A, long long ld, int k, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) A[(long long)i * ld + i] = v;
+}
+
 int g_pqr_blocks_per_sm = -1;
 
 }  // namespace
@@ -432,6 +447,22 @@ void launch_extract_upper(Ctx& c, const double* W, long long ldw, int mr, int m,
   const long long total = (long long)mr * m;
   int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c.num_sms * 8));
   extract_upper_kernel<<<blocks, 256, 0, c.stream>>>(W, ldw, mr, m, R);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void launch_zero_strict_lower_block(Ctx& c, double* A, long long ld, int rows, int cols) {
+  const long long total = (long long)rows * cols;
+  if (total <= 0) return;
+  int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c.num_sms * 8));
+  zero_strict_lower_kernel<<<blocks, 256, 0, c.stream>>>(A, ld, rows, cols);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void launch_set_diag_block(Ctx& c, double* A, long long ld, int k, double v) {
+  if (k <= 0) return;
+  set_diag_kernel<<<(k + 255) / 256, 256, 0, c.stream>>>(A, ld, k, v);
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }

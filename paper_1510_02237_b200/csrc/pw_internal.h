@@ -88,6 +88,7 @@ struct Ctx {
   int num_sms = 0;
   void* cublas = nullptr;    // cublasHandle_t
   void* cusolver = nullptr;  // cusolverDnHandle_t
+  void* blas_ws = nullptr;   // fixed cuBLAS workspace
   // scratch for grid barriers / reductions
   double* red = nullptr;     // reduction scratch (doubles)
   size_t red_cap = 0;
@@ -117,6 +118,8 @@ bool fused_supported(int nx, int ny);
 void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,
                        double beta, size_t n);
 void launch_extract_upper(Ctx& c, const double* W, long long ldw, int mr, int m, double* R);
+void launch_zero_strict_lower_block(Ctx& c, double* A, long long ld, int rows, int cols);
+void launch_set_diag_block(Ctx& c, double* A, long long ld, int k, double v);
 size_t residual_scratch_doubles(int ncols, long long nrows);
 void launch_residual(Ctx& c, const double* a, long long lda, const double* b, long long ldb,
                      int ncols, long long nrows, double* scratch, double* out_dev);

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_full.log 2>&1
+echo "bench rc=$?" >> gpurun_out/bench_full.log

@@ -44,6 +44,11 @@ elif what in ("c3k2", "c3k5"):
     f, c = specs(wl.n)
     fine, coarse = SlicePropagator(f, wl.slice_span), SlicePropagator(c, wl.slice_span)
     q0 = torch.as_tensor(harness.initial_state("c3")).cuda()
-    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, 2 if what == "c3k2" else 5, return_device=True)
+    k = 2 if what == "c3k2" else 5
+    if os.environ.get("PW_WARM") == "1":
+        kse_sweep(q0, fine, coarse, wl.n_p, k, return_device=True)
+        torch.cuda.synchronize()
+        print("---- warm")
+    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, k, return_device=True)
     torch.cuda.synchronize()
     print("c3k2 ok", res, sub.rank)
