@@ -222,6 +222,44 @@ def test_c1_original_matches_reference():
         assert rel(ends[i], g["orig_final"][i]) <= 1e-12
 
 
+def test_c1_kse_strict_mode_matches_reference(dev):
+    """Every kernel in reference operation order (strict): the c1 window vs the reference run."""
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    g = golden("c1_kse.npz")
+    wl, fine, coarse = c1_props()
+    dev.set_strict(True)
+    try:
+        ends, res, sub = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    finally:
+        dev.set_strict(False)
+    assert sub.rank == g["kse_ranks"][-1]
+    worst = max(rel(ends[i], g["kse_hist"][-1][i]) for i in range(wl.n_p))
+    assert worst <= 1e-12, worst
+    np.testing.assert_allclose(res, g["kse_res"], rtol=1e-12)
+
+
+def test_edge_cases_zero_state_single_slice_and_tol():
+    """Zero initial state (empty subspace: rank 0), n_c = 1, and a PDE tol early exit."""
+    from paper_1510_02237_b200.parareal import kse_sweep, parareal_sweep
+
+    wl, fine, coarse = c1_props()
+    d = 3 * wl.n * wl.n
+    ends, res, sub = kse_sweep(np.zeros(d), fine, coarse, 4, 2)
+    assert sub.rank == 0 and res == [0.0, 0.0]
+    assert all(np.count_nonzero(e) == 0 for e in ends)
+    q0 = harness.initial_state("c1")
+    ends1, res1, _ = kse_sweep(q0, fine, coarse, 1, 2)
+    np.testing.assert_allclose(ends1[0], fine(q0), rtol=0, atol=1e-14)   # one slice: exact after 1 iteration
+    assert res1[1] == 0.0
+    _, res_t = parareal_sweep(q0, fine, coarse, wl.n_p, 12, tol=1e-6)
+    assert len(res_t) <= wl.n_p + 1 and res_t[-1] <= 1e-6     # exact after n_c iterations
+    with pytest.raises(ValueError):
+        kse_sweep(q0, fine, coarse, 0, 1)
+    with pytest.raises(ValueError):
+        kse_sweep(q0[:-3], fine, coarse, 2, 1)
+
+
 def test_pde8_production_window_matches_reference():
     """nx=8 solid-body production window (reference tests/test_parareal.py:245-265 seam)."""
     from paper_1510_02237_b200.integrators import RK3, SPLIT_FE_FB, make_propagator
