@@ -10,6 +10,7 @@
 #include <cusolverDn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -519,6 +520,11 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     PW_SOLVER(cusolverDnCreate(&sh));
     PW_SOLVER(cusolverDnSetStream(sh, ctx->c.stream));
     ctx->c.cusolver = sh;
+    PW_CUDA(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
+    PW_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming));
+    PW_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming));
+    if (const char* e = std::getenv("PW_COOP_CAP")) ctx->c.sweep_coop_cap = std::atoi(e);
+    if (const char* e = std::getenv("PW_SWEEP_OVERLAP")) ctx->c.sweep_overlap = std::atoi(e) != 0;
     *out = ctx.release();
   });
 }
@@ -531,6 +537,12 @@ int pw_ctx_destroy(pw_ctx* ctx) {
     if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
     if (ctx->c.cusolver) cusolverDnDestroy(solver(ctx->c));
+    if (ctx->c.side) {
+      cudaStreamSynchronize(ctx->c.side);
+      cudaStreamDestroy(ctx->c.side);
+    }
+    if (ctx->c.ev_fork) cudaEventDestroy(ctx->c.ev_fork);
+    if (ctx->c.ev_join) cudaEventDestroy(ctx->c.ev_join);
     delete ctx;
   });
 }
@@ -787,7 +799,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     const long long d = fine->dim;
     const bool kse = mode == PW_MODE_KSE;
     // buffers (column-major, ld = d)
-    DBuf bQK, bQN, bPred, bGK, bGN, bRes, bScr, bAlpha, bPart;
+    DBuf bQK, bQN, bPred, bGK, bGN, bRes, bScr, bAlpha, bPart, bYt;
     double* QK = bQK.ensure(c, (size_t)d * (n_c + 1));
     double* QN = bQN.ensure(c, (size_t)d * (n_c + 1));
     double* PRED = bPred.ensure(c, (size_t)d * n_c);
@@ -857,13 +869,39 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       double* part = bPart.ensure(c, pw::combine_part_doubles(d, kse ? (int)std::min<long long>(B->cap, d) : 1));
       double* a_cur = alpha;
       double* a_buf[2] = {alpha_next, alpha_next ? alpha_next + r : nullptr};
-      for (int i = 0; i < n_c; ++i) {
-        prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
-        double* a_nxt = (r > 0) ? a_buf[i % 2] : nullptr;
-        pw::launch_combine_gemv(c, GN + (size_t)i * d, B ? B->Y.p : nullptr, PRED + (size_t)i * d,
-                                a_cur, B ? B->Q.p : nullptr, r, d, QN + (size_t)(i + 1) * d, a_nxt,
-                                part);
-        a_cur = a_nxt;
+      if (r > 0 && c.sweep_overlap) {
+        // Two streams per correction step i:
+        //   side: y_i = c_i + D alpha_i            (waits for alpha_i)
+        //   main: G(qn_i); qn_{i+1} = G + y_i;  alpha_{i+1} = Q^T qn_{i+1}
+        // so the D pass (r*d*8 bytes) streams while the latency-bound coarse G runs.
+        double* Yt = bYt.ensure(c, (size_t)d * 2);
+        PW_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        const int saved_cap = c.coop_blocks_per_sm;
+        c.coop_blocks_per_sm = c.sweep_coop_cap;
+        for (int i = 0; i < n_c; ++i) {
+          double* yi = Yt + (size_t)(i % 2) * d;
+          PW_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+          pw::launch_combine_gemv(c, c.side, nullptr, B->Y.p, r, PRED + (size_t)i * d, a_cur, nullptr,
+                                  0, d, yi, nullptr, nullptr);
+          PW_CUDA(cudaEventRecord(c.ev_join, c.side));
+          prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
+          PW_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+          double* a_nxt = a_buf[i % 2];
+          pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, nullptr, 0, yi, nullptr, B->Q.p, r, d,
+                                  QN + (size_t)(i + 1) * d, a_nxt, part);
+          PW_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          a_cur = a_nxt;
+        }
+        c.coop_blocks_per_sm = saved_cap;
+      } else {
+        for (int i = 0; i < n_c; ++i) {
+          prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
+          double* a_nxt = (r > 0) ? a_buf[i % 2] : nullptr;
+          pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B ? B->Y.p : nullptr, r,
+                                  PRED + (size_t)i * d, a_cur, B ? B->Q.p : nullptr, r, d,
+                                  QN + (size_t)(i + 1) * d, a_nxt, part);
+          a_cur = a_nxt;
+        }
       }
       pw::launch_residual(c, QK + d, d, QN + d, d, n_c, d, scr, res_dev + k);
       if (timed) {

@@ -439,7 +439,8 @@ static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch
     if (per_sm < 1) per_sm = 1;
   }
   const long long items = (long long)(p.nx / T) * (p.ny / T) * batch;
-  int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * per_sm));
+  const int cap_sm = c.coop_blocks_per_sm > 0 ? std::min(per_sm, c.coop_blocks_per_sm) : per_sm;
+  int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * cap_sm));
   double tau = h / nsub;
   ExactParams pp = p;
   void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work};

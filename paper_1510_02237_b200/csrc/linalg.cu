@@ -253,15 +253,18 @@ __device__ __forceinline__ void flush_wpart(const double* wpart, int r, double* 
   }
 }
 
+// y = [g +] c + D alpha  (rd columns of D)  and  part = Q^T y partials (rq columns of Q);
+// g may be NULL, rd or rq may be 0 (the overlapped sweep runs the D pass and the Q pass
+// as separate launches, the D pass concurrently with the coarse propagator).
 __global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
-    const double* __restrict__ g, const double* __restrict__ D, const double* __restrict__ cvec,
-    const double* __restrict__ alpha, const double* __restrict__ Q, int r, long long d,
+    const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
+    const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d,
     double* __restrict__ y_out, double* __restrict__ part) {
   extern __shared__ double sh[];
-  double* a_s = sh;            // r
-  double* wpart = sh + r;      // kCgWarps x r
-  for (int k = threadIdx.x; k < r; k += blockDim.x) a_s[k] = alpha[k];
-  for (int k = threadIdx.x; k < kCgWarps * r; k += blockDim.x) wpart[k] = 0.0;
+  double* a_s = sh;             // rd
+  double* wpart = sh + rd;      // kCgWarps x rq
+  for (int k = threadIdx.x; k < rd; k += blockDim.x) a_s[k] = alpha[k];
+  for (int k = threadIdx.x; k < kCgWarps * rq; k += blockDim.x) wpart[k] = 0.0;
   __syncthreads();
   const long long ntiles = (d + kCgRows - 1) / kCgRows;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -270,11 +273,11 @@ __global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
 #pragma unroll
     for (int s = 0; s < kCgRpt; ++s) {
       const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-      y[s] = row < d ? g[row] + cvec[row] : 0.0;
+      y[s] = row < d ? (g ? g[row] + cvec[row] : cvec[row]) : 0.0;
     }
     // y += D alpha  (column-major D: every column read as one coalesced 8 KB run)
     int k = 0;
-    for (; k + 4 <= r; k += 4) {
+    for (; k + 4 <= rd; k += 4) {
       double t[4][kCgRpt];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
 #pragma unroll
         for (int s = 0; s < kCgRpt; ++s) y[s] = fma(t[kk][s], a_s[k + kk], y[s]);
     }
-    for (; k < r; ++k) {
+    for (; k < rd; ++k) {
 #pragma unroll
       for (int s = 0; s < kCgRpt; ++s) {
         const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
@@ -300,9 +303,9 @@ __global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
       const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
       if (row < d) y_out[row] = y[s];
     }
-    if (r > 0) tile_qty(Q, r, d, row0, y, wpart);
+    if (rq > 0) tile_qty(Q, rq, d, row0, y, wpart);
   }
-  if (r > 0) flush_wpart(wpart, r, part);
+  if (rq > 0) flush_wpart(wpart, rq, part);
 }
 
 __global__ void __launch_bounds__(kCgThreads, 2) project_partial_kernel(
@@ -551,20 +554,20 @@ static int combine_grid(const Ctx& c, long long d) {
   return (int)std::max<long long>(1, std::min<long long>(ntiles, 2LL * c.num_sms));
 }
 
-void launch_combine_gemv(Ctx& c, const double* g, const double* D, const double* cvec,
-                         const double* alpha, const double* Q, int r, long long d, double* y,
-                         double* alpha_next, double* part) {
-  const int nblk = combine_grid(c, d);
-  size_t smem = sizeof(double) * ((size_t)r * (1 + kCgWarps) + 1);
+void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
+                         const double* cvec, const double* alpha, const double* Q, int rq,
+                         long long d, double* y, double* alpha_next, double* part, int nblk) {
+  if (nblk <= 0) nblk = combine_grid(c, d);
+  size_t smem = sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 1);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     PW_CUDA(cudaFuncSetAttribute(combine_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  combine_gemv_kernel<<<nblk, kCgThreads, smem, c.stream>>>(g, D, cvec, alpha, Q, r, d, y, part);
+  combine_gemv_kernel<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, y, part);
   c.launches += 1;
-  if (r > 0) {
-    reduce_parts_kernel<<<(r + 31) / 32, 256, 0, c.stream>>>(part, nblk, r, alpha_next);
+  if (rq > 0) {
+    reduce_parts_kernel<<<(rq + 31) / 32, 256, 0, st>>>(part, nblk, rq, alpha_next);
     c.launches += 1;
   }
   PW_LAUNCH_CHECK();
