@@ -41,6 +41,19 @@ N_GRID = 256
 BATCH = 64
 STEPS_PER_SAMPLE = 200
 BYTES_PER_CELL_UPDATE = 48  # read (u,v,p) + write (u,v,p), fp64
+# fp64 flops of the folded constant-velocity RK3 form per cell-update (FMA = 2 flop, halo
+# recompute excluded): stage 1 = 65, stages 2 and 3 = 68 (+ the q base)
+FLOP_PER_CELL_UPDATE = 201
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "fine_traffic.json")
+
+
+def load_traffic():
+    """DRAM bytes per rk3_fused_kernel launch from the committed ncu --set full capture."""
+    if os.path.exists(TRAFFIC_FILE):
+        with open(TRAFFIC_FILE) as fh:
+            d = json.load(fh)
+        return float(d["dram_bytes_per_launch"]), d.get("source")
+    return None, None
 
 
 def load_peaks():
@@ -53,52 +66,87 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every ~5 ms during the timed region
+    (NVML through pynvml; `nvidia-smi -lms 100` when pynvml is unavailable)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.005):
         self.index = index
-        self.rows = []
+        self.period = period_s
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
         self.proc = None
+        self.stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.rows.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                          float(mx), int(get_reasons(h))))
+                    except Exception:  # noqa: BLE001 - sampling is best effort
+                        pass
+                    self.stop.wait(self.period)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+            self.source = "nvml"
+        except Exception:  # noqa: BLE001
+            self._start_smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+    def _start_smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.source = "nvidia-smi"
+
+        def read():
+            for line in self.proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except (ValueError, IndexError):
+                    pass
+
+        self.thread = threading.Thread(target=read, daemon=True)
+        self.thread.start()
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread is not None:
             self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for r in self.rows for name, bit in self.REASONS if r[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(self.rows),
+                "source": getattr(self, "source", None)}
 
 
 def cpu_baseline(seconds_target=12.0):
@@ -260,6 +308,9 @@ def run_ours(args, rank, world, local_rank):
     launch_s = (ms_per_step * 1e-3) / STEPS_PER_SAMPLE
     algo_bytes = BYTES_PER_CELL_UPDATE * BATCH * N_GRID * N_GRID
     achieved = algo_bytes / launch_s / 1e9
+    traffic, traffic_src = load_traffic()
+    fp64_peak = ctx.fp64_peak_tflops() if rank == 0 else None  # outside the timed region
+    fp64_achieved = FLOP_PER_CELL_UPDATE * value / world / 1e12
 
     extra = {}
     if rank == 0 and world == 1 and args.parareal:
@@ -277,11 +328,16 @@ def run_ours(args, rank, world, local_rank):
                        "l2": "256 MiB flush between timed steps; the 200 chained RK3 launches inside a "
                              "step keep their natural L2 reuse"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "avg_launch_us": launch_s * 1e6,
-                         "kernel": "rk3_fused_kernel (one launch per RK3 step over all 64 states)"},
+                         "kernel": "rk3_fused_kernel (one launch per RK3 step over all 64 states)",
+                         "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                                  "frac": (fp64_achieved / fp64_peak) if fp64_peak else None,
+                                  "flop_per_cell_update": FLOP_PER_CELL_UPDATE,
+                                  "peak_source": "measured live: DFMA probe kernel (pw_probe_fp64_peak)"}},
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": int(q_host.numel() * 8),
                     "d2h_bytes_per_step": int(q_host.numel() * 8), "finite": ok},
             "gpu_launches": int(launches),

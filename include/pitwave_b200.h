@@ -152,6 +152,10 @@ int pw_copy(pw_ctx* ctx, void* dst, const void* src, long long nbytes);
 int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long dim,
                 double* out_host);
 
+/* fp64 pipe peak (TFLOP/s) from a DFMA-throughput probe kernel: the fp64
+ * half of the roofline; no reference counterpart. */
+int pw_probe_fp64_peak(pw_ctx* ctx, int iters, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("pw_ctx_set_fine_hook", ctypes.c_int, [c_vp, FINE_HOOK, c_vp]),
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
+    ("pw_probe_fp64_peak", ctypes.c_int, [c_vp, ctypes.c_int, c_dp]),
 ]
 
 _lib = None
@@ -163,6 +164,12 @@ class Context:
 
     def synchronize(self):
         check(self.lib.pw_ctx_synchronize(self.handle))
+
+    def fp64_peak_tflops(self, iters: int = 4096) -> float:
+        """DFMA-throughput probe (TFLOP/s, FMA = 2 flop): the fp64 roofline denominator."""
+        out = ctypes.c_double()
+        check(self.lib.pw_probe_fp64_peak(self.handle, int(iters), ctypes.byref(out)))
+        return float(out.value)
 
 
 def ptr(t: torch.Tensor):

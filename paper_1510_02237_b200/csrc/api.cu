@@ -547,6 +547,13 @@ int pw_ctx_destroy(pw_ctx* ctx) {
   });
 }
 
+int pw_probe_fp64_peak(pw_ctx* ctx, int iters, double* tflops) {
+  return guarded([&] {
+    PW_CHECK(ctx && tflops && iters > 0, PW_ERR_VALUE, "bad argument");
+    *tflops = pw::probe_fp64_tflops(ctx->c, iters);
+  });
+}
+
 int pw_ctx_set_stream(pw_ctx* ctx, void* stream) {
   return guarded([&] {
     PW_CHECK(ctx, PW_ERR_VALUE, "ctx is NULL");

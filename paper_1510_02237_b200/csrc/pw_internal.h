@@ -131,6 +131,9 @@ void launch_set_diag_block(Ctx& c, double* A, long long ld, int k, double v);
 size_t residual_scratch_doubles(int ncols, long long nrows);
 void launch_residual(Ctx& c, const double* a, long long lda, const double* b, long long ldb,
                      int ncols, long long nrows, double* scratch, double* out_dev);
+// fp64 pipe peak probe (probe.cu): best-of-3 DFMA throughput in TFLOP/s
+double probe_fp64_tflops(Ctx& c, int iters);
+
 size_t combine_part_doubles(long long d, int r);
 // R: mr x m (lda mr), mr = min(d, m); returns rank, fills piv (m), tau/diag (min(mr, m))
 int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv_dev,
