@@ -278,7 +278,33 @@ struct PhaseClock {
 // Householder QR of the whole d x m block computes (no orthogonality loss on
 // the near-duplicate snapshots Parareal produces).  The pivoted QR of R1 below
 // then picks dgeqp3's pivots on S.
+static PhaseClock* g_clk = nullptr;  // optional fine-grained marks (PW_QR_TIMING=1)
+static void mark(const char* n) { if (g_clk) g_clk->mark(n); }
+
+// cuSOLVER workspace, sized once for the largest call this basis can make (geqrf / orgqr /
+// ormqr at m = capacity): growing it update by update re-allocated (and re-mapped) pool
+// memory inside the refactorisation and stalled the stream for up to ~0.2 s.
+static void presize_solver_ws(pw_basis* B) {
+  if (B->cs_work.p) return;
+  Ctx& c = B->ctx->c;
+  const int d = (int)B->dim;
+  const int cap = (int)std::min<long long>(B->cap, B->dim);
+  double* any = B->S.p;  // size queries only: the pointers are not dereferenced
+  int lw = 1, t = 0;
+  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), d, cap, any, d, &t));
+  lw = std::max(lw, t);
+  PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), d, cap, cap, any, d, any, &t));
+  lw = std::max(lw, t);
+  for (cublasOperation_t op : {CUBLAS_OP_T, CUBLAS_OP_N}) {
+    PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, op, d, cap, cap, any, d, any,
+                                          any, d, &t));
+    lw = std::max(lw, t);
+  }
+  B->cs_work.ensure(c, (size_t)lw);
+}
+
 static int solver_ws(pw_basis* B, int lw) {
+  presize_solver_ws(B);
   B->cs_work.ensure(B->ctx->c, (size_t)std::max(lw, 1));
   return (int)B->cs_work.n;
 }
@@ -290,9 +316,11 @@ static void factor_full(pw_basis* B, int mr) {
   PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
            "snapshot block d*m exceeds the 32-bit cuSOLVER geqrf range");
   double* W = B->W.ensure(c, (size_t)d * B->cap);
-  copy_cols(c, W, d, B->S.p, d, d, m);
   double* tau1 = B->tau1.ensure(c, B->cap);
   int* info = B->info.ensure(c, 1);
+  presize_solver_ws(B);
+  mark("full.alloc");
+  copy_cols(c, W, d, B->S.p, d, d, m);
   int lw = 0;
   PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)d, m, W, (int)d, &lw));
   const int lwork = solver_ws(B, lw);
@@ -312,8 +340,6 @@ static void factor_full(pw_basis* B, int mr) {
   B->q1_cols = mr;
 }
 
-static PhaseClock* g_clk = nullptr;  // optional fine-grained marks (PW_QR_TIMING=1)
-static void mark(const char* n) { if (g_clk) g_clk->mark(n); }
 
 static void factor_append(pw_basis* B, int m_old) {
   Ctx& c = B->ctx->c;
@@ -347,13 +373,18 @@ static void factor_append(pw_basis* B, int m_old) {
   double* tmp = B->Rs.ensure(c, capc * capc);
   PW_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Wn, d * sizeof(double), m * sizeof(double), p,
                             cudaMemcpyDeviceToDevice, c.stream));
+  mark("r1.copy1");
   pw::launch_zero_strict_lower_block(c, tmp + m_old, m, p, p);
+  mark("r1.zero");
   PW_CUDA(cudaMemcpy2DAsync(R1 + (size_t)m_old * capc, capc * sizeof(double), tmp, m * sizeof(double),
                             m * sizeof(double), p, cudaMemcpyDeviceToDevice, c.stream));
+  mark("r1.copy2");
   // new explicit Q1 columns: Q_full [0; I_p; 0] with all m reflectors
   double* Q1n = B->Q1.p + (size_t)m_old * d;
   PW_CUDA(cudaMemsetAsync(Q1n, 0, sizeof(double) * (size_t)d * p, c.stream));
+  mark("r1.memset");
   pw::launch_set_diag_block(c, Q1n + m_old, d, p, 1.0);
+  mark("r1.diag");
   PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_N, (int)d, p, m, W,
                                         (int)d, tau1, Q1n, (int)d, &lw));
   lwork = solver_ws(B, lw);

@@ -218,7 +218,38 @@ __device__ __forceinline__ double transpose_reduce8(double (&acc)[8]) {
   return v;
 }
 
+// Row ownership inside a 1024-row tile: scalar layout, row(s) = row0 + tid + 256 s; paired
+// layout (V2, d even), row(s) = row0 + 512 (s/2) + 2 tid + (s%2), loaded as 16-byte pairs.
+template <bool V2>
+__device__ __forceinline__ long long cg_row(long long row0, int s) {
+  if constexpr (V2) return row0 + (long long)(s >> 1) * (2 * kCgThreads) + 2 * threadIdx.x + (s & 1);
+  else return row0 + threadIdx.x + (long long)s * kCgThreads;
+}
+
+// v[s] = col[row(s)] (0 beyond d), streaming (evict-first) loads
+template <bool V2>
+__device__ __forceinline__ void cg_load(const double* __restrict__ col, long long row0, long long d,
+                                        double (&v)[kCgRpt]) {
+  if constexpr (V2) {
+#pragma unroll
+    for (int h = 0; h < kCgRpt / 2; ++h) {
+      const long long row = cg_row<true>(row0, 2 * h);
+      double2 t = make_double2(0.0, 0.0);
+      if (row < d) t = __ldcs(reinterpret_cast<const double2*>(col + row));
+      v[2 * h] = t.x;
+      v[2 * h + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < kCgRpt; ++s) {
+      const long long row = cg_row<false>(row0, s);
+      v[s] = row < d ? __ldcs(col + row) : 0.0;
+    }
+  }
+}
+
 // wpart[warp][k] += sum over this tile's rows of Q[row, k] * y[row]
+template <bool V2>
 __device__ __forceinline__ void tile_qty(const double* __restrict__ Q, int r, long long d,
                                          long long row0, const double (&y)[kCgRpt],
                                          double* __restrict__ wpart) {
@@ -226,16 +257,13 @@ __device__ __forceinline__ void tile_qty(const double* __restrict__ Q, int r, lo
   for (int k0 = 0; k0 < r; k0 += 8) {
     double acc[8];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.0;
-#pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
+      acc[kk] = 0.0;
       if (k0 + kk < r) {
-        const double* Qk = Q + (long long)(k0 + kk) * d;
+        double q[kCgRpt];
+        cg_load<V2>(Q + (long long)(k0 + kk) * d, row0, d, q);
 #pragma unroll
-        for (int s = 0; s < kCgRpt; ++s) {
-          const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-          if (row < d) acc[kk] = fma(__ldcs(Qk + row), y[s], acc[kk]);
-        }
+        for (int s = 0; s < kCgRpt; ++s) acc[kk] = fma(q[s], y[s], acc[kk]);
       }
     }
     const double v = transpose_reduce8(acc);
@@ -256,7 +284,8 @@ __device__ __forceinline__ void flush_wpart(const double* wpart, int r, double* 
 // y = [g +] c + D alpha  (rd columns of D)  and  part = Q^T y partials (rq columns of Q);
 // g may be NULL, rd or rq may be 0 (the overlapped sweep runs the D pass and the Q pass
 // as separate launches, the D pass concurrently with the coarse propagator).
-__global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
+template <int UNR, int MINB, bool V2>
+__global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
     const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
     const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d,
     double* __restrict__ y_out, double* __restrict__ part) {
@@ -272,38 +301,32 @@ __global__ void __launch_bounds__(kCgThreads, 2) combine_gemv_kernel(
     double y[kCgRpt];
 #pragma unroll
     for (int s = 0; s < kCgRpt; ++s) {
-      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      const long long row = cg_row<V2>(row0, s);
       y[s] = row < d ? (g ? g[row] + cvec[row] : cvec[row]) : 0.0;
     }
     // y += D alpha  (column-major D: every column read as one coalesced 8 KB run)
     int k = 0;
-    for (; k + 4 <= rd; k += 4) {
-      double t[4][kCgRpt];
+    for (; k + UNR <= rd; k += UNR) {
+      double t[UNR][kCgRpt];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
+      for (int kk = 0; kk < UNR; ++kk) cg_load<V2>(D + (long long)(k + kk) * d, row0, d, t[kk]);
 #pragma unroll
-        for (int s = 0; s < kCgRpt; ++s) {
-          const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-          t[kk][s] = row < d ? __ldcs(D + (long long)(k + kk) * d + row) : 0.0;
-        }
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
+      for (int kk = 0; kk < UNR; ++kk)
 #pragma unroll
         for (int s = 0; s < kCgRpt; ++s) y[s] = fma(t[kk][s], a_s[k + kk], y[s]);
     }
     for (; k < rd; ++k) {
+      double t[kCgRpt];
+      cg_load<V2>(D + (long long)k * d, row0, d, t);
 #pragma unroll
-      for (int s = 0; s < kCgRpt; ++s) {
-        const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
-        if (row < d) y[s] = fma(__ldcs(D + (long long)k * d + row), a_s[k], y[s]);
-      }
+      for (int s = 0; s < kCgRpt; ++s) y[s] = fma(t[s], a_s[k], y[s]);
     }
 #pragma unroll
     for (int s = 0; s < kCgRpt; ++s) {
-      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      const long long row = cg_row<V2>(row0, s);
       if (row < d) y_out[row] = y[s];
     }
-    if (rq > 0) tile_qty(Q, rq, d, row0, y, wpart);
+    if (rq > 0) tile_qty<V2>(Q, rq, d, row0, y, wpart);
   }
   if (rq > 0) flush_wpart(wpart, rq, part);
 }
@@ -320,10 +343,10 @@ __global__ void __launch_bounds__(kCgThreads, 2) project_partial_kernel(
     double y[kCgRpt];
 #pragma unroll
     for (int s = 0; s < kCgRpt; ++s) {
-      const long long row = row0 + threadIdx.x + (long long)s * kCgThreads;
+      const long long row = cg_row<false>(row0, s);
       y[s] = row < d ? v[row] : 0.0;
     }
-    tile_qty(Q, r, d, row0, y, wpart);
+    tile_qty<false>(Q, r, d, row0, y, wpart);
   }
   flush_wpart(wpart, r, part);
 }
@@ -549,22 +572,60 @@ void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv,
   PW_LAUNCH_CHECK();
 }
 
-static int combine_grid(const Ctx& c, long long d) {
+static int cg_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PW_CG_VARIANT");  // tuning hook (scripts/ubench_gemv.cu)
+    v = (e && *e) ? atoi(e) : 0;
+  }
+  return v;
+}
+
+// persistent grid of at most per_sm CTAs per SM, sized so every CTA walks the same number of
+// 1024-row tiles (768 tiles at c3 -> 384 CTAs x 2 tiles instead of 444 CTAs x 1.73)
+static int combine_grid(const Ctx& c, long long d, int per_sm = 2) {
   const long long ntiles = (d + kCgRows - 1) / kCgRows;
-  return (int)std::max<long long>(1, std::min<long long>(ntiles, 2LL * c.num_sms));
+  const long long cap = std::max<long long>(1, (long long)per_sm * c.num_sms);
+  const long long per_cta = (ntiles + cap - 1) / cap;
+  return (int)std::max<long long>(1, (ntiles + per_cta - 1) / per_cta);
+}
+
+template <int UNR, int MINB, bool V2>
+static int launch_cg(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
+                      const double* cvec, const double* alpha, const double* Q, int rq, long long d,
+                      double* y, double* part, int nblk) {
+  auto kern = combine_gemv_kernel<UNR, MINB, V2>;
+  if (nblk <= 0) nblk = combine_grid(c, d, MINB);
+  size_t smem = sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 1);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  kern<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, y, part);
+  return nblk;
 }
 
 void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                          const double* cvec, const double* alpha, const double* Q, int rq,
                          long long d, double* y, double* alpha_next, double* part, int nblk) {
-  if (nblk <= 0) nblk = combine_grid(c, d);
-  size_t smem = sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 1);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    PW_CUDA(cudaFuncSetAttribute(combine_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+  const bool v2 = (d % 2 == 0);  // 16-byte pairs need every column 16-byte aligned
+  switch (cg_variant()) {
+    case 1: nblk = launch_cg<4, 2, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk); break;
+    case 2: nblk = launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk); break;
+    case 3:
+      nblk = v2 ? launch_cg<4, 4, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk)
+                : launch_cg<4, 4, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk);
+      break;
+    case 4:
+      nblk = v2 ? launch_cg<8, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk)
+                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk);
+      break;
+    default:
+      nblk = v2 ? launch_cg<4, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk)
+                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk);
+      break;
   }
-  combine_gemv_kernel<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, y, part);
   c.launches += 1;
   if (rq > 0) {
     reduce_parts_kernel<<<(rq + 31) / 32, 256, 0, st>>>(part, nblk, rq, alpha_next);
