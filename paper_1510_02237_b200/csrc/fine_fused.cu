@@ -114,7 +114,7 @@ struct Ring {
 // whose column c+E.. corresponds to output col c -- the x-window of output col
 // c starts at input col c (x offset -4).  q base at q-ring col c + S*E.
 template <class K>
-__device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, int rel0, int c,
+__device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, int s_q, int s_in, int c,
                                            const StageCoef& C, double (&au)[K::BY][K::BX],
                                            double (&av)[K::BY][K::BX], double (&ap)[K::BY][K::BX]) {
   constexpr int BX = K::BX, BY = K::BY;
@@ -124,7 +124,7 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
   // it into the stencil centre instead (its input ring is q itself)
   double qb[3][BY][BX];
   if (S != 1) {
-    int s = rel0 % qr.n;
+    int s = s_q;
 #pragma unroll
     for (int r = 0; r < BY; ++r) {
       const RowP q = rowp_of(qr.base + (size_t)s * qr.pitch, s, c);
@@ -138,7 +138,7 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
   constexpr int NR = BY + 2 * K::RY;
   RowP rows[NR];
   {
-    int s = (rel0 - K::RY) % in.n;
+    int s = s_in;
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
       rows[k] = rowp_of(in.base + (size_t)s * in.pitch, s, c);
@@ -327,8 +327,11 @@ __global__ void __launch_bounds__(K::NT, 1) rk3_fused_kernel(const double* __res
   constexpr int CH = (K::TX + 6 * E) / 2;
   constexpr int PER_ROW = 3 * CH;
   constexpr int NLD = (K::R * PER_ROW + K::NT - 1) / K::NT;
-  int ld_rr[NLD], ld_soff[NLD];
+  // per load: smem offset inside a slot, global column offset, and the ring slot / global
+  // row of the next tick's row (advanced by R per tick: no division in the tick loop)
+  int ld_soff[NLD], ld_slot[NLD], ld_gy[NLD];
   long long ld_goff[NLD];
+  bool ld_on[NLD];
 #pragma unroll
   for (int k = 0; k < NLD; ++k) {
     const int e = tid + k * K::NT;
@@ -338,39 +341,47 @@ __global__ void __launch_bounds__(K::NT, 1) rk3_fused_kernel(const double* __res
     const int col = 2 * (rem - f * CH);
     int gx = x0 - 3 * E + col;
     if (gx < 0 || gx >= nx) gx = wrapi(gx, nx);
-    ld_rr[k] = (e < K::R * PER_ROW) ? rr : -1;
+    ld_on[k] = e < K::R * PER_ROW;
     ld_soff[k] = f * K::WQ + col;  // chunk pair swap of the slot applied per tick
     ld_goff[k] = f * n + gx;
+    ld_slot[k] = rr;               // rows 0..R-1 of tick 0 (R <= NQ)
+    ld_gy[k] = wrapi(qs + rr, ny);
   }
-  auto load_rows = [&](int rel_first) {
+  auto load_rows = [&]() {
 #pragma unroll
     for (int k = 0; k < NLD; ++k) {
-      if (ld_rr[k] < 0) continue;
-      const int rel = rel_first + ld_rr[k];
-      int gy = qs + rel;
-      if (gy < 0 || gy >= ny) gy = wrapi(gy, ny);
-      const int slot = rel % K::NQ;
+      if (!ld_on[k]) continue;
+      const int slot = ld_slot[k];
       double* d = q_ring + (size_t)slot * (3 * K::WQ) + (ld_soff[k] ^ (2 * slot_flip(slot)));
-      __pipeline_memcpy_async(d, src + ld_goff[k] + (long long)gy * nx, 16);
+      __pipeline_memcpy_async(d, src + ld_goff[k] + (long long)ld_gy[k] * nx, 16);
+      ld_slot[k] = (slot + K::R >= K::NQ) ? slot + K::R - K::NQ : slot + K::R;
+      ld_gy[k] = (ld_gy[k] + K::R >= ny) ? ld_gy[k] + K::R - ny : ld_gy[k] + K::R;
     }
     __pipeline_commit();
   };
 
-  load_rows(0);
+  load_rows();
+  // ring slots of this item's rows, advanced by R per tick (positive modulo once, here)
+  const int rel_init = -lag + rb * K::BY;
+  auto pmod = [](int a, int m) { a %= m; return a < 0 ? a + m : a; };
+  int s_in = pmod(rel_init - K::RY, inring.n);
+  int s_q = pmod(rel_init, K::NQ);
+  int s_o = pmod(rel_init, K::NS);
+  int gy_o = wrapi(qs + rel_init, ny);  // stage 3: global output row
   for (int t = 0; t < K::NTICK; ++t) {
     __pipeline_wait_prior(0);
     __syncthreads();
-    if (t + 1 < K::NTICK) load_rows((t + 1) * K::R);
-    const int rel0 = t * K::R - lag + rb * K::BY;
+    if (t + 1 < K::NTICK) load_rows();
+    const int rel0 = t * K::R + rel_init;
     if (rel0 >= lo && rel0 < hi) {
       double au[K::BY][K::BX], av[K::BY][K::BX], ap[K::BY][K::BX];
-      stage_item<K>(inring, qring, S, rel0, c, C, au, av, ap);
+      stage_item<K>(inring, qring, S, s_q, s_in, c, C, au, av, ap);
       if (S == 3) {
+        int gy = gy_o;
 #pragma unroll
         for (int r = 0; r < K::BY; ++r) {
-          int gy = qs + rel0 + r;
-          if (gy < 0 || gy >= ny) gy = wrapi(gy, ny);
           double* gp = dst + (long long)gy * nx + x0 + c;
+          gy = (gy + 1 == ny) ? 0 : gy + 1;
 #pragma unroll
           for (int x = 0; x < K::BX; x += 2) {
             *reinterpret_cast<double2*>(gp + x) = make_double2(au[r][x], au[r][x + 1]);
@@ -379,15 +390,14 @@ __global__ void __launch_bounds__(K::NT, 1) rk3_fused_kernel(const double* __res
           }
         }
       } else {
-        int so = rel0 % K::NS;
 #pragma unroll
         for (int r = 0; r < K::BY; ++r) {
-          int s = so + r;
-          s -= (s >= K::NS) ? K::NS : 0;
-          double* o = out_ring + (size_t)s * out_pitch;
+          int so = s_o + r;
+          so -= (so >= K::NS) ? K::NS : 0;
+          double* o = out_ring + (size_t)so * out_pitch;
 #pragma unroll
           for (int x = 0; x < K::BX; x += 2) {
-            const int p = (c + x) ^ (2 * slot_flip(s));
+            const int p = (c + x) ^ (2 * slot_flip(so));
             *reinterpret_cast<double2*>(o + p) = make_double2(au[r][x], au[r][x + 1]);
             *reinterpret_cast<double2*>(o + out_w + p) = make_double2(av[r][x], av[r][x + 1]);
             *reinterpret_cast<double2*>(o + 2 * out_w + p) = make_double2(ap[r][x], ap[r][x + 1]);
@@ -395,6 +405,10 @@ __global__ void __launch_bounds__(K::NT, 1) rk3_fused_kernel(const double* __res
         }
       }
     }
+    s_in = (s_in + K::R >= inring.n) ? s_in + K::R - inring.n : s_in + K::R;
+    s_q = (s_q + K::R >= K::NQ) ? s_q + K::R - K::NQ : s_q + K::R;
+    s_o = (s_o + K::R >= K::NS) ? s_o + K::R - K::NS : s_o + K::R;
+    gy_o = (gy_o + K::R >= ny) ? gy_o + K::R - ny : gy_o + K::R;
   }
 }
 
