@@ -146,10 +146,8 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
     }
   }
   auto rowp = [&](int dy) -> const RowP& { return rows[dy + K::RY]; };
-#pragma unroll
-  for (int r = 0; r < BY; ++r)
-#pragma unroll
-    for (int x = 0; x < BX; ++x) au[r][x] = av[r][x] = ap[r][x] = 0.0;
+  // accumulators start from their first product (no zero fill): av in the v x-stencil,
+  // au in the u x-stencil, ap from the u difference of the pressure divergence
   const int W = in.w;
   // a[r][X] = v(r+1) - v(r-1), b[r][X] = u(r+1) - u(r-1) at x = X-1 in [-1, BX]
   double A[BY][BX + 2], B[BY][BX + 2];
@@ -163,9 +161,11 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
       double w[WW];
       ldrow(w, rowp(r), W, 0);
 #pragma unroll
-      for (int x = 0; x < BX; ++x)
+      for (int x = 0; x < BX; ++x) {
+        av[r][x] = C.cxv[0] * w[x + 1];
 #pragma unroll
-        for (int k = 0; k < 7; ++k) av[r][x] = fma(C.cxv[k], w[x + 1 + k], av[r][x]);
+        for (int k = 1; k < 7; ++k) av[r][x] = fma(C.cxv[k], w[x + 1 + k], av[r][x]);
+      }
 #pragma unroll
       for (int k = 0; k < WH; ++k) vh[r + 1][k] = w[k + 2];
     }
@@ -195,9 +195,10 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
       ldrow(w, rowp(r), 0, 0);
 #pragma unroll
       for (int x = 0; x < BX; ++x) {
+        au[r][x] = C.cxu[0] * w[x + 1];
 #pragma unroll
-        for (int k = 0; k < 7; ++k) au[r][x] = fma(C.cxu[k], w[x + 1 + k], au[r][x]);
-        ap[r][x] = fma(C.pu, w[x + 5] - w[x + 3], ap[r][x]);
+        for (int k = 1; k < 7; ++k) au[r][x] = fma(C.cxu[k], w[x + 1 + k], au[r][x]);
+        ap[r][x] = C.pu * (w[x + 5] - w[x + 3]);
       }
 #pragma unroll
       for (int k = 0; k < WH; ++k) uh[r + 1][k] = w[k + 2];
