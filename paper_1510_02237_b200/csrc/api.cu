@@ -230,8 +230,9 @@ struct pw_basis {
   DBuf S, M, W, Q, Y;      // d x cap (S, M, W); d x r (Q, Y)
   DBuf Rs, tau1, tau2, diag, Q2, X, cs_work, lazy_fq, lazy_img, tmp, alpha;
   DBuf R1;                 // unpivoted R of all snapshots (cap x cap)
-  DBuf Q1;                 // explicit orthonormal Q1 (d x cap), built column block by column block
-  int q1_cols = 0;         // snapshot columns already factored into W (incremental path)
+  DBuf T, wy1, wy2;        // compact-WY T of all reflectors (cap x cap) and two cap x cap temps
+  std::vector<char> cs_host;  // cuSOLVER host workspace (X API)
+  int v_cols = 0;          // reflectors held in W (explicit unit-lower V); incremental path
   IBuf piv, info;
   std::vector<double> diag_h;
   std::vector<int> piv_h;
@@ -270,128 +271,148 @@ struct PhaseClock {
   }
 };
 
-// Unpivoted Householder QR  S = Q1 R1  of all m snapshots, kept in factored form:
-// W holds dgeqrf's reflectors (below the diagonal) and tau1 their scales; R1 is
-// copied to a cap x cap buffer.  When the sweep appends p columns N, only they
-// are processed -- N <- Q1^T N with the stored reflectors (dormqr, BLAS3), then
-// dgeqrf of the trailing (d - m_old) x p block -- which is exactly what a blocked
-// Householder QR of the whole d x m block computes (no orthogonality loss on
-// the near-duplicate snapshots Parareal produces).  The pivoted QR of R1 below
-// then picks dgeqp3's pivots on S.
+// Unpivoted Householder QR  S = Q1 R1  of all m snapshots, kept in compact WY form:
+//   Q1 = I - V T V^T,  V (d x k, W's columns, explicit unit-lower trapezoidal),
+//   T (k x k upper triangular, ld cap),  k = min(d, m)
+// and R1 copied to a cap x cap buffer.  When the sweep appends p columns N, only they
+// are processed: N <- Q1^T N = N - V T^T V^T N (three GEMMs), a 64-bit geqrf of the
+// trailing (d - m_old) x p block, then T grows by the new panel's larft block and the
+// coupling block -T_old (V_old^T V_new) T_new.  That is exactly a blocked Householder
+// QR of the whole d x m block (no orthogonality loss on the near-duplicate snapshots
+// Parareal produces), without ever forming Q1: the basis Q = Q1 [Q2; 0] is one more
+// GEMM pass over V.  The pivoted QR of R1 below then picks dgeqp3's pivots on S
+// (SURVEY.md 8(c)).  All solver calls are the 64-bit X API and every GEMM is
+// cublasDgemm_64, so d x m may exceed 2^31 (c4: 3.1M x 1024).
 static PhaseClock* g_clk = nullptr;  // optional fine-grained marks (PW_QR_TIMING=1)
 static void mark(const char* n) { if (g_clk) g_clk->mark(n); }
 
-// cuSOLVER workspace, sized once for the largest call this basis can make (geqrf / orgqr /
-// ormqr at m = capacity): growing it update by update re-allocated (and re-mapped) pool
-// memory inside the refactorisation and stalled the stream for up to ~0.2 s.
+static cusolverDnParams_t solver_params(Ctx& c) {
+  if (!c.cusolver_params) {
+    cusolverDnParams_t prm;
+    PW_SOLVER(cusolverDnCreateParams(&prm));
+    c.cusolver_params = prm;
+  }
+  return static_cast<cusolverDnParams_t>(c.cusolver_params);
+}
+
+// cuSOLVER workspace, sized once for the largest call this basis can make (geqrf / larft
+// at k = capacity): growing it update by update re-allocated (and re-mapped) pool memory
+// inside the refactorisation and stalled the stream for up to ~0.2 s.
 static void presize_solver_ws(pw_basis* B) {
   if (B->cs_work.p) return;
   Ctx& c = B->ctx->c;
-  const int d = (int)B->dim;
-  const int cap = (int)std::min<long long>(B->cap, B->dim);
+  const long long d = B->dim;
+  const long long cap = std::min<long long>(B->cap, B->dim);
   double* any = B->S.p;  // size queries only: the pointers are not dereferenced
-  int lw = 1, t = 0;
-  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), d, cap, any, d, &t));
-  lw = std::max(lw, t);
-  PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), d, cap, cap, any, d, any, &t));
-  lw = std::max(lw, t);
-  for (cublasOperation_t op : {CUBLAS_OP_T, CUBLAS_OP_N}) {
-    PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, op, d, cap, cap, any, d, any,
-                                          any, d, &t));
-    lw = std::max(lw, t);
-  }
-  B->cs_work.ensure(c, (size_t)lw);
+  size_t dev = 8, host = 0, dv = 0, hv = 0;
+  PW_SOLVER(cusolverDnXgeqrf_bufferSize(solver(c), solver_params(c), d, cap, CUDA_R_64F, any, d,
+                                        CUDA_R_64F, any, CUDA_R_64F, &dv, &hv));
+  dev = std::max(dev, dv);
+  host = std::max(host, hv);
+  PW_SOLVER(cusolverDnXlarft_bufferSize(solver(c), solver_params(c), CUBLAS_DIRECT_FORWARD,
+                                        CUBLAS_STOREV_COLUMNWISE, d, cap, CUDA_R_64F, any, d, CUDA_R_64F,
+                                        any, CUDA_R_64F, any, B->cap, CUDA_R_64F, &dv, &hv));
+  dev = std::max(dev, dv);
+  host = std::max(host, hv);
+  B->cs_work.ensure(c, dev / sizeof(double) + 1);
+  B->cs_host.resize(std::max<size_t>(host, 1));
 }
 
-static int solver_ws(pw_basis* B, int lw) {
+// Householder QR of the panel W[row0:, col0:col0+p] (ld d) into tau1[col0..], its larft
+// block into T[col0.., col0..], then explicit unit-lower V for the panel (rows above the
+// panel's diagonal zeroed: R1 already holds them).  Returns the reflector count.
+static int factor_panel(pw_basis* B, int col0, int p) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const long long rows = d - col0;
+  const int k = (int)std::min<long long>(rows, p);
+  if (k <= 0) return 0;
+  double* P = B->W.p + (size_t)col0 * d + col0;
+  double* tau = B->tau1.p + col0;
+  int* info = B->info.ensure(c, 1);
   presize_solver_ws(B);
-  B->cs_work.ensure(B->ctx->c, (size_t)std::max(lw, 1));
-  return (int)B->cs_work.n;
+  PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, p, CUDA_R_64F, P, d, CUDA_R_64F, tau,
+                             CUDA_R_64F, B->cs_work.p, B->cs_work.n * sizeof(double), B->cs_host.data(),
+                             B->cs_host.size(), info));
+  mark("geqrf");
+  return k;
+}
+
+static void panel_to_wy(pw_basis* B, int col0, int k) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const size_t capc = (size_t)B->cap;
+  pw::launch_make_unit_lower(c, B->W.p + (size_t)col0 * d, d, col0, k);
+  // G = V[col0:, 0:m]^T V_new[col0:, :]  (V_new is zero above row col0), then T's new columns
+  const int m = col0 + k;
+  double* G = B->wy1.ensure(c, capc * capc);
+  gemm(c, true, false, m, k, d - col0, 1.0, B->W.p + col0, d, B->W.p + (size_t)col0 * d + col0, d, 0.0,
+       G, m);
+  pw::launch_larft_cols(c, B->T.p, B->cap, G, B->tau1.p, col0, k);
+  mark("larft");
+}
+
+static void alloc_factor(pw_basis* B) {
+  Ctx& c = B->ctx->c;
+  const size_t capc = (size_t)B->cap;
+  B->W.ensure(c, (size_t)B->dim * capc);
+  B->tau1.ensure(c, capc);
+  if (B->T.p == nullptr) {  // T's strict lower part is never written
+    B->T.ensure(c, capc * capc);
+    PW_CUDA(cudaMemsetAsync(B->T.p, 0, capc * capc * sizeof(double), c.stream));
+  }
+  presize_solver_ws(B);
 }
 
 static void factor_full(pw_basis* B, int mr) {
   Ctx& c = B->ctx->c;
   const long long d = B->dim;
   const int m = B->m;
-  PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
-           "snapshot block d*m exceeds the 32-bit cuSOLVER geqrf range");
-  double* W = B->W.ensure(c, (size_t)d * B->cap);
-  double* tau1 = B->tau1.ensure(c, B->cap);
-  int* info = B->info.ensure(c, 1);
-  presize_solver_ws(B);
-  mark("full.alloc");
-  copy_cols(c, W, d, B->S.p, d, d, m);
-  int lw = 0;
-  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)d, m, W, (int)d, &lw));
-  const int lwork = solver_ws(B, lw);
-  PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)d, m, W, (int)d, tau1, B->cs_work.p, lwork, info));
   const size_t capc = (size_t)B->cap;
+  alloc_factor(B);
+  PW_CUDA(cudaMemsetAsync(B->T.p, 0, capc * capc * sizeof(double), c.stream));
+  mark("full.alloc");
+  copy_cols(c, B->W.p, d, B->S.p, d, d, m);
+  const int k = factor_panel(B, 0, m);
   double* R1 = B->R1.ensure(c, capc * capc);
   double* tmp = B->Rs.ensure(c, capc * capc);
-  pw::launch_extract_upper(c, W, d, mr, m, tmp);  // mr x m, ld mr
+  pw::launch_extract_upper(c, B->W.p, d, mr, m, tmp);  // mr x m, ld mr
   PW_CUDA(cudaMemcpy2DAsync(R1, capc * sizeof(double), tmp, mr * sizeof(double), mr * sizeof(double),
                             m, cudaMemcpyDeviceToDevice, c.stream));
-  // explicit orthonormal Q1 (d x mr) next to the reflectors
-  double* Q1 = B->Q1.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
-  copy_cols(c, Q1, d, W, d, d, mr);
-  PW_SOLVER(cusolverDnDorgqr_bufferSize(solver(c), (int)d, mr, mr, Q1, (int)d, tau1, &lw));
-  const int lwork2 = solver_ws(B, lw);
-  PW_SOLVER(cusolverDnDorgqr(solver(c), (int)d, mr, mr, Q1, (int)d, tau1, B->cs_work.p, lwork2, info));
-  B->q1_cols = mr;
+  panel_to_wy(B, 0, k);
+  B->v_cols = k;
 }
-
 
 static void factor_append(pw_basis* B, int m_old) {
   Ctx& c = B->ctx->c;
   const long long d = B->dim;
   const int m = B->m, p = m - m_old;
   const size_t capc = (size_t)B->cap;
-  PW_CHECK((double)d * (double)m < 2147483647.0, PW_ERR_VALUE,
-           "snapshot block d*m exceeds the 32-bit cuSOLVER ormqr range");
+  alloc_factor(B);
   double* W = B->W.p;
   double* Wn = W + (size_t)m_old * d;
-  double* tau1 = B->tau1.p;
-  int* info = B->info.ensure(c, 1);
   copy_cols(c, Wn, d, B->S.p + (size_t)m_old * d, d, d, p);
-  // N <- Q1^T N  (the m_old stored reflectors, applied as blocked WY updates)
-  int lw = 0;
-  PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)d, p, m_old, W,
-                                        (int)d, tau1, Wn, (int)d, &lw));
-  int lwork = solver_ws(B, lw);
   mark("a.copy");
-  PW_SOLVER(cusolverDnDormqr(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)d, p, m_old, W, (int)d,
-                             tau1, Wn, (int)d, B->cs_work.p, lwork, info));
-  mark("a.ormqrT");
+  // N <- Q1^T N = N - V T^T (V^T N)   (V = the m_old explicit reflectors)
+  double* X1 = B->wy1.ensure(c, capc * capc);
+  double* X2 = B->wy2.ensure(c, capc * capc);
+  gemm(c, true, false, m_old, p, d, 1.0, W, d, Wn, d, 0.0, X1, m_old);
+  gemm(c, true, false, m_old, p, m_old, 1.0, B->T.p, B->cap, X1, m_old, 0.0, X2, m_old);
+  gemm(c, false, false, d, p, m_old, -1.0, W, d, X2, m_old, 1.0, Wn, d);
+  mark("a.applyQ1T");
   // Householder QR of the trailing rows m_old..d-1 of the new block
-  PW_SOLVER(cusolverDnDgeqrf_bufferSize(solver(c), (int)(d - m_old), p, Wn + m_old, (int)d, &lw));
-  lwork = solver_ws(B, lw);
-  PW_SOLVER(cusolverDnDgeqrf(solver(c), (int)(d - m_old), p, Wn + m_old, (int)d, tau1 + m_old,
-                             B->cs_work.p, lwork, info));
-  mark("a.geqrf");
+  const int k = factor_panel(B, m_old, p);
   // R1[:, m_old:m] = [ (Q1^T N)[0:m_old] ; upper(R_N) ]
   double* R1 = B->R1.p;
   double* tmp = B->Rs.ensure(c, capc * capc);
   PW_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Wn, d * sizeof(double), m * sizeof(double), p,
                             cudaMemcpyDeviceToDevice, c.stream));
-  mark("r1.copy1");
   pw::launch_zero_strict_lower_block(c, tmp + m_old, m, p, p);
-  mark("r1.zero");
   PW_CUDA(cudaMemcpy2DAsync(R1 + (size_t)m_old * capc, capc * sizeof(double), tmp, m * sizeof(double),
                             m * sizeof(double), p, cudaMemcpyDeviceToDevice, c.stream));
-  mark("r1.copy2");
-  // new explicit Q1 columns: Q_full [0; I_p; 0] with all m reflectors
-  double* Q1n = B->Q1.p + (size_t)m_old * d;
-  PW_CUDA(cudaMemsetAsync(Q1n, 0, sizeof(double) * (size_t)d * p, c.stream));
-  mark("r1.memset");
-  pw::launch_set_diag_block(c, Q1n + m_old, d, p, 1.0);
-  mark("r1.diag");
-  PW_SOLVER(cusolverDnDormqr_bufferSize(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_N, (int)d, p, m, W,
-                                        (int)d, tau1, Q1n, (int)d, &lw));
-  lwork = solver_ws(B, lw);
   mark("a.R1");
-  PW_SOLVER(cusolverDnDormqr(solver(c), CUBLAS_SIDE_LEFT, CUBLAS_OP_N, (int)d, p, m, W, (int)d, tau1,
-                             Q1n, (int)d, B->cs_work.p, lwork, info));
-  B->q1_cols = m;
+  panel_to_wy(B, m_old, k);
+  B->v_cols = m_old + k;
 }
 
 void basis_refactor(pw_basis* B, int m_old) {
@@ -409,7 +430,7 @@ void basis_refactor(pw_basis* B, int m_old) {
     B->R1.ensure(c, capc * capc);
     PW_CUDA(cudaMemsetAsync(B->R1.p, 0, capc * capc * sizeof(double), c.stream));
   }
-  const bool incremental = B->diff_mode && m <= d && m_old > 0 && B->q1_cols == m_old;
+  const bool incremental = m <= d && m_old > 0 && B->v_cols == m_old;
   g_clk = clk.on ? &clk : nullptr;
   if (incremental) factor_append(B, m_old);
   else factor_full(B, mr);
@@ -433,11 +454,20 @@ void basis_refactor(pw_basis* B, int m_old) {
     PW_CUDA(cudaStreamSynchronize(c.stream));
     return;
   }
-  // Q = Q1 Q2[:, :r]
+  // Q = Q1 [Q2[:, :r]; 0] = [Q2; 0] - V (T (V[0:mr]^T Q2))
   double* Q2 = B->Q2.ensure(c, capc * capc);
   pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
   double* Q = B->Q.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
-  gemm(c, false, false, d, r, mr, 1.0, B->Q1.p, d, Q2, mr, 0.0, Q, d);
+  {
+    const int k = B->v_cols;  // == mr
+    double* X1 = B->wy1.ensure(c, capc * capc);
+    double* X2 = B->wy2.ensure(c, capc * capc);
+    gemm(c, true, false, k, r, mr, 1.0, B->W.p, d, Q2, mr, 0.0, X1, k);
+    gemm(c, false, false, k, r, k, 1.0, B->T.p, B->cap, X1, k, 0.0, X2, k);
+    PW_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * (size_t)d * r, c.stream));
+    copy_cols(c, Q, d, Q2, mr, mr, r);
+    gemm(c, false, false, d, r, k, -1.0, B->W.p, d, X2, k, 1.0, Q, d);
+  }
   clk.mark("Q=Q1Q2");
   // Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep)
   double* X = B->X.ensure(c, capc * capc);
@@ -567,6 +597,7 @@ int pw_ctx_destroy(pw_ctx* ctx) {
     if (ctx->c.red) cudaFree(ctx->c.red);
     if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
+    if (ctx->c.cusolver_params) cusolverDnDestroyParams(static_cast<cusolverDnParams_t>(ctx->c.cusolver_params));
     if (ctx->c.cusolver) cusolverDnDestroy(solver(ctx->c));
     if (ctx->c.side) {
       cudaStreamSynchronize(ctx->c.side);

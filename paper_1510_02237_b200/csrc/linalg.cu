@@ -448,9 +448,66 @@ __global__ void set_diag_kernel(double* __restrict__ A, long long ld, int k, dou
   if (i < k) A[(long long)i * ld + i] = v;
 }
 
+// Column block of k Householder vectors after geqrf -> explicit unit-lower form:
+// column j (0-based in the block) gets zeros in rows [0, off + j) and 1 at row off + j.
+__global__ void make_unit_lower_kernel(double* __restrict__ A, long long ld, int off, int k) {
+  const long long rows = (long long)off + k;
+  const long long total = rows * k;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(idx / rows);
+    const long long row = idx - (long long)col * rows;
+    const long long diag = (long long)off + col;
+    if (row < diag) A[(long long)col * ld + row] = 0.0;
+    else if (row == diag) A[(long long)col * ld + row] = 1.0;
+  }
+}
+
+// Compact-WY T for reflector columns col0..col0+p-1 given G = V^T V_new (m x p, ld m,
+// m = col0 + p) and tau: the dlarft recurrence over ALL reflectors,
+//   T[i, i] = tau_i,  T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i],
+// one CTA, columns in order (each depends on the previous ones); T upper, ld ldt.
+__global__ void __launch_bounds__(1024) larft_cols_kernel(double* __restrict__ T, int ldt,
+                                                          const double* __restrict__ G,
+                                                          const double* __restrict__ tau, int col0,
+                                                          int p) {
+  const int m = col0 + p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int i = col0; i < m; ++i) {
+    const double ti = tau[i];
+    const double* g = G + (size_t)(i - col0) * m;
+    // one warp per row j, lanes split the l sum (independent L2 loads, then a warp reduction)
+    for (int j = warp; j < i; j += nwarp) {
+      double w = 0.0;
+      for (int l = j + lane; l < i; l += 32) w = fma(T[(size_t)l * ldt + j], g[l], w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      if (lane == 0) T[(size_t)i * ldt + j] = -ti * w;
+    }
+    if (threadIdx.x == 0) T[(size_t)i * ldt + i] = ti;
+    __syncthreads();
+  }
+}
+
 int g_pqr_blocks_per_sm = -1;
 
 }  // namespace
+
+void launch_larft_cols(Ctx& c, double* T, int ldt, const double* G, const double* tau, int col0, int p) {
+  if (p <= 0) return;
+  larft_cols_kernel<<<1, 1024, 0, c.stream>>>(T, ldt, G, tau, col0, p);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void launch_make_unit_lower(Ctx& c, double* A, long long ld, int off, int k) {
+  const long long total = ((long long)off + k) * k;
+  if (k <= 0) return;
+  int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c.num_sms * 8));
+  make_unit_lower_kernel<<<blocks, 256, 0, c.stream>>>(A, ld, off, k);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
 
 void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,
                        double beta, size_t n) {

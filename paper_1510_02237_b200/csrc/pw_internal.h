@@ -88,6 +88,7 @@ struct Ctx {
   int num_sms = 0;
   void* cublas = nullptr;    // cublasHandle_t
   void* cusolver = nullptr;  // cusolverDnHandle_t
+  void* cusolver_params = nullptr;  // cusolverDnParams_t (64-bit X API)
   void* blas_ws = nullptr;   // fixed cuBLAS workspace
   // scratch for grid barriers / reductions
   double* red = nullptr;     // reduction scratch (doubles)
@@ -127,6 +128,11 @@ void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, doub
                        double beta, size_t n);
 void launch_extract_upper(Ctx& c, const double* W, long long ldw, int mr, int m, double* R);
 void launch_zero_strict_lower_block(Ctx& c, double* A, long long ld, int rows, int cols);
+// k Householder vectors stored from column A (rows off.. of their block) -> explicit
+// unit-lower trapezoidal form: zero above the diagonal entry off + j, 1 on it
+void launch_make_unit_lower(Ctx& c, double* A, long long ld, int off, int k);
+// dlarft recurrence for reflector columns col0..col0+p-1 of T (ld ldt), G = V^T V_new (m x p)
+void launch_larft_cols(Ctx& c, double* T, int ldt, const double* G, const double* tau, int col0, int p);
 void launch_set_diag_block(Ctx& c, double* A, long long ld, int k, double v);
 size_t residual_scratch_doubles(int ncols, long long nrows);
 void launch_residual(Ctx& c, const double* a, long long lda, const double* b, long long ldb,
