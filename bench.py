@@ -193,9 +193,9 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def parareal_c3(dev_index):
-    """c3 KSE window: 512^2, P=64, K=5; per-iteration device time and phases."""
-    import numpy as np
+def parareal_window(name="c3", warm=True):
+    """One KSE-Parareal window of config `name` (c3: 512^2, P=64, K=5; c4: 1024^2, P=256,
+    K=4): per-iteration device time and phases."""
     import torch
 
     from paper_1510_02237_b200 import harness
@@ -204,26 +204,36 @@ def parareal_c3(dev_index):
     from paper_1510_02237_b200.parareal import Timings, kse_sweep
     from paper_1510_02237_b200.physics import ModelSpec
 
-    wl = harness.WORKLOADS["c3"]
+    wl = harness.WORKLOADS[name]
     g = build_grid(wl.n, wl.n)
     vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
     fine = SlicePropagator(make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), g, 0.5),
                            wl.slice_span)
     coarse = SlicePropagator(make_propagator(SPLIT_FE_FB, ModelSpec(ACOUSTIC, vel, 1, 1.0, 0.1, 1.0), g,
                                              4.0, 16), wl.slice_span)
-    q0 = torch.as_tensor(harness.initial_state("c3")).cuda()
-    # warm-up: first-use module loads (cuSOLVER/cuBLAS lazy loading) and pool allocations
-    kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True)
+    q0 = torch.as_tensor(harness.initial_state(name)).cuda()
+    if warm:
+        # warm-up: first-use module loads (cuSOLVER/cuBLAS lazy loading) and pool allocations
+        kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True)
     tm = Timings()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm, return_device=True)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return {"workload": "c3: 512^2, P=64, K=5 KSE-Parareal window", "window_s": wall,
-            "iteration_s": wall / wl.n_it,
+    d = q0.numel()
+    return {"workload": f"{name}: {wl.n}^2, P={wl.n_p}, K={wl.n_it} KSE-Parareal window",
+            "window_s": wall, "iteration_s": wall / wl.n_it,
             "phases_s": {"coarse_and_correction": tm.coarse, "fine": tm.fine, "qr": tm.qr},
-            "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res]}
+            "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res],
+            "fine_cell_updates_per_s": wl.n_p * wl.n_it * fine.nsteps * d / 3 / tm.fine if tm.fine else None,
+            "peak_device_gib": torch.cuda.max_memory_allocated() / 2**30,
+            "warm": warm}
+
+
+def parareal_c3(dev_index):
+    """c3 KSE window: 512^2, P=64, K=5; per-iteration device time and phases."""
+    return parareal_window("c3")
 
 
 def run_ours(args, rank, world, local_rank):

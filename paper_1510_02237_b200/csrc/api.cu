@@ -233,6 +233,7 @@ struct pw_basis {
   DBuf T, wy1, wy2;        // compact-WY T of all reflectors (cap x cap) and two cap x cap temps
   std::vector<char> cs_host;  // cuSOLVER host workspace (X API)
   int v_cols = 0;          // reflectors held in W (explicit unit-lower V); incremental path
+  bool lean = false;       // sweep under memory pressure: no separate snapshot copy S
   IBuf piv, info;
   std::vector<double> diag_h;
   std::vector<int> piv_h;
@@ -303,7 +304,7 @@ static void presize_solver_ws(pw_basis* B) {
   Ctx& c = B->ctx->c;
   const long long d = B->dim;
   const long long cap = std::min<long long>(B->cap, B->dim);
-  double* any = B->S.p;  // size queries only: the pointers are not dereferenced
+  double* any = B->W.p;  // size queries only: the pointers are not dereferenced
   size_t dev = 8, host = 0, dv = 0, hv = 0;
   PW_SOLVER(cusolverDnXgeqrf_bufferSize(solver(c), solver_params(c), d, cap, CUDA_R_64F, any, d,
                                         CUDA_R_64F, any, CUDA_R_64F, &dv, &hv));
@@ -372,7 +373,7 @@ static void factor_full(pw_basis* B, int mr) {
   alloc_factor(B);
   PW_CUDA(cudaMemsetAsync(B->T.p, 0, capc * capc * sizeof(double), c.stream));
   mark("full.alloc");
-  copy_cols(c, B->W.p, d, B->S.p, d, d, m);
+  if (!B->lean) copy_cols(c, B->W.p, d, B->S.p, d, d, m);
   const int k = factor_panel(B, 0, m);
   double* R1 = B->R1.ensure(c, capc * capc);
   double* tmp = B->Rs.ensure(c, capc * capc);
@@ -391,7 +392,7 @@ static void factor_append(pw_basis* B, int m_old) {
   alloc_factor(B);
   double* W = B->W.p;
   double* Wn = W + (size_t)m_old * d;
-  copy_cols(c, Wn, d, B->S.p + (size_t)m_old * d, d, d, p);
+  if (!B->lean) copy_cols(c, Wn, d, B->S.p + (size_t)m_old * d, d, d, p);
   mark("a.copy");
   // N <- Q1^T N = N - V T^T (V^T N)   (V = the m_old explicit reflectors)
   double* X1 = B->wy1.ensure(c, capc * capc);
@@ -431,6 +432,8 @@ void basis_refactor(pw_basis* B, int m_old) {
     PW_CUDA(cudaMemsetAsync(B->R1.p, 0, capc * capc * sizeof(double), c.stream));
   }
   const bool incremental = m <= d && m_old > 0 && B->v_cols == m_old;
+  PW_CHECK(!B->lean || incremental || m_old == 0, PW_ERR_STATE,
+           "lean subspace cannot be refactored from scratch (snapshots not retained)");
   g_clk = clk.on ? &clk : nullptr;
   if (incremental) factor_append(B, m_old);
   else factor_full(B, mr);
@@ -485,7 +488,8 @@ void basis_append(pw_basis* B, const double* states, long long lds, const double
   PW_CHECK(B->m + p <= B->cap, PW_ERR_VALUE,
            "subspace capacity exceeded (" + std::to_string(B->m + p) + " > " + std::to_string(B->cap) + ")");
   const long long d = B->dim;
-  double* S = B->S.ensure(c, (size_t)d * B->cap);
+  // lean sweeps keep the snapshots only as W's not-yet-factored columns
+  double* S = B->lean ? B->W.ensure(c, (size_t)d * B->cap) : B->S.ensure(c, (size_t)d * B->cap);
   double* M = B->M.ensure(c, (size_t)d * B->cap);
   copy_cols(c, S + (size_t)B->m * d, d, states, lds, d, p);
   copy_cols(c, M + (size_t)B->m * d, d, m_cols, ldm, d, p);
@@ -764,8 +768,8 @@ int pw_basis_views(const pw_basis* basis, const double** q, const double** fq,
     pw_basis* B = const_cast<pw_basis*>(basis);
     if (q) *q = B->Q.p;
     if (fq) *fq = B->r > 0 ? basis_fq(B) : nullptr;
-    if (snapshots) *snapshots = B->S.p;
-    if (images) *images = B->m > 0 ? basis_images(B) : nullptr;
+    if (snapshots) *snapshots = B->lean ? nullptr : B->S.p;
+    if (images) *images = (B->m > 0 && !B->lean) ? basis_images(B) : nullptr;
     PW_CUDA(cudaStreamSynchronize(B->ctx->c.stream));
   });
 }
@@ -881,6 +885,15 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       B.reset(basis_new(ctx, d, rank_tol, n_c * n_it));
       B->diff_mode = true;
       B->coarse = coarse;
+      // lean mode when the d x cap matrices (S, M, W, Q, Y) plus propagator temporaries
+      // would not fit next to the sweep buffers (c4 on one GPU: 5 x 25.8 GB)
+      size_t free_b = 0, total_b = 0;
+      PW_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const double col = 8.0 * (double)d;
+      const double need = col * std::min<long long>(B->cap, d) * 5.0 + col * n_c * 3.0 +
+                          std::max(4.0 * (1ull << 30), 0.06 * (double)total_b);
+      const char* e = getenv("PW_SWEEP_LEAN");
+      B->lean = (e && *e == '1') || need > (double)free_b;
     }
     cudaEvent_t ev[4];
     const bool timed = timings != nullptr;

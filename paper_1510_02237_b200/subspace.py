@@ -82,13 +82,20 @@ class Subspace:
     def snapshots(self):
         if self._handle is None:
             return np.empty((self.dim, 0))
-        return self._host_cols(self._views()[2], self.ncols)
+        ptr = self._views()[2]
+        if not ptr and self.ncols:
+            raise RuntimeError("snapshots were not retained: this subspace came from a lean sweep "
+                               "(device memory too small for a separate snapshot copy)")
+        return self._host_cols(ptr, self.ncols)
 
     @property
     def images(self):
         if self._handle is None:
             return np.empty((self.dim, 0))
-        return self._host_cols(self._views()[3], self.ncols)
+        ptr = self._views()[3]
+        if not ptr and self.ncols:
+            raise RuntimeError("images were not retained: this subspace came from a lean sweep")
+        return self._host_cols(ptr, self.ncols)
 
     def diag_ratios(self):
         """|R_jj| / |R_11| of the last refactorisation (rank diagnostics)."""

@@ -1,5 +1,8 @@
-"""Time the c3 KSE-Parareal window alone (bench.py's parareal field); env knobs
-PW_SWEEP_OVERLAP / PW_COOP_CAP are read by the library at context creation."""
+"""Time one KSE-Parareal window (bench.py's parareal field) of config c3 (default) or c4:
+
+    python scripts/c3_window.py [c3|c4] [--cold]
+
+Env knobs PW_SWEEP_OVERLAP / PW_COOP_CAP are read by the library at context creation."""
 import json
 import os
 import sys
@@ -8,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 
 if __name__ == "__main__":
-    out = bench.parareal_c3(0)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    out = bench.parareal_window(args[0] if args else "c3", warm="--cold" not in sys.argv)
     out["env"] = {k: os.environ.get(k) for k in ("PW_SWEEP_OVERLAP", "PW_COOP_CAP")}
     print(json.dumps(out))

@@ -1,0 +1,77 @@
+"""c4 (1024^2, P=256) first-iteration fixture from the REFERENCE itself (this container only).
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_c4_golden.py [n_it]
+
+Runs the reference's kse_sweep on BASELINE config 4 (harness.WORKLOADS["c4"]) for n_it
+iterations (default 1; each further iteration costs the reference a single-threaded
+pivoted QR of 3.1M x 256k) with a thread pool for the fine sweep, and stores what a
+multi-GB window can be pinned by in a small file: the residual history, the ranks, the
+per-slice L2 norms of qn[1:] after every iteration and 512 fixed-seed sampled entries
+per slice.  The state itself (6 GB per iteration) is not stored.
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+sys.path.insert(0, HERE)
+
+from pitwave import subspace as ref_sub  # noqa: E402
+from pitwave.parareal import kse_sweep  # noqa: E402
+
+from make_golden import slice_closures  # noqa: E402
+from paper_1510_02237_b200 import harness  # noqa: E402  (seeded generators only)
+
+N_SAMPLE = 512
+
+
+def main(n_it=1):
+    wl = harness.WORKLOADS["c4"]
+    fine, coarse = slice_closures(wl)
+    q0 = harness.initial_state("c4")
+    d = q0.size
+    idx = np.sort(np.random.default_rng(4242).choice(d, N_SAMPLE, replace=False))
+    norms, samples, ranks = [], [], []
+    orig_update = ref_sub.Subspace.update
+
+    def spy_update(self, states, images):
+        new = orig_update(self, states, images)
+        ranks.append(new.rank)
+        print(f"  update: rank {new.rank} ({time.time() - t0:.0f} s)", flush=True)
+        return new
+
+    import pitwave.parareal as ref_par
+    orig_res = ref_par.iteration_residual
+
+    def spy_res(prev, nxt):
+        st = np.stack([np.asarray(v) for v in nxt])
+        norms.append(np.linalg.norm(st, axis=1))
+        samples.append(st[:, idx])
+        r = orig_res(prev, nxt)
+        print(f"  iteration {len(norms)}: residual {r:.6e} ({time.time() - t0:.0f} s)", flush=True)
+        return r
+
+    ref_sub.Subspace.update = spy_update
+    ref_par.iteration_residual = spy_res
+    t0 = time.time()
+    try:
+        with ThreadPoolExecutor(os.cpu_count()) as pool:
+            ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, n_it, pool=pool)
+    finally:
+        ref_sub.Subspace.update = orig_update
+        ref_par.iteration_residual = orig_res
+    np.savez_compressed(os.path.join(HERE, "c4_reference.npz"), res=np.array(res), ranks=np.array(ranks),
+                        norms=np.array(norms), samples=np.array(samples), idx=idx,
+                        seconds=time.time() - t0, threads=os.cpu_count())
+    print(f"done in {time.time() - t0:.0f} s: residuals {res}, ranks {ranks}")
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 1)

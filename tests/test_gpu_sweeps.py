@@ -211,6 +211,24 @@ def test_c1_kse_history_matches_reference():
         np.testing.assert_allclose(res, g["kse_res"][:k], rtol=1e-10)
 
 
+def test_c1_kse_lean_mode_matches_reference(monkeypatch):
+    """Lean sweep (no separate snapshot copy: the c4-on-one-GPU memory mode) gives the same
+    window; the snapshot/image views then refuse instead of returning stale data."""
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    g = golden("c1_kse.npz")
+    wl, fine, coarse = c1_props()
+    monkeypatch.setenv("PW_SWEEP_LEAN", "1")
+    ends, res, sub = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    assert sub.rank == g["kse_ranks"][-1]
+    worst = max(rel(ends[i], g["kse_hist"][-1][i]) for i in range(wl.n_p))
+    assert worst <= 1e-10, worst
+    np.testing.assert_allclose(res, g["kse_res"], rtol=1e-10)
+    with pytest.raises(RuntimeError):
+        sub.snapshots
+    assert sub.q.shape == (g["q0"].size, sub.rank)
+
+
 def test_c1_original_matches_reference():
     from paper_1510_02237_b200.parareal import parareal_sweep
 
