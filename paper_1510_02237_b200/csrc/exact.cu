@@ -175,6 +175,21 @@ struct SAcc {
   __device__ __forceinline__ double a_v(int dy, int dx) const { return sav[dy * WA + dx]; }
 };
 
+// ... or a shared-memory tile with the cell's own frozen tendencies in registers (only the
+// <0, 0> velocity updates, which read a_u / a_v at the cell itself)
+struct SAccV {
+  const double* su;
+  const double* sv;
+  const double* sp;
+  int W;
+  double au, av;
+  __device__ __forceinline__ double u(int dy, int dx) const { return su[dy * W + dx]; }
+  __device__ __forceinline__ double v(int dy, int dx) const { return sv[dy * W + dx]; }
+  __device__ __forceinline__ double p(int dy, int dx) const { return sp[dy * W + dx]; }
+  __device__ __forceinline__ double a_u(int, int) const { return au; }
+  __device__ __forceinline__ double a_v(int, int) const { return av; }
+};
+
 // u' and v' of one FB substep at (j+DY, i+DX), reference operation order (fb_substeps,
 // numba_backend.py:137-143): du = au - cs dx(p) [+ a1 dx(div)], u' = u + tau du
 template <int DY, int DX, class A>
@@ -388,6 +403,173 @@ __global__ void __launch_bounds__(256, 2) fefb_tiled_coop(double* st, int batch,
   }
 }
 
+// Temporal-blocked variant: K substeps per grid barrier.  Each CTA stages its T x T
+// tile of (u, v, p) with a 3K-cell halo, then runs the K substeps on shrinking regions
+// in shared memory: u', v' of the whole region first (stored), one CTA barrier, then
+// p' from the stored neighbour velocities (no recomputation), p updated in place and
+// the (u, v) / (u', v') planes swapped.  Region margins per substep (M = 3K at entry):
+// u', v' on M - 2, p' on M - 3, next M = M - 3, so the last p' lands on the tile.
+// Same expressions as fb_cell (bitwise equal to the per-cell variants).
+struct TbPlanes {
+  double* u;
+  double* v;
+  double* p;
+  double* un;
+  double* vn;
+};
+
+template <int T, int K>
+__device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ cu,
+                                         double* __restrict__ nu, const double* __restrict__ w,
+                                         int tx0, int ty0, const ExactParams& p, double sx,
+                                         double sy, double tau, bool damp) {
+  constexpr int H = 3 * K, W = T + 2 * H, WW = W * W;
+  const int nx = p.nx, ny = p.ny, n = nx * ny;
+  double* planes = sm;  // u, v, p, un, vn : W x W each
+  // ---- stage (u, v, p) with halo H
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int CX = (W + 31) / 32;
+    int gx[CX];
+#pragma unroll
+    for (int k = 0; k < CX; ++k) {
+      int x = tx0 - H + lane + 32 * k;
+      x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+      gx[k] = x;
+    }
+    for (int y = warp; y < W; y += 8) {
+      int gy = ty0 - H + y;
+      gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
+      const double* row = cu + (size_t)gy * nx;
+#pragma unroll
+      for (int f = 0; f < 3; ++f)
+#pragma unroll
+        for (int k = 0; k < CX; ++k)
+          if (lane + 32 * k < W)
+            __pipeline_memcpy_async(&planes[f * WW + y * W + lane + 32 * k], row + (size_t)f * n + gx[k], 8);
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+  }
+  __syncthreads();
+  double* su = planes;
+  double* sv = planes + WW;
+  double* sp = planes + 2 * WW;
+  double* sun = planes + 3 * WW;
+  double* svn = planes + 4 * WW;
+  const double* au = w;
+  const double* av = w + n;
+  const double* ap = w + 2 * n;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int M = H - 3 * s;
+    // u', v' on margin M - 2 (frozen tendencies read from global memory / L2)
+    {
+      const int m = M - 2, R = T + 2 * m, o = H - m;
+      for (int c = threadIdx.x; c < R * R; c += blockDim.x) {
+        const int ly = c / R, lx = c - ly * R;
+        const int off = (ly + o) * W + (lx + o);
+        int gy = ty0 - m + ly, gxx = tx0 - m + lx;
+        gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
+        gxx = gxx < 0 ? gxx + nx : (gxx >= nx ? gxx - nx : gxx);
+        const int cell = gy * nx + gxx;
+        const SAccV acc{su + off, sv + off, sp + off, W, au[cell], av[cell]};
+        sun[off] = un_at<0, 0>(acc, p, sx, sy, tau, damp);
+        svn[off] = vn_at<0, 0>(acc, p, sx, sy, tau, damp);
+      }
+    }
+    __syncthreads();
+    // p' on margin M - 3 (in place: every thread reads and writes only its own p cells)
+    {
+      const int m = M - 3, R = T + 2 * m, o = H - m;
+      for (int c = threadIdx.x; c < R * R; c += blockDim.x) {
+        const int ly = c / R, lx = c - ly * R;
+        const int off = (ly + o) * W + (lx + o);
+        int gy = ty0 - m + ly, gxx = tx0 - m + lx;
+        gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
+        gxx = gxx < 0 ? gxx + nx : (gxx >= nx ? gxx - nx : gxx);
+        const int cell = gy * nx + gxx;
+        const double divn = (sun[off + 1] - sun[off - 1]) * sx + (svn[off + W] - svn[off - W]) * sy;
+        sp[off] = sp[off] + tau * (ap[cell] - p.cs * divn);
+      }
+    }
+    __syncthreads();
+    double* t = su; su = sun; sun = t;
+    t = sv; sv = svn; svn = t;
+  }
+  // ---- the tile's new (u, v, p)
+  for (int c = threadIdx.x; c < T * T; c += blockDim.x) {
+    const int ly = c / T, lx = c - ly * T;
+    const int off = (ly + H) * W + (lx + H);
+    const int cell = (ty0 + ly) * nx + tx0 + lx;
+    nu[cell] = su[off];
+    nu[n + cell] = sv[off];
+    nu[2 * n + cell] = sp[off];
+  }
+  __syncthreads();
+}
+
+template <int T, int K>
+__global__ void __launch_bounds__(256, 2) fefb_tb_coop(double* st, int batch, long long ld,
+                                                    ExactParams p, int nsteps, double tau, int nsub,
+                                                    double* work) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const int n = nx * ny;
+  const double sx = 0.5 / p.dx, sy = 0.5 / p.dy;
+  const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
+  const int tiles_x = nx / T, tiles = tiles_x * (ny / T);
+  const long long work_items = (long long)tiles * batch;
+  const int stride = gridDim.x * blockDim.x;
+  const int first = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nblk = nsub / K, ntail = nsub - nblk * K;
+  for (int step = 0; step < nsteps; ++step) {
+    for (long long b = 0; b < batch; ++b)
+      for (int cell = first; cell < n; cell += stride) {
+        const int j = cell / nx, i = cell - j * nx;
+        const double* q = st + b * ld;
+        double* w = work + b * 6 * n;
+        w[cell] = adv_at(p, q, j, i);
+        w[n + cell] = adv_at(p, q + n, j, i);
+        w[2 * n + cell] = adv_at(p, q + 2 * n, j, i);
+      }
+    grid.sync();
+    int blk = 0;
+    for (; blk < nblk + ntail; ++blk) {
+      const bool from_state = (blk % 2 == 0);
+      for (long long it = blockIdx.x; it < work_items; it += gridDim.x) {
+        const long long b = it / tiles;
+        const int t = (int)(it - b * tiles);
+        const int ty0 = (t / tiles_x) * T, tx0 = (t % tiles_x) * T;
+        double* w = work + b * 6 * n;
+        double* sb = st + b * ld;
+        const double* cu = from_state ? sb : w + 3 * n;
+        double* nu = from_state ? w + 3 * n : sb;
+        if (blk < nblk) tb_block<T, K>(sm, cu, nu, w, tx0, ty0, p, sx, sy, tau, damp);
+        else tb_block<T, 1>(sm, cu, nu, w, tx0, ty0, p, sx, sy, tau, damp);
+      }
+      grid.sync();
+    }
+    if (blk % 2 == 1) {
+      for (long long b = 0; b < batch; ++b)
+        for (int cell = first; cell < n; cell += stride) {
+          double* w = work + b * 6 * n;
+          double* sb = st + b * ld;
+          sb[cell] = w[3 * n + cell];
+          sb[n + cell] = w[4 * n + cell];
+          sb[2 * n + cell] = w[5 * n + cell];
+        }
+      grid.sync();
+    }
+  }
+}
+
+template <int T, int K>
+constexpr size_t tb_smem() {
+  return sizeof(double) * 5 * (T + 6 * K) * (T + 6 * K);
+}
+
 template <int T>
 constexpr size_t tiled_smem() {
   return sizeof(double) * (3 * (T + 6) * (T + 6) + 2 * (T + 2) * (T + 2));
@@ -449,12 +631,49 @@ static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch
   c.launches += 1;
 }
 
+template <int T, int K>
+static void launch_tb(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                      int nsteps, double h, int nsub, double* work) {
+  static int per_sm = -1;
+  constexpr size_t smem = tb_smem<T, K>();
+  if (per_sm < 0) {
+    PW_CUDA(cudaFuncSetAttribute(fefb_tb_coop<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fefb_tb_coop<T, K>, 256, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long items = (long long)(p.nx / T) * (p.ny / T) * batch;
+  const int cap_sm = c.coop_blocks_per_sm > 0 ? std::min(per_sm, c.coop_blocks_per_sm) : per_sm;
+  int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * cap_sm));
+  double tau = h / nsub;
+  ExactParams pp = p;
+  void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)fefb_tb_coop<T, K>, dim3(blocks), dim3(256), args, smem,
+                                      c.stream));
+  c.launches += 1;
+}
+
+static int coarse_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PW_COARSE_VARIANT");  // tuning hook (scripts/microbench.py coarse)
+    v = (e && *e) ? atoi(e) : 0;
+  }
+  return v;
+}
+
 void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                        int nsteps, double h, int nsub, double* work) {
   if (nsteps <= 0 || batch <= 0) return;
   PW_CHECK((long long)p.nx * p.ny < (1LL << 31), PW_ERR_VALUE, "grid too large");
-  if (!c.strict && p.nx % 32 == 0 && p.ny % 32 == 0 && (long long)p.nx * p.ny >= 65536)
-    return launch_tiled<32>(c, p, states, batch, ld, nsteps, h, nsub, work);
+  if (!c.strict && p.nx % 32 == 0 && p.ny % 32 == 0 && (long long)p.nx * p.ny >= 65536) {
+    switch (coarse_variant()) {
+      case 1: return launch_tiled<32>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 2: return launch_tb<32, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 3: return launch_tb<32, 3>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      default: return launch_tb<32, 2>(c, p, states, batch, ld, nsteps, h, nsub, work);
+    }
+  }
   if (!c.strict && p.nx % 16 == 0 && p.ny % 16 == 0)
     return launch_tiled<16>(c, p, states, batch, ld, nsteps, h, nsub, work);
   static int max_per_sm = -1;
