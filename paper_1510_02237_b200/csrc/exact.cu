@@ -418,12 +418,15 @@ struct TbPlanes {
   double* vn;
 };
 
-template <int T, int K>
+template <int TM, int K, bool FIX>
 __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ cu,
                                          double* __restrict__ nu, const double* __restrict__ w,
-                                         int tx0, int ty0, const ExactParams& p, double sx,
-                                         double sy, double tau, bool damp) {
-  constexpr int H = 3 * K, W = T + 2 * H, WW = W * W;
+                                         int tx0, int ty0, int twx_, int twy_, const ExactParams& p,
+                                         double sx, double sy, double tau, bool damp) {
+  // TM: largest tile edge (fixes the shared-memory pitch); this tile is twx x twy
+  // (FIX: every tile is TM x TM -- compile-time loop bounds)
+  const int twx = FIX ? TM : twx_, twy = FIX ? TM : twy_;
+  constexpr int H = 3 * K, W = TM + 2 * H, WW = W * W;
   const int nx = p.nx, ny = p.ny, n = nx * ny;
   double* planes = sm;  // u, v, p, un, vn : W x W each
   // ---- stage (u, v, p) with halo H
@@ -437,7 +440,7 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
       x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
       gx[k] = x;
     }
-    for (int y = warp; y < W; y += 8) {
+    for (int y = warp; y < twy + 2 * H; y += 8) {
       int gy = ty0 - H + y;
       gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
       const double* row = cu + (size_t)gy * nx;
@@ -445,7 +448,7 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
       for (int f = 0; f < 3; ++f)
 #pragma unroll
         for (int k = 0; k < CX; ++k)
-          if (lane + 32 * k < W)
+          if (lane + 32 * k < twx + 2 * H)
             __pipeline_memcpy_async(&planes[f * WW + y * W + lane + 32 * k], row + (size_t)f * n + gx[k], 8);
     }
     __pipeline_commit();
@@ -465,9 +468,9 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
     const int M = H - 3 * s;
     // u', v' on margin M - 2 (frozen tendencies read from global memory / L2)
     {
-      const int m = M - 2, R = T + 2 * m, o = H - m;
-      for (int c = threadIdx.x; c < R * R; c += blockDim.x) {
-        const int ly = c / R, lx = c - ly * R;
+      const int m = M - 2, Rx = twx + 2 * m, Ry = twy + 2 * m, o = H - m;
+      for (int c = threadIdx.x; c < Rx * Ry; c += blockDim.x) {
+        const int ly = c / Rx, lx = c - ly * Rx;
         const int off = (ly + o) * W + (lx + o);
         int gy = ty0 - m + ly, gxx = tx0 - m + lx;
         gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
@@ -481,9 +484,9 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
     __syncthreads();
     // p' on margin M - 3 (in place: every thread reads and writes only its own p cells)
     {
-      const int m = M - 3, R = T + 2 * m, o = H - m;
-      for (int c = threadIdx.x; c < R * R; c += blockDim.x) {
-        const int ly = c / R, lx = c - ly * R;
+      const int m = M - 3, Rx = twx + 2 * m, Ry = twy + 2 * m, o = H - m;
+      for (int c = threadIdx.x; c < Rx * Ry; c += blockDim.x) {
+        const int ly = c / Rx, lx = c - ly * Rx;
         const int off = (ly + o) * W + (lx + o);
         int gy = ty0 - m + ly, gxx = tx0 - m + lx;
         gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
@@ -498,8 +501,8 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
     t = sv; sv = svn; svn = t;
   }
   // ---- the tile's new (u, v, p)
-  for (int c = threadIdx.x; c < T * T; c += blockDim.x) {
-    const int ly = c / T, lx = c - ly * T;
+  for (int c = threadIdx.x; c < twx * twy; c += blockDim.x) {
+    const int ly = c / twx, lx = c - ly * twx;
     const int off = (ly + H) * W + (lx + H);
     const int cell = (ty0 + ly) * nx + tx0 + lx;
     nu[cell] = su[off];
@@ -509,8 +512,8 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
   __syncthreads();
 }
 
-template <int T, int K>
-__global__ void __launch_bounds__(256, 2) fefb_tb_coop(double* st, int batch, long long ld,
+template <int TM, int K, int MINB, bool FIX>
+__global__ void __launch_bounds__(256, MINB) fefb_tb_coop(double* st, int batch, long long ld,
                                                     ExactParams p, int nsteps, double tau, int nsub,
                                                     double* work) {
   cg::grid_group grid = cg::this_grid();
@@ -519,7 +522,8 @@ __global__ void __launch_bounds__(256, 2) fefb_tb_coop(double* st, int batch, lo
   const int n = nx * ny;
   const double sx = 0.5 / p.dx, sy = 0.5 / p.dy;
   const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
-  const int tiles_x = nx / T, tiles = tiles_x * (ny / T);
+  // near-equal tiles of at most TM x TM (edges floor(k n / tiles))
+  const int tiles_x = (nx + TM - 1) / TM, tiles_y = (ny + TM - 1) / TM, tiles = tiles_x * tiles_y;
   const long long work_items = (long long)tiles * batch;
   const int stride = gridDim.x * blockDim.x;
   const int first = blockIdx.x * blockDim.x + threadIdx.x;
@@ -541,13 +545,16 @@ __global__ void __launch_bounds__(256, 2) fefb_tb_coop(double* st, int batch, lo
       for (long long it = blockIdx.x; it < work_items; it += gridDim.x) {
         const long long b = it / tiles;
         const int t = (int)(it - b * tiles);
-        const int ty0 = (t / tiles_x) * T, tx0 = (t % tiles_x) * T;
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int ty0 = (int)((long long)iy * ny / tiles_y), tx0 = (int)((long long)ix * nx / tiles_x);
+        const int twy = (int)((long long)(iy + 1) * ny / tiles_y) - ty0;
+        const int twx = (int)((long long)(ix + 1) * nx / tiles_x) - tx0;
         double* w = work + b * 6 * n;
         double* sb = st + b * ld;
         const double* cu = from_state ? sb : w + 3 * n;
         double* nu = from_state ? w + 3 * n : sb;
-        if (blk < nblk) tb_block<T, K>(sm, cu, nu, w, tx0, ty0, p, sx, sy, tau, damp);
-        else tb_block<T, 1>(sm, cu, nu, w, tx0, ty0, p, sx, sy, tau, damp);
+        if (blk < nblk) tb_block<TM, K, FIX>(sm, cu, nu, w, tx0, ty0, twx, twy, p, sx, sy, tau, damp);
+        else tb_block<TM, 1, FIX>(sm, cu, nu, w, tx0, ty0, twx, twy, p, sx, sy, tau, damp);
       }
       grid.sync();
     }
@@ -565,9 +572,9 @@ __global__ void __launch_bounds__(256, 2) fefb_tb_coop(double* st, int batch, lo
   }
 }
 
-template <int T, int K>
+template <int TM, int K>
 constexpr size_t tb_smem() {
-  return sizeof(double) * 5 * (T + 6 * K) * (T + 6 * K);
+  return sizeof(double) * 5 * (TM + 6 * K) * (TM + 6 * K);
 }
 
 template <int T>
@@ -631,25 +638,25 @@ static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch
   c.launches += 1;
 }
 
-template <int T, int K>
+template <int TM, int K, int MINB, bool FIX>
 static void launch_tb(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                       int nsteps, double h, int nsub, double* work) {
+  auto kern = fefb_tb_coop<TM, K, MINB, FIX>;
   static int per_sm = -1;
-  constexpr size_t smem = tb_smem<T, K>();
+  constexpr size_t smem = tb_smem<TM, K>();
   if (per_sm < 0) {
-    PW_CUDA(cudaFuncSetAttribute(fefb_tb_coop<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fefb_tb_coop<T, K>, 256, smem));
+    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
     if (per_sm < 1) per_sm = 1;
   }
-  const long long items = (long long)(p.nx / T) * (p.ny / T) * batch;
+  const long long items =
+      (long long)((p.nx + TM - 1) / TM) * ((p.ny + TM - 1) / TM) * batch;
   const int cap_sm = c.coop_blocks_per_sm > 0 ? std::min(per_sm, c.coop_blocks_per_sm) : per_sm;
   int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * cap_sm));
   double tau = h / nsub;
   ExactParams pp = p;
   void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work};
-  PW_CUDA(cudaLaunchCooperativeKernel((void*)fefb_tb_coop<T, K>, dim3(blocks), dim3(256), args, smem,
-                                      c.stream));
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(256), args, smem, c.stream));
   c.launches += 1;
 }
 
@@ -669,9 +676,10 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
   if (!c.strict && p.nx % 32 == 0 && p.ny % 32 == 0 && (long long)p.nx * p.ny >= 65536) {
     switch (coarse_variant()) {
       case 1: return launch_tiled<32>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      case 2: return launch_tb<32, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      case 3: return launch_tb<32, 3>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      default: return launch_tb<32, 2>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 2: return launch_tb<32, 1, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 3: return launch_tb<44, 2, 1, false>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 4: return launch_tb<44, 2, 2, false>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      default: return launch_tb<32, 2, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
     }
   }
   if (!c.strict && p.nx % 16 == 0 && p.ny % 16 == 0)
