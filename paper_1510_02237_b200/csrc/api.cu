@@ -963,8 +963,10 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         for (int i = 0; i < n_c; ++i) {
           double* yi = Yt + (size_t)(i % 2) * d;
           PW_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+          // one CTA per SM: leaves room for G's co-resident cooperative CTAs (whichever of the
+          // two the scheduler starts first)
           pw::launch_combine_gemv(c, c.side, nullptr, B->Y.p, r, PRED + (size_t)i * d, a_cur, nullptr,
-                                  0, d, yi, nullptr, nullptr);
+                                  0, d, yi, nullptr, nullptr, pw::combine_grid(c, d, 1));
           PW_CUDA(cudaEventRecord(c.ev_join, c.side));
           prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
           PW_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));

@@ -46,29 +46,32 @@ __device__ __forceinline__ double face_flux(int order, double u, double qm2, dou
 
 // x-face flux on face f of row j (window cells f-3..f+2)
 __device__ __forceinline__ double fx_at(const ExactParams& p, const double* __restrict__ q, int j,
-                                        int f) {
+                                        int f, int order) {
   const double* row = q + (size_t)j * p.nx;
-  return face_flux(p.order, p.uf[(size_t)j * p.nx + f], row[wrapi(f - 3, p.nx)],
+  return face_flux(order, p.uf[(size_t)j * p.nx + f], row[wrapi(f - 3, p.nx)],
                    row[wrapi(f - 2, p.nx)], row[wrapi(f - 1, p.nx)], row[f],
                    row[wrapi(f + 1, p.nx)], row[wrapi(f + 2, p.nx)]);
 }
 
 __device__ __forceinline__ double gy_at(const ExactParams& p, const double* __restrict__ q, int f,
-                                        int i) {
+                                        int i, int order) {
   const int nx = p.nx, ny = p.ny;
-  return face_flux(p.order, p.vf[(size_t)f * nx + i], q[(size_t)wrapi(f - 3, ny) * nx + i],
+  return face_flux(order, p.vf[(size_t)f * nx + i], q[(size_t)wrapi(f - 3, ny) * nx + i],
                    q[(size_t)wrapi(f - 2, ny) * nx + i], q[(size_t)wrapi(f - 1, ny) * nx + i],
                    q[(size_t)f * nx + i], q[(size_t)wrapi(f + 1, ny) * nx + i],
                    q[(size_t)wrapi(f + 2, ny) * nx + i]);
 }
 
-// advective_tendency = flux_divergence(flux_x, flux_y) at cell (j, i)
+// advective_tendency = flux_divergence(flux_x, flux_y) at cell (j, i); ORD > 0 fixes the
+// flux order at compile time (the coarse propagator's order-1 flux), 0 reads p.order
+template <int ORD = 0>
 __device__ __forceinline__ double adv_at(const ExactParams& p, const double* __restrict__ q, int j,
                                          int i) {
+  const int order = ORD > 0 ? ORD : p.order;
   const int ip = i + 1 < p.nx ? i + 1 : 0;
   const int jp = j + 1 < p.ny ? j + 1 : 0;
-  const double fxi = fx_at(p, q, j, i), fxp = fx_at(p, q, j, ip);
-  const double gyj = gy_at(p, q, j, i), gyp = gy_at(p, q, jp, i);
+  const double fxi = fx_at(p, q, j, i, order), fxp = fx_at(p, q, j, ip, order);
+  const double gyj = gy_at(p, q, j, i, order), gyp = gy_at(p, q, jp, i, order);
   const double tx = -(fxp - fxi), ty = (gyp - gyj);
   return (p.inv_dx != 0.0 ? tx * p.inv_dx : tx / p.dx) - (p.inv_dy != 0.0 ? ty * p.inv_dy : ty / p.dy);
 }
@@ -512,7 +515,7 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
   __syncthreads();
 }
 
-template <int TM, int K, int MINB, bool FIX>
+template <int TM, int K, int MINB, bool FIX, int ORD>
 __global__ void __launch_bounds__(256, MINB) fefb_tb_coop(double* st, int batch, long long ld,
                                                     ExactParams p, int nsteps, double tau, int nsub,
                                                     double* work) {
@@ -534,9 +537,9 @@ __global__ void __launch_bounds__(256, MINB) fefb_tb_coop(double* st, int batch,
         const int j = cell / nx, i = cell - j * nx;
         const double* q = st + b * ld;
         double* w = work + b * 6 * n;
-        w[cell] = adv_at(p, q, j, i);
-        w[n + cell] = adv_at(p, q + n, j, i);
-        w[2 * n + cell] = adv_at(p, q + 2 * n, j, i);
+        w[cell] = adv_at<ORD>(p, q, j, i);
+        w[n + cell] = adv_at<ORD>(p, q + n, j, i);
+        w[2 * n + cell] = adv_at<ORD>(p, q + 2 * n, j, i);
       }
     grid.sync();
     int blk = 0;
@@ -638,10 +641,10 @@ static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch
   c.launches += 1;
 }
 
-template <int TM, int K, int MINB, bool FIX>
+template <int TM, int K, int MINB, bool FIX, int ORD = 0>
 static void launch_tb(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                       int nsteps, double h, int nsub, double* work) {
-  auto kern = fefb_tb_coop<TM, K, MINB, FIX>;
+  auto kern = fefb_tb_coop<TM, K, MINB, FIX, ORD>;
   static int per_sm = -1;
   constexpr size_t smem = tb_smem<TM, K>();
   if (per_sm < 0) {
@@ -679,7 +682,12 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
       case 2: return launch_tb<32, 1, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
       case 3: return launch_tb<44, 2, 1, false>(c, p, states, batch, ld, nsteps, h, nsub, work);
       case 4: return launch_tb<44, 2, 2, false>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      default: return launch_tb<32, 2, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 5:
+        if (p.order == 1) return launch_tb<32, 2, 3, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
+        return launch_tb<32, 2, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      default:
+        if (p.order == 1) return launch_tb<32, 2, 2, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
+        return launch_tb<32, 2, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
     }
   }
   if (!c.strict && p.nx % 16 == 0 && p.ny % 16 == 0)

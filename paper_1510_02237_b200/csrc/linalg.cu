@@ -640,7 +640,7 @@ static int cg_variant() {
 
 // persistent grid of at most per_sm CTAs per SM, sized so every CTA walks the same number of
 // 1024-row tiles (768 tiles at c3 -> 384 CTAs x 2 tiles instead of 444 CTAs x 1.73)
-static int combine_grid(const Ctx& c, long long d, int per_sm = 2) {
+int combine_grid(const Ctx& c, long long d, int per_sm) {
   const long long ntiles = (d + kCgRows - 1) / kCgRows;
   const long long cap = std::max<long long>(1, (long long)per_sm * c.num_sms);
   const long long per_cta = (ntiles + cap - 1) / cap;

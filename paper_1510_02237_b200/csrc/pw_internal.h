@@ -140,6 +140,8 @@ void launch_residual(Ctx& c, const double* a, long long lda, const double* b, lo
 // fp64 pipe peak probe (probe.cu): best-of-3 DFMA throughput in TFLOP/s
 double probe_fp64_tflops(Ctx& c, int iters);
 
+// balanced persistent grid for the combine/projection kernels: <= per_sm CTAs per SM
+int combine_grid(const Ctx& c, long long d, int per_sm = 2);
 size_t combine_part_doubles(long long d, int r);
 // R: mr x m (lda mr), mr = min(d, m); returns rank, fills piv (m), tau/diag (min(mr, m))
 int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv_dev,
