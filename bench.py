@@ -325,6 +325,13 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     if rank == 0 and world == 1 and args.parareal:
         extra["parareal"] = parareal_c3(local_rank)
+        if args.c4:
+            del x, out, flush, pinned_in, pinned_out
+            torch.cuda.empty_cache()
+            try:
+                extra["parareal_c4"] = parareal_window("c4")
+            except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
+                extra["parareal_c4"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         line = {
             "metric": "fine RK-3 fp64 cell-updates/s", "value": value, "unit": "cell-updates/s",
@@ -370,6 +377,9 @@ def main():
     ap.add_argument("--parareal", dest="parareal", action="store_true", default=True)
     ap.add_argument("--no-parareal", dest="parareal", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c4", dest="c4", action="store_true", default=True,
+                    help="also time one c4 window (1024^2, P=256, K=4; ~20 s)")
+    ap.add_argument("--no-c4", dest="c4", action="store_false")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
