@@ -1,14 +1,15 @@
-"""c4 (1024^2, P=256) first-iteration fixture from the REFERENCE itself (this container only).
+"""c3 / c4 KSE-window fixtures from the REFERENCE itself (this container only).
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_c4_golden.py [n_it]
+        python tests/golden/make_window_golden.py [n_it] [config]
 
-Runs the reference's kse_sweep on BASELINE config 4 (harness.WORKLOADS["c4"]) for n_it
-iterations (default 1; each further iteration costs the reference a single-threaded
-pivoted QR of 3.1M x 256k) with a thread pool for the fine sweep, and stores what a
-multi-GB window can be pinned by in a small file: the residual history, the ranks, the
-per-slice L2 norms of qn[1:] after every iteration and 512 fixed-seed sampled entries
-per slice.  The state itself (6 GB per iteration) is not stored.
+Runs the reference's kse_sweep on a BASELINE config (default c4 = harness.WORKLOADS["c4"],
+1024^2, P=256; or c3) for n_it iterations (default 1; at c4 each further iteration
+costs the reference a single-threaded pivoted QR of 3.1M x 256k) with a thread pool for
+the fine sweep, and stores what a multi-GB window can be pinned by in a small file
+(<config>_reference.npz): the residual history, the ranks, the per-slice L2 norms of
+qn[1:] after every iteration and 512 fixed-seed sampled entries per slice.  The states
+themselves (6 GB per iteration at c4) are not stored.
 """
 from __future__ import annotations
 
@@ -32,10 +33,10 @@ from paper_1510_02237_b200 import harness  # noqa: E402  (seeded generators only
 N_SAMPLE = 512
 
 
-def main(n_it=1):
-    wl = harness.WORKLOADS["c4"]
+def main(n_it=1, name="c4"):
+    wl = harness.WORKLOADS[name]
     fine, coarse = slice_closures(wl)
-    q0 = harness.initial_state("c4")
+    q0 = harness.initial_state(name)
     d = q0.size
     idx = np.sort(np.random.default_rng(4242).choice(d, N_SAMPLE, replace=False))
     norms, samples, ranks = [], [], []
@@ -67,11 +68,11 @@ def main(n_it=1):
     finally:
         ref_sub.Subspace.update = orig_update
         ref_par.iteration_residual = orig_res
-    np.savez_compressed(os.path.join(HERE, "c4_reference.npz"), res=np.array(res), ranks=np.array(ranks),
+    np.savez_compressed(os.path.join(HERE, f"{name}_reference.npz"), res=np.array(res), ranks=np.array(ranks),
                         norms=np.array(norms), samples=np.array(samples), idx=idx,
                         seconds=time.time() - t0, threads=os.cpu_count())
     print(f"done in {time.time() - t0:.0f} s: residuals {res}, ranks {ranks}")
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 1)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 1, sys.argv[2] if len(sys.argv) > 2 else "c4")
