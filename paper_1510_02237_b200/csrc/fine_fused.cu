@@ -85,7 +85,9 @@ struct RowP {
   const double* o;
 };
 __device__ __forceinline__ RowP rowp_of(const double* slot_base, int s, int c) {
-  const int f = slot_flip(s);
+  // physical chunk = (c/2 + k) ^ flip: +2 doubles for even absolute chunks, -2 for odd
+  // ones; a group whose first chunk is odd (BX = 2) swaps the roles of e and o
+  const int f = ((c >> 1) & 1) ? -slot_flip(s) : slot_flip(s);
   return RowP{slot_base + c + 2 * f, slot_base + c - 2 * f};
 }
 
@@ -276,7 +278,7 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
 }
 
 template <class K>
-__global__ void __launch_bounds__(K::NT, 1) rk3_fused_kernel(const double* __restrict__ in,
+__global__ void __launch_bounds__(K::NT, K::MINB_SMEM < 1 ? 1 : K::MINB_SMEM) rk3_fused_kernel(const double* __restrict__ in,
                                                           double* __restrict__ out, FusedParams P) {
   extern __shared__ __align__(16) double smem[];
   double* q_ring = smem;
