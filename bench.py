@@ -193,9 +193,11 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def parareal_window(name="c3", warm=True):
+def parareal_window(name="c3", warm=True, group=None):
     """One KSE-Parareal window of config `name` (c3: 512^2, P=64, K=5; c4: 1024^2, P=256,
-    K=4): per-iteration device time and phases."""
+    K=4): per-iteration device time and phases.  Under torchrun (`group`) the fine sweep
+    is slice-sharded over the ranks (dist.ShardedFine, NCCL all-gather of the end states)
+    and the serial correction is replicated; the window time is the max over ranks."""
     import torch
 
     from paper_1510_02237_b200 import harness
@@ -214,13 +216,22 @@ def parareal_window(name="c3", warm=True):
     q0 = torch.as_tensor(harness.initial_state(name)).cuda()
     if warm:
         # warm-up: first-use module loads (cuSOLVER/cuBLAS lazy loading) and pool allocations
-        kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True)
+        kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True, group=group)
     tm = Timings()
+    if group is not None:
+        torch.distributed.barrier(group)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm, return_device=True)
+    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm, return_device=True,
+                               group=group)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    n_ranks = 1
+    if group is not None:
+        t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=group)
+        wall = float(t.item())
+        n_ranks = torch.distributed.get_world_size(group)
     d = q0.numel()
     return {"workload": f"{name}: {wl.n}^2, P={wl.n_p}, K={wl.n_it} KSE-Parareal window",
             "window_s": wall, "iteration_s": wall / wl.n_it,
@@ -228,7 +239,9 @@ def parareal_window(name="c3", warm=True):
             "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res],
             "fine_cell_updates_per_s": wl.n_p * wl.n_it * fine.nsteps * d / 3 / tm.fine if tm.fine else None,
             "peak_device_gib": torch.cuda.max_memory_allocated() / 2**30,
-            "warm": warm}
+            "warm": warm, "n_gpus": n_ranks,
+            "parallelism": "fine sweep slice-sharded over ranks, serial correction replicated"
+                           if n_ranks > 1 else "single GPU"}
 
 
 def parareal_c3(dev_index):
@@ -326,6 +339,8 @@ def run_ours(args, rank, world, local_rank):
     fp64_achieved = FLOP_PER_CELL_UPDATE * value / world / 1e12
 
     extra = {}
+    if world > 1 and args.parareal:
+        extra["parareal"] = parareal_window("c3", group=dist.group.WORLD)
     if rank == 0 and world == 1 and args.parareal:
         extra["parareal"] = parareal_c3(local_rank)
         if args.c4:
