@@ -894,6 +894,13 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
                           std::max(4.0 * (1ull << 30), 0.06 * (double)total_b);
       const char* e = getenv("PW_SWEEP_LEAN");
       B->lean = (e && *e == '1') || need > (double)free_b;
+      // even lean (4 d x cap matrices) must fit, or fail now instead of after the first fine
+      // sweep (c5 on one GPU: 4 x 96 GiB; it needs the row-sharded basis of SURVEY 8(e))
+      const double need_lean = need - col * std::min<long long>(B->cap, d);
+      PW_CHECK(need_lean <= (double)free_b, PW_ERR_MEMORY,
+               "KSE sweep needs ~" + std::to_string((long long)(need_lean / (1 << 30))) +
+                   " GiB for its d x " + std::to_string(B->cap) + " basis even without a snapshot copy; " +
+                   std::to_string((long long)(free_b >> 30)) + " GiB free on this device");
     }
     cudaEvent_t ev[4];
     const bool timed = timings != nullptr;
