@@ -142,6 +142,25 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
 typedef int (*pw_fine_hook)(void* user, const double* qk, double* pred, int n_c, long long dim);
 int pw_ctx_set_fine_hook(pw_ctx* ctx, pw_fine_hook hook, void* user);
 
+/* ---- row-sharded serial correction --------------------------
+ * With world > 1 every rank keeps the whole subspace (replicated, deterministic
+ * refactorisation) but streams only its row block [rank*blk, (rank+1)*blk) of D
+ * and Q in each serial step (blk = ceil(dim/world) rounded up to even).  Per step
+ * the sweep calls, on the context stream:
+ *   allreduce(user, data, count)        in-place sum over ranks of count doubles
+ *                                       (the partial alpha_{i+1} = Q_g^T y_g)
+ *   allgather(user, data, block, total) data[rank*block .. +block) is valid on this
+ *                                       rank; fill the other ranks' blocks (the
+ *                                       last block may be shorter than `block`)
+ * Both return 0 on success.  world = 1 (default) keeps the single-device loop.
+ * pw_ctx_set_row_shards(ctx, n) runs n row shards inside one process, summing
+ * the partials in shard order (the same arithmetic as n ranks; for tests). */
+typedef int (*pw_allreduce_hook)(void* user, double* data, long long count);
+typedef int (*pw_allgather_hook)(void* user, double* data, long long block, long long total);
+int pw_ctx_set_comm(pw_ctx* ctx, int rank, int world, pw_allreduce_hook allreduce,
+                    pw_allgather_hook allgather, void* user);
+int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards);
+
 /* ---- memory helper ------------------------------------------------------
  * stream-ordered copy of nbytes between any host/device pointers (UVA,
  * cudaMemcpyDefault), synchronising the context stream afterwards. */

@@ -26,6 +26,8 @@ c_dp = ctypes.POINTER(ctypes.c_double)
 c_ip = ctypes.POINTER(ctypes.c_int)
 c_vp = ctypes.c_void_p
 FINE_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong)
+ALLREDUCE_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, ctypes.c_longlong)
+ALLGATHER_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong)
 
 
 class PdeDesc(ctypes.Structure):
@@ -77,6 +79,9 @@ SIGNATURES = [
                                 ctypes.c_double, ctypes.c_double, c_vp, c_dp, c_ip, c_dp, c_ip,
                                 ctypes.POINTER(c_vp)]),
     ("pw_ctx_set_fine_hook", ctypes.c_int, [c_vp, FINE_HOOK, c_vp]),
+    ("pw_ctx_set_comm", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ALLREDUCE_HOOK, ALLGATHER_HOOK,
+                                       c_vp]),
+    ("pw_ctx_set_row_shards", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
     ("pw_probe_fp64_peak", ctypes.c_int, [c_vp, ctypes.c_int, c_dp]),
@@ -164,6 +169,11 @@ class Context:
 
     def synchronize(self):
         check(self.lib.pw_ctx_synchronize(self.handle))
+
+    def set_row_shards(self, n: int):
+        """Run the serial correction as n row shards in this process (tests of the
+        multi-GPU arithmetic); 1 restores the single-shard loop."""
+        check(self.lib.pw_ctx_set_row_shards(self.handle, int(n)))
 
     def fp64_peak_tflops(self, iters: int = 4096) -> float:
         """DFMA-throughput probe (TFLOP/s, FMA = 2 flop): the fp64 roofline denominator."""

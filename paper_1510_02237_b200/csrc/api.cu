@@ -585,11 +585,7 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     PW_SOLVER(cusolverDnCreate(&sh));
     PW_SOLVER(cusolverDnSetStream(sh, ctx->c.stream));
     ctx->c.cusolver = sh;
-    PW_CUDA(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
-    PW_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming));
-    PW_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming));
-    if (const char* e = std::getenv("PW_COOP_CAP")) ctx->c.sweep_coop_cap = std::atoi(e);
-    if (const char* e = std::getenv("PW_SWEEP_OVERLAP")) ctx->c.sweep_overlap = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PW_ROW_SHARDS")) ctx->c.vshards = std::atoi(e);
     *out = ctx.release();
   });
 }
@@ -603,13 +599,28 @@ int pw_ctx_destroy(pw_ctx* ctx) {
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
     if (ctx->c.cusolver_params) cusolverDnDestroyParams(static_cast<cusolverDnParams_t>(ctx->c.cusolver_params));
     if (ctx->c.cusolver) cusolverDnDestroy(solver(ctx->c));
-    if (ctx->c.side) {
-      cudaStreamSynchronize(ctx->c.side);
-      cudaStreamDestroy(ctx->c.side);
-    }
-    if (ctx->c.ev_fork) cudaEventDestroy(ctx->c.ev_fork);
-    if (ctx->c.ev_join) cudaEventDestroy(ctx->c.ev_join);
     delete ctx;
+  });
+}
+
+int pw_ctx_set_comm(pw_ctx* ctx, int rank, int world, pw_allreduce_hook allreduce,
+                    pw_allgather_hook allgather, void* user) {
+  return guarded([&] {
+    PW_CHECK(ctx, PW_ERR_VALUE, "ctx is NULL");
+    PW_CHECK(world >= 1 && rank >= 0 && rank < world, PW_ERR_VALUE, "bad rank / world");
+    PW_CHECK(world == 1 || (allreduce && allgather), PW_ERR_VALUE, "world > 1 needs both hooks");
+    ctx->c.comm_rank = rank;
+    ctx->c.comm_world = world;
+    ctx->c.allreduce_hook = allreduce;
+    ctx->c.allgather_hook = allgather;
+    ctx->c.comm_user = user;
+  });
+}
+
+int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards) {
+  return guarded([&] {
+    PW_CHECK(ctx && nshards >= 1, PW_ERR_VALUE, "bad argument");
+    ctx->c.vshards = nshards;
   });
 }
 
@@ -872,7 +883,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     const long long d = fine->dim;
     const bool kse = mode == PW_MODE_KSE;
     // buffers (column-major, ld = d)
-    DBuf bQK, bQN, bPred, bGK, bGN, bRes, bScr, bAlpha, bPart, bYt;
+    DBuf bQK, bQN, bPred, bGK, bGN, bRes, bScr, bAlpha, bPart, bAlphaPart;
     double* QK = bQK.ensure(c, (size_t)d * (n_c + 1));
     double* QN = bQN.ensure(c, (size_t)d * (n_c + 1));
     double* PRED = bPred.ensure(c, (size_t)d * n_c);
@@ -958,32 +969,54 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       double* part = bPart.ensure(c, pw::combine_part_doubles(d, kse ? (int)std::min<long long>(B->cap, d) : 1));
       double* a_cur = alpha;
       double* a_buf[2] = {alpha_next, alpha_next ? alpha_next + r : nullptr};
-      if (r > 0 && c.sweep_overlap) {
-        // Two streams per correction step i:
-        //   side: y_i = c_i + D alpha_i            (waits for alpha_i)
-        //   main: G(qn_i); qn_{i+1} = G + y_i;  alpha_{i+1} = Q^T qn_{i+1}
-        // so the D pass (r*d*8 bytes) streams while the latency-bound coarse G runs.
-        double* Yt = bYt.ensure(c, (size_t)d * 2);
-        PW_CUDA(cudaEventRecord(c.ev_fork, c.stream));
-        const int saved_cap = c.coop_blocks_per_sm;
-        c.coop_blocks_per_sm = c.sweep_coop_cap;
+      const bool comm = c.comm_world > 1;
+      const int nsh = (r > 0) ? (comm ? c.comm_world : std::max(1, c.vshards)) : 1;
+      if (nsh > 1) {
+        // Row-sharded serial correction: shard s owns rows [s blk, (s+1) blk)
+        // of D and Q.  Per step: G(qn_i) (replicated), the combine pass over the shard's rows
+        // -> partial alpha_{i+1}, a sum of the partials over the shards, and the shards' rows
+        // of qn_{i+1} gathered back into every replica.  Across ranks (comm hooks) the sum is
+        // an allreduce of r doubles and the gather an all-gather of d doubles; a single
+        // process with vshards > 1 runs every shard itself and sums in shard order (tests).
+        const long long blk = ((d + nsh - 1) / nsh + 1) / 2 * 2;  // even: 16-byte row blocks
+        double* a_part = bAlphaPart.ensure(c, (size_t)r * nsh);
+        if (comm) {  // every replica must have found the same rank
+          double* rr = a_part;
+          const double rv = (double)r;
+          PW_CUDA(cudaMemcpyAsync(rr, &rv, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+          PW_CHECK(c.allreduce_hook(c.comm_user, rr, 1) == 0, PW_ERR_STATE, "allreduce hook failed");
+          double tot = 0.0;
+          PW_CUDA(cudaMemcpyAsync(&tot, rr, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+          PW_CUDA(cudaStreamSynchronize(c.stream));
+          PW_CHECK(tot == rv * c.comm_world, PW_ERR_STATE,
+                   "replicas disagree on the subspace rank (" + std::to_string(r) + " here)");
+        }
         for (int i = 0; i < n_c; ++i) {
-          double* yi = Yt + (size_t)(i % 2) * d;
-          PW_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-          // one CTA per SM: leaves room for G's co-resident cooperative CTAs (whichever of the
-          // two the scheduler starts first)
-          pw::launch_combine_gemv(c, c.side, nullptr, B->Y.p, r, PRED + (size_t)i * d, a_cur, nullptr,
-                                  0, d, yi, nullptr, nullptr, pw::combine_grid(c, d, 1));
-          PW_CUDA(cudaEventRecord(c.ev_join, c.side));
           prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
-          PW_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
           double* a_nxt = a_buf[i % 2];
-          pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, nullptr, 0, yi, nullptr, B->Q.p, r, d,
-                                  QN + (size_t)(i + 1) * d, a_nxt, part);
-          PW_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          const int s0 = comm ? c.comm_rank : 0, s1 = comm ? c.comm_rank + 1 : nsh;
+          for (int sh = s0; sh < s1; ++sh) {
+            const long long lo = std::min<long long>(d, sh * blk), hi = std::min<long long>(d, lo + blk);
+            double* dst = comm ? a_nxt : a_part + (size_t)sh * r;
+            if (hi <= lo) {
+              PW_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * r, c.stream));
+              continue;
+            }
+            pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d + lo, B->Y.p + lo, r,
+                                    PRED + (size_t)i * d + lo, a_cur, B->Q.p + lo, r, hi - lo,
+                                    QN + (size_t)(i + 1) * d + lo, dst, part, 0, d);
+          }
+          if (comm) {
+            PW_CHECK(c.allreduce_hook(c.comm_user, a_nxt, r) == 0, PW_ERR_STATE, "allreduce hook failed");
+            PW_CHECK(c.allgather_hook(c.comm_user, QN + (size_t)(i + 1) * d, blk, d) == 0, PW_ERR_STATE,
+                     "all-gather hook failed");
+          } else {
+            pw::launch_axpby_cols(c, a_nxt, a_part, a_part + r, 1.0, 1.0, (size_t)r);
+            for (int sh = 2; sh < nsh; ++sh)
+              pw::launch_axpby_cols(c, a_nxt, a_nxt, a_part + (size_t)sh * r, 1.0, 1.0, (size_t)r);
+          }
           a_cur = a_nxt;
         }
-        c.coop_blocks_per_sm = saved_cap;
       } else {
         for (int i = 0; i < n_c; ++i) {
           prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);

@@ -250,7 +250,7 @@ __device__ __forceinline__ void cg_load(const double* __restrict__ col, long lon
 
 // wpart[warp][k] += sum over this tile's rows of Q[row, k] * y[row]
 template <bool V2>
-__device__ __forceinline__ void tile_qty(const double* __restrict__ Q, int r, long long d,
+__device__ __forceinline__ void tile_qty(const double* __restrict__ Q, long long ldq, int r, long long d,
                                          long long row0, const double (&y)[kCgRpt],
                                          double* __restrict__ wpart) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -261,7 +261,7 @@ __device__ __forceinline__ void tile_qty(const double* __restrict__ Q, int r, lo
       acc[kk] = 0.0;
       if (k0 + kk < r) {
         double q[kCgRpt];
-        cg_load<V2>(Q + (long long)(k0 + kk) * d, row0, d, q);
+        cg_load<V2>(Q + (long long)(k0 + kk) * ldq, row0, d, q);
 #pragma unroll
         for (int s = 0; s < kCgRpt; ++s) acc[kk] = fma(q[s], y[s], acc[kk]);
       }
@@ -287,8 +287,10 @@ __device__ __forceinline__ void flush_wpart(const double* wpart, int r, double* 
 template <int UNR, int MINB, bool V2>
 __global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
     const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
-    const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d,
+    const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d, long long ld,
     double* __restrict__ y_out, double* __restrict__ part) {
+  // d rows starting at the given pointers; D and Q columns are ld apart (ld >= d: a row
+  // block of a sharded basis passes its block's first-row pointers)
   extern __shared__ double sh[];
   double* a_s = sh;             // rd
   double* wpart = sh + rd;      // kCgWarps x rq
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
     for (; k + UNR <= rd; k += UNR) {
       double t[UNR][kCgRpt];
 #pragma unroll
-      for (int kk = 0; kk < UNR; ++kk) cg_load<V2>(D + (long long)(k + kk) * d, row0, d, t[kk]);
+      for (int kk = 0; kk < UNR; ++kk) cg_load<V2>(D + (long long)(k + kk) * ld, row0, d, t[kk]);
 #pragma unroll
       for (int kk = 0; kk < UNR; ++kk)
 #pragma unroll
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
     }
     for (; k < rd; ++k) {
       double t[kCgRpt];
-      cg_load<V2>(D + (long long)k * d, row0, d, t);
+      cg_load<V2>(D + (long long)k * ld, row0, d, t);
 #pragma unroll
       for (int s = 0; s < kCgRpt; ++s) y[s] = fma(t[s], a_s[k], y[s]);
     }
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
       const long long row = cg_row<V2>(row0, s);
       if (row < d) y_out[row] = y[s];
     }
-    if (rq > 0) tile_qty<V2>(Q, rq, d, row0, y, wpart);
+    if (rq > 0) tile_qty<V2>(Q, ld, rq, d, row0, y, wpart);
   }
   if (rq > 0) flush_wpart(wpart, rq, part);
 }
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kCgThreads, 2) project_partial_kernel(
       const long long row = cg_row<false>(row0, s);
       y[s] = row < d ? v[row] : 0.0;
     }
-    tile_qty<false>(Q, r, d, row0, y, wpart);
+    tile_qty<false>(Q, d, r, d, row0, y, wpart);
   }
   flush_wpart(wpart, r, part);
 }
@@ -650,7 +652,7 @@ int combine_grid(const Ctx& c, long long d, int per_sm) {
 template <int UNR, int MINB, bool V2>
 static int launch_cg(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                       const double* cvec, const double* alpha, const double* Q, int rq, long long d,
-                      double* y, double* part, int nblk) {
+                      long long ld, double* y, double* part, int nblk) {
   auto kern = combine_gemv_kernel<UNR, MINB, V2>;
   if (nblk <= 0) nblk = combine_grid(c, d, MINB);
   size_t smem = sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 1);
@@ -659,28 +661,33 @@ static int launch_cg(Ctx& c, cudaStream_t st, const double* g, const double* D, 
     PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  kern<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, y, part);
+  kern<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part);
   return nblk;
 }
 
 void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                          const double* cvec, const double* alpha, const double* Q, int rq,
-                         long long d, double* y, double* alpha_next, double* part, int nblk) {
-  const bool v2 = (d % 2 == 0);  // 16-byte pairs need every column 16-byte aligned
+                         long long d, double* y, double* alpha_next, double* part, int nblk,
+                         long long ld) {
+  if (ld <= 0) ld = d;
+  // 16-byte pairs need every column (and the row block) 16-byte aligned
+  const bool v2 = (d % 2 == 0) && (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(D) |
+                  reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(y) |
+                  reinterpret_cast<uintptr_t>(cvec) | reinterpret_cast<uintptr_t>(g)) % 16 == 0);
   switch (cg_variant()) {
-    case 1: nblk = launch_cg<4, 2, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk); break;
-    case 2: nblk = launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk); break;
+    case 1: nblk = launch_cg<4, 2, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk); break;
+    case 2: nblk = launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk); break;
     case 3:
-      nblk = v2 ? launch_cg<4, 4, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk)
-                : launch_cg<4, 4, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk);
+      nblk = v2 ? launch_cg<4, 4, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk)
+                : launch_cg<4, 4, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk);
       break;
     case 4:
-      nblk = v2 ? launch_cg<8, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk)
-                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk);
+      nblk = v2 ? launch_cg<8, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk)
+                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk);
       break;
     default:
-      nblk = v2 ? launch_cg<4, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk)
-                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, y, part, nblk);
+      nblk = v2 ? launch_cg<4, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk)
+                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk);
       break;
   }
   c.launches += 1;

@@ -95,14 +95,13 @@ struct Ctx {
   size_t red_cap = 0;
   int launches = 0;          // kernels launched by this library (bench gpu_launches)
   bool strict = false;       // force reference-order kernels everywhere
-  cudaStream_t side = nullptr;       // second stream: projection pass overlapped with G
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int coop_blocks_per_sm = 0;        // cap for cooperative G launches (0 = occupancy max)
-  int sweep_coop_cap = 0;            // the cap used while a D pass runs beside G (PW_COOP_CAP)
-  // PW_SWEEP_OVERLAP=1 runs y = c + D alpha on a side stream beside G.  Off by default: the
-  // tiled G kernel fills the register file (2 x 256 x 128 regs per SM), so nothing co-resides
-  // unless G is capped to 1 CTA/SM (PW_COOP_CAP=1), which slows G more than the overlap saves.
-  bool sweep_overlap = false;
+  // row-sharded serial correction: across ranks through the comm hooks (pw_ctx_set_comm),
+  // or vshards > 1 row shards in one process (tests, PW_ROW_SHARDS)
+  int comm_rank = 0, comm_world = 1, vshards = 1;
+  pw_allreduce_hook allreduce_hook = nullptr;
+  pw_allgather_hook allgather_hook = nullptr;
+  void* comm_user = nullptr;
   pw_fine_hook fine_hook = nullptr;  // slice-sharded fine predictor (multi-GPU), see header
   void* fine_hook_user = nullptr;
 };
@@ -151,9 +150,11 @@ void form_q2(Ctx& c, const double* R, int mr, const int* piv, const double* tau,
 void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv, int r,
                          double* X);
 // y = [g +] c + D alpha (rd cols) and alpha_next = Q^T y (rq cols); nblk <= 0: default grid
+// d rows from the given pointers; D / Q columns ld apart (ld <= 0: ld = d)
 void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                          const double* cvec, const double* alpha, const double* Q, int rq,
-                         long long d, double* y, double* alpha_next, double* part, int nblk = 0);
+                         long long d, double* y, double* alpha_next, double* part, int nblk = 0,
+                         long long ld = 0);
 void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const double* v,
                          double* alpha, double* part);
 

@@ -68,3 +68,57 @@ class ShardedFine:
     def batch(self, states):
         t = torch.as_tensor(states)
         return self(t).cpu().numpy()
+
+
+class _DevVector:
+    """A raw device pointer seen by torch without a copy (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_vector(ptr: int, n: int, device) -> torch.Tensor:
+    return torch.as_tensor(_DevVector(ptr, n), device=device)
+
+
+class RowShardComm:
+    """Collectives of the row-sharded serial correction (include/pitwave_b200.h,
+    pw_ctx_set_comm): an in-place allreduce of the partial alpha (r doubles) and an
+    all-gather of the ranks' row blocks of qn_{i+1}, over a torch.distributed group."""
+
+    def __init__(self, group, device):
+        self.group = group
+        self.device = device
+        self.world = tdist.get_world_size(group)
+        self.rank = tdist.get_rank(group)
+        self.last_error = None
+
+    def allreduce(self, ptr: int, count: int) -> None:
+        tdist.all_reduce(device_vector(ptr, count, self.device), group=self.group)
+
+    def allgather(self, ptr: int, block: int, total: int) -> None:
+        gather_rows(device_vector(ptr, total, self.device), block, self.group)
+
+
+def row_block(total: int, block: int, rank: int):
+    """[lo, hi) of `rank`'s rows for blocks of `block` rows (the last may be short or empty)."""
+    lo = min(total, rank * block)
+    return lo, min(total, lo + block)
+
+
+def gather_rows(full: torch.Tensor, block: int, group=None) -> None:
+    """In-place all-gather of a (total,) vector whose block `rank` is valid on each rank."""
+    world, rank = tdist.get_world_size(group), tdist.get_rank(group)
+    total = full.shape[0]
+    lo, hi = row_block(total, block, rank)
+    mine = torch.zeros(block, dtype=full.dtype, device=full.device)
+    mine[: hi - lo] = full[lo:hi]
+    out = torch.empty(world * block, dtype=full.dtype, device=full.device)
+    if out.device.type == "cuda":
+        tdist.all_gather_into_tensor(out, mine, group=group)
+    else:  # gloo: list form
+        parts = list(out.split(block))
+        tdist.all_gather(parts, mine, group=group)
+        out = torch.cat(parts)
+    full.copy_(out[:total])

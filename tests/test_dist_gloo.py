@@ -73,3 +73,58 @@ def test_sharded_fine_matches_single_process_world2(mode):
     assert sorted(r[0] for r in results) == [0, 1]
     assert all(r[1] for r in results), results   # bitwise-equal endpoints on both ranks
     assert all(r[2] for r in results), results   # identical residual histories
+
+
+def _row_worker(rank, world, port, out_q):
+    """Row-sharded serial correction arithmetic (the per-step work of pw_sweep with
+    pw_ctx_set_comm): each rank combines its row block of D and Q, the partial alphas
+    are allreduced and the rows of qn_{i+1} all-gathered -- over gloo on CPU tensors,
+    against the unsharded recursion."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_02237_b200.dist import gather_rows, row_block
+
+        g = torch.Generator().manual_seed(5)
+        d, r, steps = 1001, 7, 5  # odd d: the last block is short
+        D = torch.randn(d, r, generator=g, dtype=torch.float64)
+        Q = torch.linalg.qr(torch.randn(d, r, generator=g, dtype=torch.float64))[0]
+        G = torch.randn(d, d, generator=g, dtype=torch.float64) / d ** 0.5
+        c = torch.randn(steps, d, generator=g, dtype=torch.float64)
+        q0 = torch.randn(d, generator=g, dtype=torch.float64)
+        # unsharded: q_{i+1} = G q_i + c_i + D alpha_i,  alpha_i = Q^T q_i
+        q, a = q0.clone(), Q.T @ q0
+        for i in range(steps):
+            q = G @ q + c[i] + D @ a
+            a = Q.T @ q
+        block = ((d + world - 1) // world + 1) // 2 * 2
+        lo, hi = row_block(d, block, rank)
+        qs, as_ = q0.clone(), Q.T @ q0
+        for i in range(steps):
+            gq = G @ qs                                   # replicated coarse step
+            y = torch.zeros(d, dtype=torch.float64)
+            y[lo:hi] = gq[lo:hi] + c[i, lo:hi] + D[lo:hi] @ as_
+            part = Q[lo:hi].T @ y[lo:hi]
+            dist.all_reduce(part)                         # partial alphas -> alpha_{i+1}
+            gather_rows(y, block)                         # rows of qn_{i+1} -> every rank
+            qs, as_ = y, part
+        out_q.put((rank, float((qs - q).norm() / q.norm()), float((as_ - a).norm() / a.norm())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_serial_correction_matches_unsharded(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert len(results) == world
+    for _, dq, da in results:
+        assert dq <= 1e-13 and da <= 1e-13

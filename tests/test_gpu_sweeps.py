@@ -229,6 +229,27 @@ def test_c1_kse_lean_mode_matches_reference(monkeypatch):
     assert sub.q.shape == (g["q0"].size, sub.rank)
 
 
+@pytest.mark.parametrize("nsh", [2, 3, 5])
+def test_c1_kse_row_sharded_serial_correction(dev, nsh):
+    """The multi-GPU serial step (row shards of D and Q, partial alphas summed, rows
+    gathered) run as nsh shards in one process: same window as the
+    single-shard loop up to the order of the alpha partial sums."""
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    g = golden("c1_kse.npz")
+    wl, fine, coarse = c1_props()
+    ends1, res1, sub1 = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    dev.set_row_shards(nsh)
+    try:
+        ends, res, sub = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    finally:
+        dev.set_row_shards(1)
+    assert sub.rank == sub1.rank == g["kse_ranks"][-1]
+    assert max(rel(ends[i], ends1[i]) for i in range(wl.n_p)) <= 1e-12
+    assert max(rel(ends[i], g["kse_hist"][-1][i]) for i in range(wl.n_p)) <= 1e-10
+    np.testing.assert_allclose(res, g["kse_res"], rtol=1e-10)
+
+
 def test_c1_original_matches_reference():
     from paper_1510_02237_b200.parareal import parareal_sweep
 
