@@ -900,6 +900,14 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       // would not fit next to the sweep buffers (c4 on one GPU: 5 x 25.8 GB)
       size_t free_b = 0, total_b = 0;
       PW_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      {  // memory the stream-ordered pool holds but does not use is free for our allocations
+        cudaMemPool_t pool;
+        uint64_t reserved = 0, used = 0;
+        PW_CUDA(cudaDeviceGetDefaultMemPool(&pool, c.device));
+        PW_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+        PW_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+        if (reserved > used) free_b += (size_t)(reserved - used);
+      }
       const double col = 8.0 * (double)d;
       const double need = col * std::min<long long>(B->cap, d) * 5.0 + col * n_c * 3.0 +
                           std::max(4.0 * (1ull << 30), 0.06 * (double)total_b);
