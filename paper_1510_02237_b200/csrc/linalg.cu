@@ -333,6 +333,151 @@ __global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
   if (rq > 0) flush_wpart(wpart, rq, part);
 }
 
+// ---------------------------------------------------------------- TMA-fed serial step
+// Same arithmetic as combine_gemv_kernel<., ., true> (row pairs, fixed-order sums), but the
+// D and Q column chunks reach shared memory by 1D bulk copies (cp.async.bulk, the TMA
+// engine): one producer lane per CTA keeps kTmaStages x 8 columns x 512 rows (192 KB) in
+// flight through full/empty mbarrier pairs, and 8 consumer warps only read shared memory.
+// One CTA per SM; tiles of 512 rows, 2 rows (one 16-byte pair) per consumer thread.
+constexpr int kTmaRows = 512;                 // rows per tile
+constexpr int kTmaCols = 8;                   // columns per stage
+constexpr int kTmaStages = 6;                 // ring depth
+constexpr int kTmaConsumers = 256;            // 8 warps
+constexpr int kTmaThreads = kTmaConsumers + 32;
+constexpr size_t kTmaStageBytes = (size_t)kTmaCols * kTmaRows * sizeof(double);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// The chunk schedule both sides walk: per tile, ceil(rd/8) D stages then ceil(rq/8) Q stages.
+__global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
+    const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
+    const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d, long long ld,
+    double* __restrict__ y_out, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* ring = reinterpret_cast<double*>(smraw);                       // stages x 8 x 512
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + kTmaStages * kTmaStageBytes);
+  uint64_t* empty = full + kTmaStages;
+  double* a_s = reinterpret_cast<double*>(empty + kTmaStages);            // rd
+  double* wpart = a_s + rd;                                               // 8 warps x rq
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int k = tid; k < rd; k += blockDim.x) a_s[k] = alpha[k];
+  for (int k = tid; k < kCgWarps * rq; k += blockDim.x) wpart[k] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCgWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long ntiles = (d + kTmaRows - 1) / kTmaRows;
+  const int nsd = (rd + kTmaCols - 1) / kTmaCols, nsq = (rq + kTmaCols - 1) / kTmaCols;
+  if (warp == kCgWarps) {
+    // ---------------- producer: one lane issues every bulk copy
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long row0 = tile * kTmaRows;
+        const uint32_t rows = (uint32_t)min((long long)kTmaRows, d - row0);
+        for (int q = 0; q < nsd + nsq; ++q) {
+          const bool isd = q < nsd;
+          const int k0 = (isd ? q : q - nsd) * kTmaCols;
+          const int ncol = min(kTmaCols, (isd ? rd : rq) - k0);
+          const double* base = (isd ? D : Q) + row0;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_tx(&full[stage], (uint32_t)(ncol * rows * sizeof(double)));
+          double* dst = ring + (size_t)stage * kTmaCols * kTmaRows;
+          for (int c = 0; c < ncol; ++c)
+            bulk_g2s(dst + (size_t)c * kTmaRows, base + (long long)(k0 + c) * ld, rows * sizeof(double),
+                     &full[stage]);
+          if (++stage == kTmaStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers: rows 2*tid, 2*tid+1 of each tile
+    int stage = 0;
+    uint32_t phase = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const long long row0 = tile * kTmaRows;
+      const long long row = row0 + 2 * tid;
+      const bool ok = row < d;  // d even: both rows of the pair or neither
+      double y0 = 0.0, y1 = 0.0;
+      if (ok) {
+        y0 = g ? g[row] + cvec[row] : cvec[row];
+        y1 = g ? g[row + 1] + cvec[row + 1] : cvec[row + 1];
+      }
+      for (int q = 0; q < nsd; ++q) {
+        const int k0 = q * kTmaCols, ncol = min(kTmaCols, rd - k0);
+        mbar_wait(&full[stage], phase);
+        const double* src = ring + (size_t)stage * kTmaCols * kTmaRows + 2 * tid;
+#pragma unroll
+        for (int c = 0; c < kTmaCols; ++c) {
+          if (c < ncol) {
+            const double2 t = *reinterpret_cast<const double2*>(src + (size_t)c * kTmaRows);
+            if (ok) {
+              y0 = fma(t.x, a_s[k0 + c], y0);
+              y1 = fma(t.y, a_s[k0 + c], y1);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kTmaStages) { stage = 0; phase ^= 1; }
+      }
+      if (ok) *reinterpret_cast<double2*>(y_out + row) = make_double2(y0, y1);
+      for (int q = 0; q < nsq; ++q) {
+        const int k0 = q * kTmaCols, ncol = min(kTmaCols, rq - k0);
+        mbar_wait(&full[stage], phase);
+        const double* src = ring + (size_t)stage * kTmaCols * kTmaRows + 2 * tid;
+        double acc[8];
+#pragma unroll
+        for (int c = 0; c < kTmaCols; ++c) {
+          acc[c] = 0.0;
+          if (c < ncol && ok) {
+            const double2 t = *reinterpret_cast<const double2*>(src + (size_t)c * kTmaRows);
+            acc[c] = fma(t.x, y0, t.y * y1);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kTmaStages) { stage = 0; phase ^= 1; }
+        const double v = transpose_reduce8(acc);
+        if (lane < 8 && k0 + lane < rq) wpart[warp * rq + k0 + lane] += v;
+      }
+    }
+  }
+  if (rq > 0) flush_wpart(wpart, rq, part);
+}
+
 __global__ void __launch_bounds__(kCgThreads, 2) project_partial_kernel(
     const double* __restrict__ Q, int r, long long d, const double* __restrict__ v,
     double* __restrict__ part) {
@@ -674,7 +819,30 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
   const bool v2 = (d % 2 == 0) && (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(D) |
                   reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(y) |
                   reinterpret_cast<uintptr_t>(cvec) | reinterpret_cast<uintptr_t>(g)) % 16 == 0);
-  switch (cg_variant()) {
+  const int var = cg_variant();  // 0: TMA kernel when the layout allows it, 6: LSU kernel
+  if ((var == 0 || var == 5) && v2 && d >= kTmaRows) {
+    const long long ntiles = (d + kTmaRows - 1) / kTmaRows;
+    if (nblk <= 0) {
+      const long long per = (ntiles + c.num_sms - 1) / c.num_sms;
+      nblk = (int)((ntiles + per - 1) / per);
+    }
+    const size_t smem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * sizeof(uint64_t) +
+                        sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps);
+    static size_t attr = 0;
+    if (smem > attr) {
+      PW_CUDA(cudaFuncSetAttribute(combine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    combine_tma_kernel<<<nblk, kTmaThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part);
+    c.launches += 1;
+    if (rq > 0) {
+      reduce_parts_kernel<<<(rq + 31) / 32, 256, 0, st>>>(part, nblk, rq, alpha_next);
+      c.launches += 1;
+    }
+    PW_LAUNCH_CHECK();
+    return;
+  }
+  switch (var) {
     case 1: nblk = launch_cg<4, 2, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk); break;
     case 2: nblk = launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk); break;
     case 3:
@@ -715,7 +883,8 @@ void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const doub
 }
 
 size_t combine_part_doubles(long long d, int r) {
-  return (size_t)((d + kCgRows - 1) / kCgRows) * (size_t)std::max(r, 1);  // >= grid x r
+  // >= grid x r for both the 1024-row LSU kernel and the 512-row TMA kernel
+  return (size_t)((d + kTmaRows - 1) / kTmaRows) * (size_t)std::max(r, 1);
 }
 
 }  // namespace pw
