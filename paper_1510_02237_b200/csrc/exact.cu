@@ -421,20 +421,20 @@ struct TbPlanes {
   double* vn;
 };
 
-template <int TM, int K, bool FIX>
+template <int TMX, int TMY, int K, bool FIXX, bool FIXY>
 __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ cu,
                                          double* __restrict__ nu, const double* __restrict__ w,
                                          int tx0, int ty0, int twx_, int twy_, const ExactParams& p,
                                          double sx, double sy, double tau, bool damp) {
-  // TM: largest tile edge (fixes the shared-memory pitch); this tile is twx x twy
-  // (FIX: every tile is TM x TM -- compile-time loop bounds)
-  const int twx = FIX ? TM : twx_, twy = FIX ? TM : twy_;
-  constexpr int H = 3 * K, W = TM + 2 * H, WW = W * W;
+  // TMX x TMY: largest tile (fixes the shared-memory planes); this tile is twx x twy
+  // (FIXX / FIXY: every tile has the full extent -- compile-time loop bounds)
+  const int twx = FIXX ? TMX : twx_, twy = FIXY ? TMY : twy_;
+  constexpr int H = 3 * K, W = TMX + 2 * H, WW = W * (TMY + 2 * H);
   const int nx = p.nx, ny = p.ny, n = nx * ny;
   double* planes = sm;  // u, v, p, un, vn : W x W each
   // ---- stage (u, v, p) with halo H
   {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     constexpr int CX = (W + 31) / 32;
     int gx[CX];
 #pragma unroll
@@ -443,7 +443,7 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
       x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
       gx[k] = x;
     }
-    for (int y = warp; y < twy + 2 * H; y += 8) {
+    for (int y = warp; y < twy + 2 * H; y += nwarp) {
       int gy = ty0 - H + y;
       gy = gy < 0 ? gy + ny : (gy >= ny ? gy - ny : gy);
       const double* row = cu + (size_t)gy * nx;
@@ -515,18 +515,18 @@ __device__ __forceinline__ void tb_block(double* sm, const double* __restrict__ 
   __syncthreads();
 }
 
-template <int TM, int K, int MINB, bool FIX, int ORD>
-__global__ void __launch_bounds__(256, MINB) fefb_tb_coop(double* st, int batch, long long ld,
-                                                    ExactParams p, int nsteps, double tau, int nsub,
-                                                    double* work) {
+template <int TMX, int TMY, int K, int NT, int MINB, bool FIXX, bool FIXY, int ORD>
+__global__ void __launch_bounds__(NT, MINB) fefb_tb_coop(double* st, int batch, long long ld,
+                                                   ExactParams p, int nsteps, double tau, int nsub,
+                                                   double* work, int tiles_x, int tiles_y) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
   const int nx = p.nx, ny = p.ny;
   const int n = nx * ny;
   const double sx = 0.5 / p.dx, sy = 0.5 / p.dy;
   const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
-  // near-equal tiles of at most TM x TM (edges floor(k n / tiles))
-  const int tiles_x = (nx + TM - 1) / TM, tiles_y = (ny + TM - 1) / TM, tiles = tiles_x * tiles_y;
+  // tiles_x x tiles_y near-equal tiles of at most TMX x TMY (edges floor(k n / tiles))
+  const int tiles = tiles_x * tiles_y;
   const long long work_items = (long long)tiles * batch;
   const int stride = gridDim.x * blockDim.x;
   const int first = blockIdx.x * blockDim.x + threadIdx.x;
@@ -556,8 +556,10 @@ __global__ void __launch_bounds__(256, MINB) fefb_tb_coop(double* st, int batch,
         double* sb = st + b * ld;
         const double* cu = from_state ? sb : w + 3 * n;
         double* nu = from_state ? w + 3 * n : sb;
-        if (blk < nblk) tb_block<TM, K, FIX>(sm, cu, nu, w, tx0, ty0, twx, twy, p, sx, sy, tau, damp);
-        else tb_block<TM, 1, FIX>(sm, cu, nu, w, tx0, ty0, twx, twy, p, sx, sy, tau, damp);
+        if (blk < nblk)
+          tb_block<TMX, TMY, K, FIXX, FIXY>(sm, cu, nu, w, tx0, ty0, twx, twy, p, sx, sy, tau, damp);
+        else
+          tb_block<TMX, TMY, 1, FIXX, FIXY>(sm, cu, nu, w, tx0, ty0, twx, twy, p, sx, sy, tau, damp);
       }
       grid.sync();
     }
@@ -575,9 +577,9 @@ __global__ void __launch_bounds__(256, MINB) fefb_tb_coop(double* st, int batch,
   }
 }
 
-template <int TM, int K>
+template <int TMX, int TMY, int K>
 constexpr size_t tb_smem() {
-  return sizeof(double) * 5 * (TM + 6 * K) * (TM + 6 * K);
+  return sizeof(double) * 5 * (TMX + 6 * K) * (TMY + 6 * K);
 }
 
 template <int T>
@@ -641,25 +643,30 @@ static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch
   c.launches += 1;
 }
 
-template <int TM, int K, int MINB, bool FIX, int ORD = 0>
+// tiles_y <= 0: ceil(ny / TMY) (tall tiles: at least one tile row per ~SM budget)
+template <int TMX, int TMY, int K, int NT, int MINB, bool FIXX, bool FIXY, int ORD = 0>
 static void launch_tb(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
-                      int nsteps, double h, int nsub, double* work) {
-  auto kern = fefb_tb_coop<TM, K, MINB, FIX, ORD>;
+                      int nsteps, double h, int nsub, double* work, bool fill_sms = false) {
+  auto kern = fefb_tb_coop<TMX, TMY, K, NT, MINB, FIXX, FIXY, ORD>;
   static int per_sm = -1;
-  constexpr size_t smem = tb_smem<TM, K>();
+  constexpr size_t smem = tb_smem<TMX, TMY, K>();
   if (per_sm < 0) {
     PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     if (per_sm < 1) per_sm = 1;
   }
-  const long long items =
-      (long long)((p.nx + TM - 1) / TM) * ((p.ny + TM - 1) / TM) * batch;
+  int tiles_x = (p.nx + TMX - 1) / TMX, tiles_y = (p.ny + TMY - 1) / TMY;
+  if (fill_sms) {  // as many tile rows as keep every SM busy with one tile (batch 1)
+    const int want = (c.num_sms * per_sm) / std::max(1, tiles_x * batch);
+    tiles_y = std::min(p.ny, std::max(tiles_y, want));
+  }
+  const long long items = (long long)tiles_x * tiles_y * batch;
   const int cap_sm = c.coop_blocks_per_sm > 0 ? std::min(per_sm, c.coop_blocks_per_sm) : per_sm;
   int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * cap_sm));
   double tau = h / nsub;
   ExactParams pp = p;
-  void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work};
-  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(256), args, smem, c.stream));
+  void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work, &tiles_x, &tiles_y};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(NT), args, smem, c.stream));
   c.launches += 1;
 }
 
@@ -677,17 +684,23 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
   if (nsteps <= 0 || batch <= 0) return;
   PW_CHECK((long long)p.nx * p.ny < (1LL << 31), PW_ERR_VALUE, "grid too large");
   if (!c.strict && p.nx % 32 == 0 && p.ny % 32 == 0 && (long long)p.nx * p.ny >= 65536) {
+    const bool o1 = p.order == 1;
     switch (coarse_variant()) {
       case 1: return launch_tiled<32>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      case 2: return launch_tb<32, 1, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      case 3: return launch_tb<44, 2, 1, false>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      case 4: return launch_tb<44, 2, 2, false>(c, p, states, batch, ld, nsteps, h, nsub, work);
-      case 5:
-        if (p.order == 1) return launch_tb<32, 2, 3, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
-        return launch_tb<32, 2, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 2: return launch_tb<32, 32, 1, 256, 2, true, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
+      case 3:  // tall near-equal tiles, one 512-thread CTA per SM
+        if (o1) return launch_tb<32, 60, 2, 512, 1, true, false, 1>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
+        return launch_tb<32, 60, 2, 512, 1, true, false>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
+      case 4:
+        if (o1) return launch_tb<32, 32, 2, 256, 2, true, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
+        return launch_tb<32, 32, 2, 256, 2, true, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
       default:
-        if (p.order == 1) return launch_tb<32, 2, 2, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
-        return launch_tb<32, 2, 2, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
+        // one state (the serial sweep): tall tiles, one per SM (balanced barrier phases);
+        // batches: 32 x 32 tiles, 2 CTAs per SM
+        if (batch == 1 && o1)
+          return launch_tb<32, 60, 2, 512, 1, true, false, 1>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
+        if (o1) return launch_tb<32, 32, 2, 256, 2, true, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
+        return launch_tb<32, 32, 2, 256, 2, true, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
     }
   }
   if (!c.strict && p.nx % 16 == 0 && p.ny % 16 == 0)
