@@ -37,6 +37,10 @@ extern "C" {
 
 #define PW_SCHEME_RK3 0          /* integrators.rk3_step, integrators.py:79-85         */
 #define PW_SCHEME_SPLIT_FE_FB 1  /* integrators.split_fe_fb_step, integrators.py:103-106 */
+#define PW_SCHEME_RK3_SCALAR 2   /* rk3_step on the scalar advection model (physics.py:77-80);
+                                    states are one (ny, nx) field                            */
+#define PW_SCHEME_SPLIT_RK3_FB 3 /* integrators.split_rk3_fb_step, integrators.py:109-120:
+                                    damping per stage from nu_damp (a1/a2 unused)           */
 
 #define PW_MODE_ORIGINAL 0       /* parareal.parareal_sweep, parareal.py:68-97 */
 #define PW_MODE_KSE 1            /* parareal.kse_sweep,      parareal.py:100-138 */
@@ -66,6 +70,7 @@ typedef struct pw_pde_desc {
   double vel_u, vel_v;
   const double* uf; /* host */
   const double* vf; /* host */
+  double nu_damp;   /* PW_SCHEME_SPLIT_RK3_FB: alpha = nu_damp (dx^2, dy^2) / tau per stage */
 } pw_pde_desc;
 
 /* ---- library / context ------------------------------------------------ */

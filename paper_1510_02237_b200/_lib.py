@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(_HERE, "libpitwave_b200.so")
 PW_OK = 0
 SCHEME_RK3 = 0
 SCHEME_SPLIT_FE_FB = 1
+SCHEME_RK3_SCALAR = 2
+SCHEME_SPLIT_RK3_FB = 3
 MODE_ORIGINAL = 0
 MODE_KSE = 1
 
@@ -44,6 +46,7 @@ class PdeDesc(ctypes.Structure):
         ("const_velocity", ctypes.c_int),
         ("vel_u", ctypes.c_double), ("vel_v", ctypes.c_double),
         ("uf", c_dp), ("vf", c_dp),
+        ("nu_damp", ctypes.c_double),
     ]
 
 

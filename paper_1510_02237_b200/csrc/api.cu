@@ -206,7 +206,13 @@ void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long 
   }
   // reference-order kernels, in place on `out`
   copy_cols(c, out, ld, in, ld, d, batch);
-  if (D.scheme == PW_SCHEME_RK3) {
+  if (D.scheme == PW_SCHEME_RK3_SCALAR) {
+    double* w = P->work.ensure(c, pw::scalar_rk3_work_doubles(P->ex, batch));
+    pw::launch_rk3_exact_scalar(c, P->ex, out, batch, ld, nsteps, D.h, w);
+  } else if (D.scheme == PW_SCHEME_SPLIT_RK3_FB) {
+    double* w = P->work.ensure(c, pw::split_rk3_fb_work_doubles(P->ex, batch));
+    pw::launch_split_rk3_fb(c, P->ex, D.nu_damp, out, batch, ld, nsteps, D.h, D.n_sound, w);
+  } else if (D.scheme == PW_SCHEME_RK3) {
     double* w = P->work.ensure(c, pw::rk3_exact_work_doubles(P->ex, batch));
     pw::launch_rk3_exact(c, P->ex, out, batch, ld, nsteps, D.h, w);
   } else {
@@ -662,20 +668,24 @@ int pw_prop_create_pde(pw_ctx* ctx, const pw_pde_desc* desc, pw_prop** out) {
   return guarded([&] {
     PW_CHECK(ctx && desc && out, PW_ERR_VALUE, "NULL argument");
     const pw_pde_desc& D = *desc;
-    PW_CHECK(D.scheme == PW_SCHEME_RK3 || D.scheme == PW_SCHEME_SPLIT_FE_FB, PW_ERR_VALUE,
-             "scheme must be rk3 or split_fe_fb");
+    PW_CHECK(D.scheme == PW_SCHEME_RK3 || D.scheme == PW_SCHEME_SPLIT_FE_FB ||
+                 D.scheme == PW_SCHEME_RK3_SCALAR || D.scheme == PW_SCHEME_SPLIT_RK3_FB,
+             PW_ERR_VALUE, "scheme must be rk3, split_fe_fb, rk3_scalar or split_rk3_fb");
+    const bool scalar = D.scheme == PW_SCHEME_RK3_SCALAR;
     PW_CHECK(D.nx >= 8 && D.ny >= 8, PW_ERR_VALUE, "grid too small (need at least 8 cells per direction)");
     PW_CHECK(D.order >= 1 && D.order <= 6, PW_ERR_VALUE, "flux order must be in 1..6");
     PW_CHECK(D.nsteps >= 0, PW_ERR_VALUE, "nsteps must be non-negative");
     PW_CHECK(D.scheme == PW_SCHEME_RK3 || D.n_sound >= 1, PW_ERR_VALUE, "n_sound must be at least 1");
-    PW_CHECK(D.h > 0 && D.dx > 0 && D.dy > 0 && D.cs > 0, PW_ERR_VALUE, "non-positive step/spacing/sound speed");
+    PW_CHECK(D.h > 0 && D.dx > 0 && D.dy > 0 && (scalar || D.cs > 0), PW_ERR_VALUE,
+             "non-positive step/spacing/sound speed");
+    PW_CHECK(D.scheme != PW_SCHEME_SPLIT_RK3_FB || D.nu_damp >= 0, PW_ERR_VALUE, "negative nu_damp");
     Ctx& c = ctx->c;
     auto P = std::make_unique<pw_prop>();
     P->ctx = ctx;
     P->kind = 0;
     P->desc = D;
     P->desc.uf = P->desc.vf = nullptr;
-    P->dim = 3LL * D.nx * D.ny;
+    P->dim = (scalar ? 1LL : 3LL) * D.nx * D.ny;
     const size_t n = (size_t)D.nx * D.ny;
     std::vector<double> hu(n), hv(n);
     if (D.const_velocity) {

@@ -21,6 +21,9 @@
 #include <cooperative_groups.h>
 #include <cuda_pipeline.h>
 
+#include <cmath>
+#include <utility>
+
 #include "pw_internal.h"
 
 namespace cg = cooperative_groups;
@@ -120,6 +123,35 @@ __global__ void rk3_stage_exact(const double* q, const double* __restrict__ s, d
     ob[cell] = qu + du * beta;
     ob[n + cell] = qv + dv * beta;
     ob[2 * n + cell] = qp + dp * beta;
+  }
+}
+
+// scalar advection RK3 stage (physics.advection_rhs, physics.py:77-80): out = q + adv(s) * beta
+__global__ void rk3_stage_exact_scalar(const double* q, const double* __restrict__ s, double* out,
+                                       long long ldq, long long lds, long long ldo, ExactParams p,
+                                       double beta) {
+  const int n = p.nx * p.ny;
+  const long long b = blockIdx.y;
+  for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < n; cell += gridDim.x * blockDim.x) {
+    const int j = cell / p.nx, i = cell - j * p.nx;
+    const double f = adv_at(p, s + b * lds, j, i);
+    out[b * ldo + cell] = q[b * ldq + cell] + f * beta;
+  }
+}
+
+// advective tendencies of the 3 acoustic fields of `cur` (physics.advective_tendencies,
+// physics.py:67-74) into work planes 0..2 of each state (split RK3-FB stages)
+__global__ void adv3_exact(const double* __restrict__ cur, long long ld, double* __restrict__ work,
+                           ExactParams p) {
+  const int n = p.nx * p.ny;
+  const long long b = blockIdx.y;
+  const double* q = cur + b * ld;
+  double* w = work + b * 6 * (long long)n;
+  for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < n; cell += gridDim.x * blockDim.x) {
+    const int j = cell / p.nx, i = cell - j * p.nx;
+    w[cell] = adv_at(p, q, j, i);
+    w[n + cell] = adv_at(p, q + n, j, i);
+    w[2 * n + cell] = adv_at(p, q + 2 * n, j, i);
   }
 }
 
@@ -238,7 +270,8 @@ __device__ __forceinline__ void fb_cell(const A& a, const ExactParams& p, double
 }
 
 __global__ void __launch_bounds__(128) fefb_coop(double* st, int batch, long long ld, ExactParams p,
-                                                 int nsteps, double tau, int nsub, double* work) {
+                                                 int nsteps, double tau, int nsub, double* work,
+                                                 int adv_given) {
   cg::grid_group grid = cg::this_grid();
   const int n = p.nx * p.ny;
   const double sx = 0.5 / p.dx, sy = 0.5 / p.dy, cs = p.cs;
@@ -246,7 +279,9 @@ __global__ void __launch_bounds__(128) fefb_coop(double* st, int batch, long lon
   const int stride = gridDim.x * blockDim.x;
   const int first = blockIdx.x * blockDim.x + threadIdx.x;
   for (int step = 0; step < nsteps; ++step) {
-    // frozen slow tendency A(q) (physics.advective_tendencies, physics.py:67-74)
+    // frozen slow tendency A(q) (physics.advective_tendencies, physics.py:67-74); split
+    // RK3-FB stages pass it precomputed from another state (adv_given)
+    if (!adv_given)
     for (long long b = 0; b < batch; ++b)
     for (int cell = first; cell < n; cell += stride) {
       const int j = cell / p.nx, i = cell - j * p.nx;
@@ -705,6 +740,12 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
   }
   if (!c.strict && p.nx % 16 == 0 && p.ny % 16 == 0)
     return launch_tiled<16>(c, p, states, batch, ld, nsteps, h, nsub, work);
+  launch_fefb_coop(c, p, states, batch, ld, nsteps, h / nsub, nsub, work, 0);
+}
+
+// per-cell cooperative FE-FB: nsteps x (A phase unless adv_given, nsub substeps of tau)
+void launch_fefb_coop(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                      int nsteps, double tau, int nsub, double* work, int adv_given) {
   static int max_per_sm = -1;
   if (max_per_sm < 0) {
     PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, fefb_coop, kCoopThreads, 0));
@@ -714,12 +755,78 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
   long long want = (total + kCoopThreads - 1) / kCoopThreads;
   long long cap = (long long)c.num_sms * max_per_sm;
   int blocks = (int)std::max<long long>(1, std::min(want, cap));
-  double tau = h / nsub;
   ExactParams pp = p;
-  void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work};
+  void* args[] = {&states, &batch, &ld, &pp, &nsteps, &tau, &nsub, &work, &adv_given};
   PW_CUDA(cudaLaunchCooperativeKernel((void*)fefb_coop, dim3(blocks), dim3(kCoopThreads), args, 0,
                                       c.stream));
   c.launches += 1;
+}
+
+size_t scalar_rk3_work_doubles(const ExactParams& p, int batch) {
+  return (size_t)2 * p.nx * p.ny * (size_t)batch;
+}
+
+void launch_rk3_exact_scalar(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                             int nsteps, double h, double* work) {
+  const long long n = (long long)p.nx * p.ny;
+  int bx = (int)std::min<long long>((n + kThreads - 1) / kThreads, (long long)c.num_sms * 16);
+  if (bx < 1) bx = 1;
+  PW_CHECK(batch <= 65535, PW_ERR_VALUE, "batch too large for one launch");
+  const dim3 blocks(bx, batch);
+  double* s1 = work;
+  double* s2 = work + n * batch;
+  const double h3 = h / 3.0, h2 = h / 2.0;
+  for (int s = 0; s < nsteps; ++s) {
+    rk3_stage_exact_scalar<<<blocks, kThreads, 0, c.stream>>>(states, states, s1, ld, ld, n, p, h3);
+    rk3_stage_exact_scalar<<<blocks, kThreads, 0, c.stream>>>(states, s1, s2, ld, n, n, p, h2);
+    rk3_stage_exact_scalar<<<blocks, kThreads, 0, c.stream>>>(states, s2, states, ld, n, ld, p, h);
+    c.launches += 3;
+  }
+  PW_LAUNCH_CHECK();
+}
+
+size_t split_rk3_fb_work_doubles(const ExactParams& p, int batch) {
+  return (size_t)(6 + 3 + 3) * p.nx * p.ny * (size_t)batch;  // FB work, stage start copy, cur
+}
+
+// split_rk3_fb_step (integrators.py:109-120): three stages; stage k takes the advective
+// tendency of the latest stage result and restarts the FB integration from the step-start
+// state over frac*dt with ceil(n_sound*frac) substeps; damping from the stage's tau.
+void launch_split_rk3_fb(Ctx& c, const ExactParams& p, double nu, double* states, int batch,
+                         long long ld, int nsteps, double dt, int n_sound, double* work) {
+  const long long n = (long long)p.nx * p.ny, n3 = 3 * n;
+  double* fbw = work;                      // 6 planes per state (A + ping-pong)
+  double* start = work + 6 * n * batch;    // stage integration buffer (d x batch, ld n3)
+  double* cur = start + n3 * batch;        // latest stage result (ld n3)
+  int bx = (int)std::min<long long>((n + kThreads - 1) / kThreads, (long long)c.num_sms * 16);
+  if (bx < 1) bx = 1;
+  PW_CHECK(batch <= 65535, PW_ERR_VALUE, "batch too large for one launch");
+  const double fracs[3] = {1.0 / 3.0, 0.5, 1.0};
+  for (int s = 0; s < nsteps; ++s) {
+    for (int st = 0; st < 3; ++st) {
+      const double frac = fracs[st];
+      const int nsub = std::max(1, (int)std::ceil(n_sound * frac));
+      const double tau = frac * dt / nsub;
+      ExactParams q = p;
+      if (nu > 0.0) {
+        q.a1 = nu * p.dx * p.dx / tau;
+        q.a2 = nu * p.dy * p.dy / tau;
+      } else {
+        q.a1 = q.a2 = 0.0;
+      }
+      // A(latest stage) -> fbw planes 0..2
+      adv3_exact<<<dim3(bx, batch), kThreads, 0, c.stream>>>(st == 0 ? states : cur, st == 0 ? ld : n3, fbw, q);
+      c.launches += 1;
+      // integrate from the step-start state
+      PW_CUDA(cudaMemcpy2DAsync(start, n3 * sizeof(double), states, ld * sizeof(double), n3 * sizeof(double),
+                                batch, cudaMemcpyDeviceToDevice, c.stream));
+      launch_fefb_coop(c, q, start, batch, n3, 1, tau, nsub, fbw, 1);
+      std::swap(start, cur);
+    }
+    PW_CUDA(cudaMemcpy2DAsync(states, ld * sizeof(double), cur, n3 * sizeof(double), n3 * sizeof(double),
+                              batch, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  PW_LAUNCH_CHECK();
 }
 
 }  // namespace pw

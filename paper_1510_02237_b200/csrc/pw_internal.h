@@ -113,6 +113,17 @@ void launch_rk3_exact(Ctx& c, const ExactParams& p, double* states, int batch, l
 void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                        int nsteps, double h, int nsub, double* work);
 size_t rk3_exact_work_doubles(const ExactParams& p, int batch);
+// per-cell cooperative FE-FB (adv_given: A already in the work planes 0..2)
+void launch_fefb_coop(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                      int nsteps, double tau, int nsub, double* work, int adv_given);
+// scalar advection RK3 (one field per state), reference order
+size_t scalar_rk3_work_doubles(const ExactParams& p, int batch);
+void launch_rk3_exact_scalar(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
+                             int nsteps, double h, double* work);
+// split RK3-FB, reference order; damping per stage from nu
+size_t split_rk3_fb_work_doubles(const ExactParams& p, int batch);
+void launch_split_rk3_fb(Ctx& c, const ExactParams& p, double nu, double* states, int batch,
+                         long long ld, int nsteps, double dt, int n_sound, double* work);
 size_t fefb_exact_work_doubles(const ExactParams& p, int batch);
 
 // fine_fused.cu

@@ -152,11 +152,6 @@ class SlicePropagator(DevicePropagator):
     def __init__(self, spec: PropagatorSpec, span: float | None = None, nsteps: int | None = None,
                  h: float | None = None, device=None):
         super().__init__(device)
-        if spec.model.kind != ACOUSTIC:
-            raise NotImplementedError("the B200 kernels implement the acoustic-advection model "
-                                      "(scalar advection is SURVEY.md row f2, not built yet)")
-        if spec.scheme == SPLIT_RK3_FB:
-            raise NotImplementedError("split_rk3_fb is out of scope (SURVEY.md row f3)")
         self.spec = spec
         self.h = spec.dt if h is None else float(h)
         if nsteps is None:
@@ -164,18 +159,23 @@ class SlicePropagator(DevicePropagator):
         self.nsteps = int(nsteps)
         g = spec.grid
         self.grid = g
-        self.dim = 3 * g.nx * g.ny
         model = spec.model
-        if spec.scheme == RK3:
+        scalar = model.kind != ACOUSTIC
+        self.dim = (1 if scalar else 3) * g.nx * g.ny
+        a1 = a2 = 0.0
+        if scalar:                   # advection_rhs (physics.py:77-80): no acoustics, no damping
+            scheme = _lib.SCHEME_RK3_SCALAR
+        elif spec.scheme == RK3:
             if model.nu_damp > 0:   # physics._alphas: tau = model.damping_timescale
                 a1, a2 = damping_coefficients(model.nu_damp, g.dx, g.dy, model.damping_timescale)
-            else:
-                a1 = a2 = 0.0
             scheme = _lib.SCHEME_RK3
-        else:                        # _fb_integrate: tau = dt / n_sound
+        elif spec.scheme == SPLIT_FE_FB:   # _fb_integrate: tau = dt / n_sound
             tau = self.h / spec.n_sound
-            a1, a2 = damping_coefficients(model.nu_damp, g.dx, g.dy, tau) if model.nu_damp > 0 else (0.0, 0.0)
+            if model.nu_damp > 0:
+                a1, a2 = damping_coefficients(model.nu_damp, g.dx, g.dy, tau)
             scheme = _lib.SCHEME_SPLIT_FE_FB
+        else:                        # split_rk3_fb: the device derives each stage's damping
+            scheme = _lib.SCHEME_SPLIT_RK3_FB
         ux, vy = face_normal_velocities(model.vel, g)
         self._uf = np.ascontiguousarray(ux, dtype=np.float64)
         self._vf = np.ascontiguousarray(vy, dtype=np.float64)
@@ -183,7 +183,8 @@ class SlicePropagator(DevicePropagator):
             scheme=scheme, nx=g.nx, ny=g.ny, dx=g.dx, dy=g.dy, cs=float(model.sound_speed),
             order=int(model.advective_flux_order), a1=float(a1), a2=float(a2), h=self.h,
             n_sound=int(spec.n_sound), nsteps=self.nsteps, const_velocity=0, vel_u=0.0, vel_v=0.0,
-            uf=self._uf.ctypes.data_as(_lib.c_dp), vf=self._vf.ctypes.data_as(_lib.c_dp))
+            uf=self._uf.ctypes.data_as(_lib.c_dp), vf=self._vf.ctypes.data_as(_lib.c_dp),
+            nu_damp=float(model.nu_damp))
         h = _lib.c_vp()
         _lib.check(self.ctx.lib.pw_prop_create_pde(self.ctx.handle, ctypes.byref(desc), ctypes.byref(h)))
         self.handle = h
@@ -226,6 +227,14 @@ def rk3_step(state: State, spec: PropagatorSpec, h: float) -> State:
     if spec.scheme != RK3:
         spec = PropagatorSpec(RK3, spec.model, spec.grid, spec.cfl, spec.n_sound)
     prop = SlicePropagator(spec, nsteps=1, h=h)
+    return State.unflatten(state.grid, prop(state.flatten()), state.kind)
+
+
+def split_rk3_fb_step(state: State, spec: PropagatorSpec, dt: float) -> State:
+    """One split RK3-FB step of size dt (reference integrators.py:109-120)."""
+    if spec.scheme != SPLIT_RK3_FB:
+        spec = PropagatorSpec(SPLIT_RK3_FB, spec.model, spec.grid, spec.cfl, spec.n_sound)
+    prop = SlicePropagator(spec, nsteps=1, h=dt)
     return State.unflatten(state.grid, prop(state.flatten()), state.kind)
 
 
