@@ -176,6 +176,14 @@ int pw_copy(pw_ctx* ctx, void* dst, const void* src, long long nbytes);
 int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long dim,
                 double* out_host);
 
+/* The sweep's fused serial-step pass on caller buffers (device pointers; test and
+ * diagnostic entry):  y = [g +] c + D alpha  (rd columns of D) and
+ * alpha_next = Q^T y (rq columns of Q); D and Q are column-major with leading
+ * dimension ld >= d; g may be NULL; rd or rq may be 0. */
+int pw_serial_step(pw_ctx* ctx, const double* g, const double* D, int rd, const double* c,
+                   const double* alpha, const double* Q, int rq, long long d, long long ld,
+                   double* y, double* alpha_next);
+
 /* fp64 pipe peak (TFLOP/s) from a DFMA-throughput probe kernel: the fp64
  * half of the roofline; no reference counterpart. */
 int pw_probe_fp64_peak(pw_ctx* ctx, int iters, double* tflops);

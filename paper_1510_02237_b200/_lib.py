@@ -88,6 +88,8 @@ SIGNATURES = [
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
     ("pw_probe_fp64_peak", ctypes.c_int, [c_vp, ctypes.c_int, c_dp]),
+    ("pw_serial_step", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int,
+                                      ctypes.c_longlong, ctypes.c_longlong, c_vp, c_vp]),
 ]
 
 _lib = None

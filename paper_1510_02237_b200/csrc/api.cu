@@ -630,6 +630,21 @@ int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards) {
   });
 }
 
+int pw_serial_step(pw_ctx* ctx, const double* g, const double* D, int rd, const double* cv,
+                   const double* alpha, const double* Q, int rq, long long d, long long ld,
+                   double* y, double* alpha_next) {
+  return guarded([&] {
+    PW_CHECK(ctx && cv && y && d >= 1 && ld >= d && rd >= 0 && rq >= 0, PW_ERR_VALUE, "bad argument");
+    PW_CHECK(rd == 0 || (D && alpha), PW_ERR_VALUE, "rd > 0 needs D and alpha");
+    PW_CHECK(rq == 0 || (Q && alpha_next), PW_ERR_VALUE, "rq > 0 needs Q and alpha_next");
+    Ctx& c = ctx->c;
+    DBuf part;
+    double* pp = part.ensure(c, pw::combine_part_doubles(d, std::max(rq, 1)));
+    pw::launch_combine_gemv(c, c.stream, g, D, rd, cv, alpha, Q, rq, d, y, alpha_next, pp, 0, ld);
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
 int pw_probe_fp64_peak(pw_ctx* ctx, int iters, double* tflops) {
   return guarded([&] {
     PW_CHECK(ctx && tflops && iters > 0, PW_ERR_VALUE, "bad argument");

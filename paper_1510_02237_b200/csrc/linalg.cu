@@ -379,18 +379,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
     const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
     const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d, long long ld,
-    double* __restrict__ y_out, double* __restrict__ part) {
+    double* __restrict__ y_out, double* __restrict__ part, int nst) {
+  // nst ring stages (<= kTmaStages: fewer when rd + 8 rq doubles of bookkeeping must fit too)
   extern __shared__ __align__(128) unsigned char smraw[];
-  double* ring = reinterpret_cast<double*>(smraw);                       // stages x 8 x 512
-  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + kTmaStages * kTmaStageBytes);
-  uint64_t* empty = full + kTmaStages;
-  double* a_s = reinterpret_cast<double*>(empty + kTmaStages);            // rd
+  double* ring = reinterpret_cast<double*>(smraw);                       // nst x 8 x 512
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + nst * kTmaStageBytes);
+  uint64_t* empty = full + nst;
+  double* a_s = reinterpret_cast<double*>(empty + nst);                   // rd
   double* wpart = a_s + rd;                                               // 8 warps x rq
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int k = tid; k < rd; k += blockDim.x) a_s[k] = alpha[k];
   for (int k = tid; k < kCgWarps * rq; k += blockDim.x) wpart[k] = 0.0;
   if (tid == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCgWarps);
     }
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
           for (int c = 0; c < ncol; ++c)
             bulk_g2s(dst + (size_t)c * kTmaRows, base + (long long)(k0 + c) * ld, rows * sizeof(double),
                      &full[stage]);
-          if (++stage == kTmaStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == kTmaStages) { stage = 0; phase ^= 1; }
+        if (++stage == nst) { stage = 0; phase ^= 1; }
       }
       if (ok) *reinterpret_cast<double2*>(y_out + row) = make_double2(y0, y1);
       for (int q = 0; q < nsq; ++q) {
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == kTmaStages) { stage = 0; phase ^= 1; }
+        if (++stage == nst) { stage = 0; phase ^= 1; }
         const double v = transpose_reduce8(acc);
         if (lane < 8 && k0 + lane < rq) wpart[warp * rq + k0 + lane] += v;
       }
@@ -820,20 +821,24 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
                   reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(y) |
                   reinterpret_cast<uintptr_t>(cvec) | reinterpret_cast<uintptr_t>(g)) % 16 == 0);
   const int var = cg_variant();  // 0: TMA kernel when the layout allows it, 6: LSU kernel
-  if ((var == 0 || var == 5) && v2 && d >= kTmaRows) {
+  const size_t tma_extra = 2 * kTmaStages * sizeof(uint64_t) + sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps);
+  const int tma_nst = (int)std::min<size_t>(kTmaStages, (227u * 1024 - tma_extra) / kTmaStageBytes);
+  if ((var == 0 || var == 5) && v2 && d >= kTmaRows && tma_extra < 227u * 1024 && tma_nst >= 2) {
     const long long ntiles = (d + kTmaRows - 1) / kTmaRows;
     if (nblk <= 0) {
       const long long per = (ntiles + c.num_sms - 1) / c.num_sms;
       nblk = (int)((ntiles + per - 1) / per);
     }
-    const size_t smem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * sizeof(uint64_t) +
+    const size_t smem = tma_nst * kTmaStageBytes + 2 * tma_nst * sizeof(uint64_t) +
                         sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps);
-    static size_t attr = 0;
-    if (smem > attr) {
-      PW_CUDA(cudaFuncSetAttribute(combine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
+    static bool attr = false;
+    if (!attr) {
+      PW_CUDA(cudaFuncSetAttribute(combine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+      attr = true;
     }
-    combine_tma_kernel<<<nblk, kTmaThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part);
+    combine_tma_kernel<<<nblk, kTmaThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part,
+                                                        tma_nst);
     c.launches += 1;
     if (rq > 0) {
       reduce_parts_kernel<<<(rq + 31) / 32, 256, 0, st>>>(part, nblk, rq, alpha_next);

@@ -368,6 +368,33 @@ def test_kse_residual_and_ranks_against_oracle_c1_shape_p16():
     np.testing.assert_allclose(res, o_res, rtol=1e-8)
 
 
+@pytest.mark.parametrize("d,ld,r,g_null", [(786432, 786432, 310, False), (200000, 200000, 1024, False),
+                                          (4096, 5000, 600, True), (1001, 1001, 37, False),
+                                          (100000, 100002, 0, False)])
+def test_serial_step_kernel_against_torch(dev, d, ld, r, g_null):
+    """The fused serial-step pass (TMA ring; LSU kernel for odd d / misaligned blocks) on
+    caller buffers: y = g + c + D alpha, alpha' = Q^T y, against torch fp64 GEMV."""
+    from paper_1510_02237_b200 import _lib
+
+    gen = torch.Generator(device="cuda").manual_seed(d + r)
+    rr = max(r, 1)
+    Dm = torch.randn(rr, ld, device="cuda", dtype=torch.float64, generator=gen)  # column k = row k
+    Qm = torch.randn(rr, ld, device="cuda", dtype=torch.float64, generator=gen)
+    g = torch.randn(d, device="cuda", dtype=torch.float64, generator=gen)
+    c = torch.randn(d, device="cuda", dtype=torch.float64, generator=gen)
+    a = torch.randn(rr, device="cuda", dtype=torch.float64, generator=gen)
+    y = torch.empty(d, device="cuda", dtype=torch.float64)
+    an = torch.zeros(rr, device="cuda", dtype=torch.float64)
+    _lib.check(dev.lib.pw_serial_step(dev.handle, None if g_null else _lib.ptr(g), _lib.ptr(Dm), r,
+                                      _lib.ptr(c), _lib.ptr(a), _lib.ptr(Qm), r, d, ld, _lib.ptr(y),
+                                      _lib.ptr(an)))
+    want_y = (c if g_null else g + c) + (Dm[:r, :d].T @ a[:r] if r else 0.0)
+    assert torch.linalg.norm(y - want_y) <= 1e-13 * torch.linalg.norm(want_y)
+    if r:
+        want_a = Qm[:r, :d] @ want_y
+        assert torch.linalg.norm(an[:r] - want_a) <= 1e-12 * torch.linalg.norm(want_a)
+
+
 def test_sharded_fine_hook_single_rank_group():
     """The multi-GPU fine hook (pw_ctx_set_fine_hook + dist.ShardedFine) on a 1-rank NCCL group."""
     import os
