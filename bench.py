@@ -233,13 +233,27 @@ def parareal_window(name="c3", warm=True, group=None):
         wall = float(t.item())
         n_ranks = torch.distributed.get_world_size(group)
     d = q0.numel()
+    ranks = getattr(sub, "ranks_history", None) or []
+    # roofline per phase: fine 48 B per cell-update; the serial correction
+    # streams D and Q (2 r d 8 B) plus g, c, y (3 d 8 B) per step -- the coarse G it
+    # interleaves with is L2-resident and adds no HBM bytes
+    peak, _ = load_peaks()
+    fine_bytes = 48.0 * wl.n_p * len(res) * fine.nsteps * d / 3
+    serial_bytes = sum(wl.n_p * (2.0 * r * d * 8 + 3.0 * d * 8) for r in ranks)
+    roof = {"peak_gbs": peak,
+            "fine": {"algorithmic_bytes": fine_bytes,
+                     "frac": fine_bytes / tm.fine / 1e9 / peak if tm.fine else None},
+            "coarse_and_correction": {"algorithmic_bytes": serial_bytes,
+                                      "frac": serial_bytes / tm.coarse / 1e9 / peak if tm.coarse else None,
+                                      "note": "HBM bytes of the serial GEMV passes over the whole phase "
+                                              "time (the latency-bound coarse G included)"}}
     return {"workload": f"{name}: {wl.n}^2, P={wl.n_p}, K={wl.n_it} KSE-Parareal window",
             "window_s": wall, "iteration_s": wall / wl.n_it,
             "phases_s": {"coarse_and_correction": tm.coarse, "fine": tm.fine, "qr": tm.qr},
             "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res],
             "fine_cell_updates_per_s": wl.n_p * wl.n_it * fine.nsteps * d / 3 / tm.fine if tm.fine else None,
             "peak_device_gib": torch.cuda.max_memory_allocated() / 2**30,
-            "warm": warm, "n_gpus": n_ranks,
+            "roofline": roof, "warm": warm, "n_gpus": n_ranks,
             "parallelism": "fine sweep slice-sharded over ranks, serial correction replicated"
                            if n_ranks > 1 else "single GPU"}
 
