@@ -726,14 +726,17 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
       case 3:  // tall near-equal tiles, one 512-thread CTA per SM
         if (o1) return launch_tb<32, 60, 2, 512, 1, true, false, 1>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
         return launch_tb<32, 60, 2, 512, 1, true, false>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
+      case 5:  // tall tiles, 3 substeps per barrier
+        if (o1) return launch_tb<32, 60, 3, 512, 1, true, false, 1>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
+        return launch_tb<32, 60, 3, 512, 1, true, false>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
       case 4:
         if (o1) return launch_tb<32, 32, 2, 256, 2, true, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
         return launch_tb<32, 32, 2, 256, 2, true, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
       default:
-        // one state (the serial sweep): tall tiles, one per SM (balanced barrier phases);
-        // batches: 32 x 32 tiles, 2 CTAs per SM
+        // one state (the serial sweep): tall tiles, one per SM (balanced barrier phases),
+        // 3 substeps per grid barrier; batches: 32 x 32 tiles, 2 CTAs per SM, 2 substeps
         if (batch == 1 && o1)
-          return launch_tb<32, 60, 2, 512, 1, true, false, 1>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
+          return launch_tb<32, 60, 3, 512, 1, true, false, 1>(c, p, states, batch, ld, nsteps, h, nsub, work, true);
         if (o1) return launch_tb<32, 32, 2, 256, 2, true, true, 1>(c, p, states, batch, ld, nsteps, h, nsub, work);
         return launch_tb<32, 32, 2, 256, 2, true, true>(c, p, states, batch, ld, nsteps, h, nsub, work);
     }
