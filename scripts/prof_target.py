@@ -39,12 +39,13 @@ elif what == "coarse":
     y = SlicePropagator(c, nsteps=1).apply(x)
     torch.cuda.synchronize()
     print("coarse ok", bool(torch.isfinite(y).all()))
-elif what in ("c3k2", "c3k5"):
-    wl = harness.WORKLOADS["c3"]
+elif what in ("c3k2", "c3k5", "c4k2", "c4k4"):
+    cfgname = "c4" if what.startswith("c4") else "c3"
+    wl = harness.WORKLOADS[cfgname]
     f, c = specs(wl.n)
     fine, coarse = SlicePropagator(f, wl.slice_span), SlicePropagator(c, wl.slice_span)
-    q0 = torch.as_tensor(harness.initial_state("c3")).cuda()
-    k = 2 if what == "c3k2" else 5
+    q0 = torch.as_tensor(harness.initial_state(cfgname)).cuda()
+    k = {"c3k2": 2, "c3k5": 5, "c4k2": 2, "c4k4": 4}[what]
     if os.environ.get("PW_WARM") == "1":
         kse_sweep(q0, fine, coarse, wl.n_p, k, return_device=True)
         torch.cuda.synchronize()

@@ -33,7 +33,7 @@ from paper_1510_02237_b200 import harness  # noqa: E402  (seeded generators only
 N_SAMPLE = 512
 
 
-def main(n_it=1, name="c4"):
+def main(n_it=1, name="c4", suffix=""):
     wl = harness.WORKLOADS[name]
     fine, coarse = slice_closures(wl)
     q0 = harness.initial_state(name)
@@ -68,11 +68,14 @@ def main(n_it=1, name="c4"):
     finally:
         ref_sub.Subspace.update = orig_update
         ref_par.iteration_residual = orig_res
-    np.savez_compressed(os.path.join(HERE, f"{name}_reference.npz"), res=np.array(res), ranks=np.array(ranks),
+    np.savez_compressed(os.path.join(HERE, f"{name}_reference{suffix}.npz"), res=np.array(res), ranks=np.array(ranks),
                         norms=np.array(norms), samples=np.array(samples), idx=idx,
                         seconds=time.time() - t0, threads=os.cpu_count())
     print(f"done in {time.time() - t0:.0f} s: residuals {res}, ranks {ranks}")
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 1, sys.argv[2] if len(sys.argv) > 2 else "c4")
+    # a third argument names a variant file, e.g. "_numpy" for a PITWAVE_KERNELS=numpy run
+    # (the reference's own backend-to-backend noise floor)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 1, sys.argv[2] if len(sys.argv) > 2 else "c4",
+         sys.argv[3] if len(sys.argv) > 3 else "")
