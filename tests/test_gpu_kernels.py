@@ -99,7 +99,7 @@ def test_fused_fine_matches_oracle(dev, order, U, V):
         assert rel(got[b], want[b]) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [8, 16, 32, 96, 128])
+@pytest.mark.parametrize("n", [8, 16, 32, 96, 128, 1024])
 def test_fused_fine_small_and_odd_tilings(dev, n):
     from paper_1510_02237_b200.integrators import SlicePropagator
 
@@ -172,13 +172,14 @@ def test_propagate_api_and_composition_bitwise(dev):
         propagate(fspec, st, 0.0, 2.5 * h)
 
 
-@pytest.mark.parametrize("n", [256, 512])
-def test_tiled_coarse_bitwise_with_global_variant(dev, n):
-    """Shared-memory tiled FE-FB (T=32) == per-cell global variant (strict mode), bitwise."""
+@pytest.mark.parametrize("n,batch", [(256, 1), (256, 2), (512, 1), (512, 2), (1024, 1), (96, 1)])
+def test_tiled_coarse_bitwise_with_global_variant(dev, n, batch):
+    """Temporal-blocked FE-FB (single state: tall tiles, 3 substeps per barrier; batches:
+    32^2 tiles, 2 substeps) == per-cell global variant (strict mode), bitwise."""
     from paper_1510_02237_b200.integrators import SlicePropagator
 
     _, cspec = make_specs(n)
-    q0 = torch.as_tensor(harness.fine_batch_states(n=n, batch=2, seed=13)).cuda()
+    q0 = torch.as_tensor(harness.fine_batch_states(n=n, batch=batch, seed=13)).cuda()
     tiled = SlicePropagator(cspec, nsteps=2).apply(q0)
     dev.set_strict(True)
     try:

@@ -57,6 +57,9 @@ def check_window(name, tol_per_iteration):
         d_norm = np.max(np.abs(norms - want_n) / want_n)
         d_samp = np.max(np.linalg.norm(samp - want_s, axis=1) / np.linalg.norm(want_s, axis=1))
         worst.append(max(d_norm, d_samp))
+        d_res = abs(res[-1] - g["res"][k - 1]) / abs(g["res"][k - 1])
+        print(f"{name} iteration {k}: rank {sub.rank} (ref {g['ranks'][k - 1]}), state deviation "
+              f"{worst[-1]:.3e}, residual deviation {d_res:.3e}", flush=True)
         assert sub.rank == g["ranks"][k - 1], (k, sub.rank, g["ranks"][k - 1])
         np.testing.assert_allclose(res, g["res"][:k], rtol=max(1e-10, tol_per_iteration[k - 1]))
         assert worst[-1] <= tol_per_iteration[k - 1], (k, worst[-1])
