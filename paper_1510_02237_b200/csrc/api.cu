@@ -356,6 +356,13 @@ static void panel_to_wy(pw_basis* B, int col0, int k) {
   gemm(c, true, false, m, k, d - col0, 1.0, B->W.p + col0, d, B->W.p + (size_t)col0 * d + col0, d, 0.0,
        G, m);
   pw::launch_larft_cols(c, B->T.p, B->cap, G, B->tau1.p, col0, k);
+  if (col0 > 0) {  // T[0:col0, new] = -T_old (G[0:col0, :] T_new)
+    double* X2 = B->wy2.ensure(c, capc * capc);
+    double* Tn = B->T.p + (size_t)col0 * capc + col0;
+    gemm(c, false, false, col0, k, k, 1.0, G, m, Tn, B->cap, 0.0, X2, col0);
+    gemm(c, false, false, col0, k, col0, -1.0, B->T.p, B->cap, X2, col0, 0.0, B->T.p + (size_t)col0 * capc,
+         B->cap);
+  }
   mark("larft");
 }
 

@@ -611,10 +611,11 @@ __global__ void make_unit_lower_kernel(double* __restrict__ A, long long ld, int
   }
 }
 
-// Compact-WY T for reflector columns col0..col0+p-1 given G = V^T V_new (m x p, ld m,
-// m = col0 + p) and tau: the dlarft recurrence over ALL reflectors,
-//   T[i, i] = tau_i,  T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i],
-// one CTA, columns in order (each depends on the previous ones); T upper, ld ldt.
+// Compact-WY T block of reflector columns col0..col0+p-1 given G = V^T V_new (m x p, ld m,
+// m = col0 + p) and tau: the dlarft recurrence restricted to the new block,
+//   T[i, i] = tau_i,  T[col0:i, i] = -tau_i T[col0:i, col0:i] G[col0:i, i],
+// one CTA, columns in order (each depends on the previous ones); T upper, ld ldt.  The
+// coupling block T[0:col0, new] = -T_old (V_old^T V_new) T_new is two GEMMs (api.cu).
 __global__ void __launch_bounds__(1024) larft_cols_kernel(double* __restrict__ T, int ldt,
                                                           const double* __restrict__ G,
                                                           const double* __restrict__ tau, int col0,
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(1024) larft_cols_kernel(double* __restrict__ T
     const double ti = tau[i];
     const double* g = G + (size_t)(i - col0) * m;
     // one warp per row j, lanes split the l sum (independent L2 loads, then a warp reduction)
-    for (int j = warp; j < i; j += nwarp) {
+    for (int j = col0 + warp; j < i; j += nwarp) {
       double w = 0.0;
       for (int l = j + lane; l < i; l += 32) w = fma(T[(size_t)l * ldt + j], g[l], w);
 #pragma unroll
