@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(kQ2Warps * 32) form_q2_kernel(const double* A,
 // X[piv[k], c] = (R11^-1)[k, c]; R11[i][k] = A[i, piv[k]] (i <= k < r).
 // Column-oriented back substitution, one warp per column, b staged in smem.
 __global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A, int mr, int m,
-                                                                 const int* piv, int r, double* X) {
+                                                                 const int* piv, int r, double* X,
+                                                                 int scatter) {
   extern __shared__ double bs[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * kQ2Warps + warp;
@@ -184,7 +185,20 @@ __global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A,
     if (lane == 0) b[l] = yl;
     __syncwarp();
   }
-  for (int k = lane; k <= c; k += 32) X[(size_t)c * m + piv[k]] = b[k];
+  // scatter: X[piv[k], c] (m x r); else the plain upper-triangular R11^-1 (r x r)
+  for (int k = lane; k <= c; k += 32) X[scatter ? (size_t)c * m + piv[k] : (size_t)c * r + k] = b[k];
+}
+
+// Y[:, k] = M[:, piv[k]], k < r (d rows, column-major, ld d)
+__global__ void gather_cols_kernel(double* __restrict__ Y, const double* __restrict__ M, long long d,
+                                   const int* __restrict__ piv, int r) {
+  const long long total = d * r;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / d);
+    const long long row = idx - (long long)k * d;
+    Y[idx] = M[(long long)piv[k] * d + row];
+  }
 }
 
 // ---------------------------------------------------------------- fused serial step
@@ -773,7 +787,30 @@ void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv,
     PW_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, m, piv, r, X);
+  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, m, piv, r, X, 1);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void tri_inverse(Ctx& c, const double* R, int mr, const int* piv, int r, double* Rinv) {
+  if (r <= 0) return;
+  PW_CUDA(cudaMemsetAsync(Rinv, 0, sizeof(double) * (size_t)r * r, c.stream));
+  size_t smem = sizeof(double) * mr * kQ2Warps;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PW_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, mr, piv, r, Rinv, 0);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+void launch_gather_cols(Ctx& c, double* Y, const double* M, long long d, const int* piv, int r) {
+  if (r <= 0) return;
+  const long long total = d * r;
+  int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c.num_sms * 16));
+  gather_cols_kernel<<<blocks, 256, 0, c.stream>>>(Y, M, d, piv, r);
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }
