@@ -485,9 +485,9 @@ void basis_refactor(pw_basis* B, int m_old) {
     gemm(c, false, false, d, r, k, -1.0, B->W.p, d, X2, k, 1.0, Q, d);
   }
   clk.mark("Q=Q1Q2");
-  // Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep).  A gather of the r
-  // pivot columns + in-place TRMM (d r^2 flops) measured slower than this GEMM on B200
-  // (in-place cublasDtrmm_64: 186 vs 111 ms at c4's last update), so the GEMM stays.
+  // Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep).  Gathering the r pivot
+  // columns and an in-place cublasDtrmm_64 (d r^2 flops) measured slower than this GEMM
+  // (186 vs 111 ms at c4's last update).
   double* X = B->X.ensure(c, capc * capc);
   pw::tri_inverse_scatter(c, Rs, mr, m, piv, r, X);
   double* Y = B->Y.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));

@@ -189,18 +189,6 @@ __global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A,
   for (int k = lane; k <= c; k += 32) X[scatter ? (size_t)c * m + piv[k] : (size_t)c * r + k] = b[k];
 }
 
-// Y[:, k] = M[:, piv[k]], k < r (d rows, column-major, ld d)
-__global__ void gather_cols_kernel(double* __restrict__ Y, const double* __restrict__ M, long long d,
-                                   const int* __restrict__ piv, int r) {
-  const long long total = d * r;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(idx / d);
-    const long long row = idx - (long long)k * d;
-    Y[idx] = M[(long long)piv[k] * d + row];
-  }
-}
-
 // ---------------------------------------------------------------- fused serial step
 // One HBM pass over D and Q per serial correction step (2 r d 8 bytes).  A
 // persistent grid of 2 CTAs per SM walks 1024-row tiles: 4 rows per thread and
@@ -788,29 +776,6 @@ void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv,
     attr = smem;
   }
   tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, m, piv, r, X, 1);
-  c.launches += 1;
-  PW_LAUNCH_CHECK();
-}
-
-void tri_inverse(Ctx& c, const double* R, int mr, const int* piv, int r, double* Rinv) {
-  if (r <= 0) return;
-  PW_CUDA(cudaMemsetAsync(Rinv, 0, sizeof(double) * (size_t)r * r, c.stream));
-  size_t smem = sizeof(double) * mr * kQ2Warps;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    PW_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, mr, piv, r, Rinv, 0);
-  c.launches += 1;
-  PW_LAUNCH_CHECK();
-}
-
-void launch_gather_cols(Ctx& c, double* Y, const double* M, long long d, const int* piv, int r) {
-  if (r <= 0) return;
-  const long long total = d * r;
-  int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c.num_sms * 16));
-  gather_cols_kernel<<<blocks, 256, 0, c.stream>>>(Y, M, d, piv, r);
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }

@@ -158,10 +158,6 @@ int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv
                      double* tau_dev, double* diag_dev, int* rank_host);
 void form_q2(Ctx& c, const double* R, int mr, const int* piv, const double* tau, int r,
              double* Q2);
-// plain upper-triangular R11^-1 (r x r, ld r) of the pivoted factor
-void tri_inverse(Ctx& c, const double* R, int mr, const int* piv, int r, double* Rinv);
-// Y[:, k] = M[:, piv[k]] for k < r
-void launch_gather_cols(Ctx& c, double* Y, const double* M, long long d, const int* piv, int r);
 void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv, int r,
                          double* X);
 // y = [g +] c + D alpha (rd cols) and alpha_next = Q^T y (rq cols); nblk <= 0: default grid
