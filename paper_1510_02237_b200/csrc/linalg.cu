@@ -168,8 +168,7 @@ __global__ void __launch_bounds__(kQ2Warps * 32) form_q2_kernel(const double* A,
 // X[piv[k], c] = (R11^-1)[k, c]; R11[i][k] = A[i, piv[k]] (i <= k < r).
 // Column-oriented back substitution, one warp per column, b staged in smem.
 __global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A, int mr, int m,
-                                                                 const int* piv, int r, double* X,
-                                                                 int scatter) {
+                                                                 const int* piv, int r, double* X) {
   extern __shared__ double bs[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * kQ2Warps + warp;
@@ -185,8 +184,7 @@ __global__ void __launch_bounds__(kQ2Warps * 32) tri_inv_kernel(const double* A,
     if (lane == 0) b[l] = yl;
     __syncwarp();
   }
-  // scatter: X[piv[k], c] (m x r); else the plain upper-triangular R11^-1 (r x r)
-  for (int k = lane; k <= c; k += 32) X[scatter ? (size_t)c * m + piv[k] : (size_t)c * r + k] = b[k];
+  for (int k = lane; k <= c; k += 32) X[(size_t)c * m + piv[k]] = b[k];
 }
 
 // ---------------------------------------------------------------- fused serial step
@@ -775,7 +773,7 @@ void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv,
     PW_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, m, piv, r, X, 1);
+  tri_inv_kernel<<<(r + kQ2Warps - 1) / kQ2Warps, kQ2Warps * 32, smem, c.stream>>>(R, mr, m, piv, r, X);
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }
