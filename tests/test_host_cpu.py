@@ -174,3 +174,16 @@ def test_initial_state_generators_seeded():
     u = q3[: 64 * 64]
     assert np.max(np.abs(u)) == pytest.approx(1e-3)
     assert q3[2 * 64 * 64:].max() <= 1.0
+
+
+def test_damping_coefficient_known_values():
+    """reference tests/test_physics.py:19-35"""
+    from paper_1510_02237_b200.physics import damping_coefficients
+
+    assert damping_coefficients(0.0, 0.025, 0.1, 0.3) == (0.0, 0.0)
+    a1, a2 = damping_coefficients(0.1, 0.025, 0.025, (1.0 / 300.0) / 4.0)
+    assert a1 == pytest.approx(0.075, rel=1e-12) and a2 == pytest.approx(0.075, rel=1e-12)
+    a1, _ = damping_coefficients(0.005, 0.025, 0.025, 0.2 * 0.025 / 30.0)
+    assert a1 == pytest.approx(0.01875, rel=1e-10)
+    with pytest.raises(ValueError, match="timescale"):
+        damping_coefficients(0.1, 0.025, 0.025, 0.0)
