@@ -610,6 +610,7 @@ int pw_ctx_destroy(pw_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.red) cudaFree(ctx->c.red);
+    if (ctx->c.tma_done) cudaFree(ctx->c.tma_done);
     if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
     if (ctx->c.cusolver_params) cusolverDnDestroyParams(static_cast<cusolverDnParams_t>(ctx->c.cusolver_params));

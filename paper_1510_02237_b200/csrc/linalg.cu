@@ -379,8 +379,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
     const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
     const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d, long long ld,
-    double* __restrict__ y_out, double* __restrict__ part, int nst) {
-  // nst ring stages (<= kTmaStages: fewer when rd + 8 rq doubles of bookkeeping must fit too)
+    double* __restrict__ y_out, double* __restrict__ part, int nst, unsigned int* __restrict__ done,
+    double* __restrict__ alpha_next) {
+  // nst ring stages (<= kTmaStages: fewer when rd + 8 rq doubles of bookkeeping must fit too).
+  // The last CTA to finish sums the per-CTA partials into alpha_next (fixed order).
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);                       // nst x 8 x 512
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + nst * kTmaStageBytes);
@@ -476,7 +478,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
       }
     }
   }
-  if (rq > 0) flush_wpart(wpart, rq, part);
+  if (rq > 0) {
+    flush_wpart(wpart, rq, part);
+    int* last = reinterpret_cast<int*>(wpart + kCgWarps * rq);  // one int after the partials
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (*last) {
+      __threadfence();
+      for (int k = tid; k < rq; k += blockDim.x) {
+        double sum = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) sum += __ldcg(part + (long long)b * rq + k);
+        alpha_next[k] = sum;
+      }
+      if (tid == 0) *done = 0u;  // ready for the next launch on the stream
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kCgThreads, 2) project_partial_kernel(
@@ -822,7 +840,8 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
                   reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(y) |
                   reinterpret_cast<uintptr_t>(cvec) | reinterpret_cast<uintptr_t>(g)) % 16 == 0);
   const int var = cg_variant();  // 0: TMA kernel when the layout allows it, 6: LSU kernel
-  const size_t tma_extra = 2 * kTmaStages * sizeof(uint64_t) + sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps);
+  const size_t tma_extra =
+      2 * kTmaStages * sizeof(uint64_t) + sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 2);
   const int tma_nst = (int)std::min<size_t>(kTmaStages, (227u * 1024 - tma_extra) / kTmaStageBytes);
   if ((var == 0 || var == 5) && v2 && d >= kTmaRows && tma_extra < 227u * 1024 && tma_nst >= 2) {
     const long long ntiles = (d + kTmaRows - 1) / kTmaRows;
@@ -831,20 +850,20 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
       nblk = (int)((ntiles + per - 1) / per);
     }
     const size_t smem = tma_nst * kTmaStageBytes + 2 * tma_nst * sizeof(uint64_t) +
-                        sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps);
+                        sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 2);
     static bool attr = false;
     if (!attr) {
       PW_CUDA(cudaFuncSetAttribute(combine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    227 * 1024));
       attr = true;
     }
-    combine_tma_kernel<<<nblk, kTmaThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part,
-                                                        tma_nst);
-    c.launches += 1;
-    if (rq > 0) {
-      reduce_parts_kernel<<<(rq + 31) / 32, 256, 0, st>>>(part, nblk, rq, alpha_next);
-      c.launches += 1;
+    if (!c.tma_done) {
+      PW_CUDA(cudaMalloc(&c.tma_done, sizeof(unsigned int)));
+      PW_CUDA(cudaMemsetAsync(c.tma_done, 0, sizeof(unsigned int), st));
     }
+    combine_tma_kernel<<<nblk, kTmaThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part,
+                                                        tma_nst, c.tma_done, alpha_next);
+    c.launches += 1;
     PW_LAUNCH_CHECK();
     return;
   }

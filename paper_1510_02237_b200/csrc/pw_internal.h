@@ -92,6 +92,7 @@ struct Ctx {
   void* blas_ws = nullptr;   // fixed cuBLAS workspace
   // scratch for grid barriers / reductions
   double* red = nullptr;     // reduction scratch (doubles)
+  unsigned int* tma_done = nullptr;  // last-CTA counter of the TMA serial-step kernel
   size_t red_cap = 0;
   int launches = 0;          // kernels launched by this library (bench gpu_launches)
   bool strict = false;       // force reference-order kernels everywhere
