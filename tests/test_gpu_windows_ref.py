@@ -73,4 +73,11 @@ def test_c3_window_matches_reference_run():
 
 
 def test_c4_first_iteration_matches_reference_run():
-    check_window("c4", [1e-10] * 4)
+    """c4 iteration 1: ranks equal (142) but the rank gap is tight -- kept min |R_jj|/|R_11|
+    1.36e-10 against dropped max 9.45e-11, so cond(R11) ~ 7e9 and eps * cond ~ 1.6e-6.
+    Two QR algorithms (the reference's dgeqp3 on S, this repo's Householder of S + pivoted
+    QR of R1) then legitimately differ at that level: measured 1.3e-6 max / 6.2e-7 median,
+    identical in strict mode (so not the stencils), while the same-algorithm perturbation
+    floor (fast vs strict kernels, scripts/floor_check.py) is 3.2e-8.
+    expects c4/c5 floors of 1e-6 to 1e-5; the bound used is 1e-5."""
+    check_window("c4", [1e-5] * 4)
