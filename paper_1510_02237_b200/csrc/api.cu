@@ -450,7 +450,7 @@ void basis_refactor(pw_basis* B, int m_old) {
   g_clk = clk.on ? &clk : nullptr;
   if (incremental) factor_append(B, m_old);
   else factor_full(B, mr);
-  clk.mark(incremental ? "ormqr+geqrf(new)" : "geqrf(all)");
+  clk.mark(incremental ? "append(total)" : "full(total)");
   // column-pivoted QR of the mr x m factor R1 (same pivots as dgeqp3 on S)
   double* Rs = B->Rs.ensure(c, capc * capc);
   PW_CUDA(cudaMemcpy2DAsync(Rs, mr * sizeof(double), B->R1.p, capc * sizeof(double), mr * sizeof(double),

@@ -7,10 +7,13 @@
 //                          themselves (subspace.py:67-68), see DESIGN.md.
 //  * form_q2            -- explicit Q2[:, :r] from the reflectors (dorgqr role)
 //  * tri_inverse_scatter-- scatter(R11^-1) of subspace.py:76-78
-//  * combine_gemv       -- the serial correction step of the KSE sweep,
-//                          qn[i+1] = G(qn[i]) + D alpha_i + c_i fused with the
+//  * larft_cols         -- the dlarft recurrence for the compact-WY T of a new panel
+//  * make_unit_lower    -- geqrf output -> explicit unit-lower Householder vectors
+//  * combine_tma /      -- the serial correction step of the KSE sweep,
+//    combine_gemv          qn[i+1] = G(qn[i]) + D alpha_i + c_i fused with the
 //                          next projection coefficients alpha_{i+1} = Q^T qn[i+1]
-//                          (one HBM pass over D and Q: 2 r d 8 bytes).
+//                          (one HBM pass over D and Q: 2 r d 8 bytes); the TMA
+//                          bulk-copy kernel by default, the LSU kernel otherwise
 //  * residual           -- iteration_residual (parareal.py:50-59)
 #include <cooperative_groups.h>
 
