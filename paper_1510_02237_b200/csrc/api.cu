@@ -956,10 +956,17 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
                    " GiB for its d x " + std::to_string(B->cap) + " basis even without a snapshot copy; " +
                    std::to_string((long long)(free_b >> 30)) + " GiB free on this device");
     }
-    cudaEvent_t ev[4];
+    struct Events {  // destroyed on every exit path, errors included
+      cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+      ~Events() {
+        for (auto& x : e)
+          if (x) cudaEventDestroy(x);
+      }
+    } evs;
+    cudaEvent_t* ev = evs.e;
     const bool timed = timings != nullptr;
     double t_coarse = 0, t_fine = 0, t_qr = 0;
-    if (timed) for (auto& e : ev) PW_CUDA(cudaEventCreate(&e));
+    if (timed) for (int i = 0; i < 4; ++i) PW_CUDA(cudaEventCreate(&ev[i]));
     auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
       float ms = 0;
       PW_CUDA(cudaEventSynchronize(b));
@@ -1101,7 +1108,6 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       timings[0] = t_coarse;
       timings[1] = t_fine;
       timings[2] = t_qr;
-      for (auto& e : ev) cudaEventDestroy(e);
     }
     if (out_basis) *out_basis = B.release();
   });
