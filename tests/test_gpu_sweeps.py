@@ -414,6 +414,9 @@ def test_sharded_fine_hook_single_rank_group():
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         ends_g, res_g, _ = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it, group=dist.group.WORLD)
+        import bench  # the collective self-test bench.py runs before multi-GPU windows
+
+        assert bench.comm_selftest(dist)
     finally:
         dist.destroy_process_group()
     ends, res, _ = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
