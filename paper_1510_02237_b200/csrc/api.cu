@@ -429,7 +429,10 @@ static void factor_append(pw_basis* B, int m_old) {
   B->v_cols = m_old + k;
 }
 
-void basis_refactor(pw_basis* B, int m_old) {
+// Everything of the refactorisation that depends on the snapshots only: the QR of S, the
+// pivoted QR of R1 and the rank, Q, and the scattered R11^-1 (X).  The sweep runs it on the
+// side stream while the fine propagator runs (the images are not needed until Y).
+void basis_factor(pw_basis* B, int m_old) {
   Ctx& c = B->ctx->c;
   PhaseClock clk(c.stream);
   clk.mark("start");
@@ -466,10 +469,7 @@ void basis_refactor(pw_basis* B, int m_old) {
   PW_CUDA(cudaMemcpyAsync(B->diag_h.data(), diag, sizeof(double) * mr, cudaMemcpyDeviceToHost, c.stream));
   PW_CUDA(cudaMemcpyAsync(B->piv_h.data(), piv, sizeof(int) * m, cudaMemcpyDeviceToHost, c.stream));
   B->r = r;
-  if (r == 0) {
-    PW_CUDA(cudaStreamSynchronize(c.stream));
-    return;
-  }
+  if (r == 0) return;
   // Q = Q1 [Q2[:, :r]; 0] = [Q2; 0] - V (T (V[0:mr]^T Q2))
   double* Q2 = B->Q2.ensure(c, capc * capc);
   pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
@@ -485,30 +485,53 @@ void basis_refactor(pw_basis* B, int m_old) {
     gemm(c, false, false, d, r, k, -1.0, B->W.p, d, X2, k, 1.0, Q, d);
   }
   clk.mark("Q=Q1Q2");
-  // Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep).  Gathering the r pivot
-  // columns and an in-place cublasDtrmm_64 (d r^2 flops) measured slower than this GEMM
-  // (186 vs 111 ms at c4's last update).
   double* X = B->X.ensure(c, capc * capc);
   pw::tri_inverse_scatter(c, Rs, mr, m, piv, r, X);
-  double* Y = B->Y.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
-  gemm(c, false, false, d, r, m, 1.0, B->M.p, d, X, m, 0.0, Y, d);
-  clk.mark("Rinv+Y");
-  PW_CUDA(cudaStreamSynchronize(c.stream));
+  B->Y.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
+  clk.mark("Rinv");
 }
 
-void basis_append(pw_basis* B, const double* states, long long lds, const double* m_cols,
-                  long long ldm, int p) {
+// Y = M scatter(R11^-1)   (FQ, or D = (F-G)(S) R^-1 in the sweep) -- the only part of the
+// refactorisation that needs the images.  Gathering the r pivot columns and an in-place
+// cublasDtrmm_64 (d r^2 flops) measured slower than this GEMM (186 vs 111 ms, c4).
+void basis_images_gemm(pw_basis* B) {
+  Ctx& c = B->ctx->c;
+  if (B->r == 0) return;
+  const long long d = B->dim;
+  gemm(c, false, false, d, B->r, B->m, 1.0, B->M.p, d, B->X.p, B->m, 0.0, B->Y.p, d);
+}
+
+void basis_refactor(pw_basis* B, int m_old) {
+  basis_factor(B, m_old);
+  basis_images_gemm(B);
+  PW_CUDA(cudaStreamSynchronize(B->ctx->c.stream));
+}
+
+// snapshot columns (lean sweeps keep them only as W's not-yet-factored columns)
+void basis_append_snapshots(pw_basis* B, const double* states, long long lds, int p) {
   Ctx& c = B->ctx->c;
   PW_CHECK(p >= 0, PW_ERR_VALUE, "negative column count");
   PW_CHECK(B->m + p <= B->cap, PW_ERR_VALUE,
            "subspace capacity exceeded (" + std::to_string(B->m + p) + " > " + std::to_string(B->cap) + ")");
   const long long d = B->dim;
-  // lean sweeps keep the snapshots only as W's not-yet-factored columns
   double* S = B->lean ? B->W.ensure(c, (size_t)d * B->cap) : B->S.ensure(c, (size_t)d * B->cap);
-  double* M = B->M.ensure(c, (size_t)d * B->cap);
   copy_cols(c, S + (size_t)B->m * d, d, states, lds, d, p);
-  copy_cols(c, M + (size_t)B->m * d, d, m_cols, ldm, d, p);
   B->m += p;
+}
+
+// the matching image columns at column offset col0
+void basis_append_images(pw_basis* B, int col0, const double* m_cols, long long ldm, int p) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  double* M = B->M.ensure(c, (size_t)d * B->cap);
+  copy_cols(c, M + (size_t)col0 * d, d, m_cols, ldm, d, p);
+}
+
+void basis_append(pw_basis* B, const double* states, long long lds, const double* m_cols,
+                  long long ldm, int p) {
+  const int m_old = B->m;
+  basis_append_snapshots(B, states, lds, p);
+  basis_append_images(B, m_old, m_cols, ldm, p);
 }
 
 // alpha (r x batch) = Q^T v
@@ -601,6 +624,8 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     PW_SOLVER(cusolverDnSetStream(sh, ctx->c.stream));
     ctx->c.cusolver = sh;
     if (const char* e = std::getenv("PW_ROW_SHARDS")) ctx->c.vshards = std::atoi(e);
+    PW_CUDA(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
+    if (const char* e = std::getenv("PW_QR_OVERLAP")) ctx->c.qr_overlap = std::atoi(e) != 0;
     *out = ctx.release();
   });
 }
@@ -611,6 +636,10 @@ int pw_ctx_destroy(pw_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.red) cudaFree(ctx->c.red);
     if (ctx->c.tma_done) cudaFree(ctx->c.tma_done);
+    if (ctx->c.side) {
+      cudaStreamSynchronize(ctx->c.side);
+      cudaStreamDestroy(ctx->c.side);
+    }
     if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
     if (ctx->c.cusolver_params) cusolverDnDestroyParams(static_cast<cusolverDnParams_t>(ctx->c.cusolver_params));
@@ -905,6 +934,32 @@ int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long 
 }
 
 // ------------------------------------------------------------ the sweep
+namespace {
+// Run a scope's launches (our kernels, cuBLAS, cuSOLVER) on another stream.
+struct StreamScope {
+  Ctx& c;
+  cudaStream_t saved;
+  StreamScope(Ctx& ctx, cudaStream_t s) : c(ctx), saved(ctx.stream) { set(s); }
+  ~StreamScope() { set(saved); }
+  void set(cudaStream_t s) {
+    c.stream = s;
+    cublasSetStream(blas(c), s);
+    cusolverDnSetStream(solver(c), s);
+  }
+};
+struct SyncEvents {
+  cudaEvent_t snap = nullptr, fact = nullptr;
+  SyncEvents() {
+    PW_CUDA(cudaEventCreateWithFlags(&snap, cudaEventDisableTiming));
+    PW_CUDA(cudaEventCreateWithFlags(&fact, cudaEventDisableTiming));
+  }
+  ~SyncEvents() {
+    cudaEventDestroy(snap);
+    cudaEventDestroy(fact);
+  }
+};
+}  // namespace
+
 int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double* q0, int n_c,
              int n_it, double tol, double rank_tol, double* out_states, double* residuals,
              int* n_done, double* timings, int* ranks, pw_basis** out_basis) {
@@ -983,9 +1038,13 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       PW_CUDA(cudaEventRecord(ev[1], c.stream));
       t_coarse += elapsed(ev[0], ev[1]);
     }
+    SyncEvents sync;
     int k_done = 0;
     for (int k = 0; k < n_it; ++k) {
       if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
+      // the snapshots qk[0..P-1] are final here: their QR runs on the side stream while
+      // the fine propagator runs on the main one (only Y needs the fine images)
+      if (kse) PW_CUDA(cudaEventRecord(sync.snap, c.stream));
       // fine predictor over all slices at once (_fine_all, parareal.py:62-65)
       if (c.fine_hook) {
         const int rc = c.fine_hook(c.fine_hook_user, QK, PRED, n_c, d);
@@ -994,15 +1053,23 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         prop_apply(fine, QK, PRED, n_c, d);
       }
       if (timed) PW_CUDA(cudaEventRecord(ev[1], c.stream));
+      const int m_old = kse ? B->m : 0;
+      if (kse) {
+        StreamScope side(c, c.qr_overlap ? c.side : c.stream);
+        PW_CUDA(cudaStreamWaitEvent(c.stream, sync.snap, 0));
+        basis_append_snapshots(B.get(), QK, d, n_c);
+        basis_factor(B.get(), m_old);  // blocks the host at the rank read; the fine sweep runs on
+        PW_CUDA(cudaEventRecord(sync.fact, c.stream));
+      }
       // c_i = F(qk[i]) - G(qk[i])  [- D Q^T qk[i] in KSE mode]
       pw::launch_axpby_cols(c, PRED, PRED, GK, 1.0, -1.0, (size_t)d * n_c);
       int r = 0;
       double* alpha = nullptr;
       double* alpha_next = nullptr;
       if (kse) {
-        const int m_old = B->m;
-        basis_append(B.get(), QK, d, PRED, d, n_c);
-        basis_refactor(B.get(), m_old);
+        basis_append_images(B.get(), m_old, PRED, d, n_c);
+        PW_CUDA(cudaStreamWaitEvent(c.stream, sync.fact, 0));
+        basis_images_gemm(B.get());
         r = B->r;
         if (ranks) ranks[k] = r;
         if (r > 0) {
