@@ -162,12 +162,13 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
     for (int r = 0; r < BY; ++r) {
       double w[WW];
       ldrow(w, rowp(r), W, 0);
+      // tap-major order: BX independent FMA chains per tap (same per-cell summation order)
 #pragma unroll
-      for (int x = 0; x < BX; ++x) {
-        av[r][x] = C.cxv[0] * w[x + 1];
+      for (int x = 0; x < BX; ++x) av[r][x] = C.cxv[0] * w[x + 1];
 #pragma unroll
-        for (int k = 1; k < 7; ++k) av[r][x] = fma(C.cxv[k], w[x + 1 + k], av[r][x]);
-      }
+      for (int k = 1; k < 7; ++k)
+#pragma unroll
+        for (int x = 0; x < BX; ++x) av[r][x] = fma(C.cxv[k], w[x + 1 + k], av[r][x]);
 #pragma unroll
       for (int k = 0; k < WH; ++k) vh[r + 1][k] = w[k + 2];
     }
@@ -198,10 +199,12 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
 #pragma unroll
       for (int x = 0; x < BX; ++x) {
         au[r][x] = C.cxu[0] * w[x + 1];
-#pragma unroll
-        for (int k = 1; k < 7; ++k) au[r][x] = fma(C.cxu[k], w[x + 1 + k], au[r][x]);
         ap[r][x] = C.pu * (w[x + 5] - w[x + 3]);
       }
+#pragma unroll
+      for (int k = 1; k < 7; ++k)
+#pragma unroll
+        for (int x = 0; x < BX; ++x) au[r][x] = fma(C.cxu[k], w[x + 1 + k], au[r][x]);
 #pragma unroll
       for (int k = 0; k < WH; ++k) uh[r + 1][k] = w[k + 2];
     }
@@ -221,9 +224,11 @@ __device__ __forceinline__ void stage_item(const Ring in, const Ring qr, int S, 
       double w[WW];
       ldrow(w, rowp(r), 2 * W, 0);
 #pragma unroll
-      for (int x = 0; x < BX; ++x) {
+      for (int k = 0; k < 7; ++k)
 #pragma unroll
-        for (int k = 0; k < 7; ++k) ap[r][x] = fma(C.cxp[k], w[x + 1 + k], ap[r][x]);
+        for (int x = 0; x < BX; ++x) ap[r][x] = fma(C.cxp[k], w[x + 1 + k], ap[r][x]);
+#pragma unroll
+      for (int x = 0; x < BX; ++x) {
         au[r][x] = fma(C.pgx, w[x + 5] - w[x + 3], au[r][x]);
         pc[r][x] = w[x + 4];
       }
