@@ -556,6 +556,8 @@ void make_fused_params(FusedParams& fp, int nx, int ny, double dx, double dy, do
 
 void launch_rk3_fused(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch,
                       bool vadv) {
+  if (!vadv && march_supported(fp.nx, fp.ny, fp.ld_in, fp.ld_out, in, out))
+    return launch_rk3_march(c, fp, in, out, batch);
   if (vadv) launch_ry<3, true>(c, fp, in, out, batch);
   else launch_ry<2, false>(c, fp, in, out, batch);
 }

@@ -1,0 +1,412 @@
+// Row-marching fused RK3 step for constant x-advection (V = 0), sm_100a, fp64.
+//
+// Same operator as rk3_fused_kernel (fine_fused.cu: the folded constant-
+// velocity RK3 of integrators.py:126-146 with acoustic_rhs,
+// numba_backend.py:119-128), with a data movement built around the fact that
+// the y coupling of the operator is narrow (radius 1, radius 2 only for the
+// v damping) while the x stencils are 7 wide:
+//
+// * A CTA owns whole grid rows (TX = nx, periodic in x: 4 ghost columns on
+//   each side of every ring row, so there is no x halo recompute) and a
+//   y-segment of TY rows of one state.  It marches down the segment one row
+//   per tick.
+// * Three warp groups, one per RK stage.  In tick t stage 1 consumes q row
+//   t-6, stage 2 s1 row t-9, stage 3 s2 row t-12: each group reads rows the
+//   previous group finished in an earlier tick, so one barrier per tick.
+// * y coupling in registers ("scatter"): a thread consuming input row k adds
+//   its x-stencil terms to row k and its y-difference terms to the
+//   accumulators of rows k-2..k+2, which it keeps in registers (u, p: 3 rows,
+//   v: 5 rows).  Rows k-1 (u, p) and k-2 (v) are then complete and stored
+//   (stage 1/2: shared ring; stage 3: global).  Only the input row's x
+//   windows come from shared memory: 3 fields x (BX+8) doubles per BX cells.
+// * q rows arrive by 16-byte cp.async two ticks ahead into an 8-row ring;
+//   stages 2/3 take their q base from it when a row's accumulator is born.
+//
+// Shared-memory rows are chunk-swizzled (chunk c at c ^ ((c >> 3) & (BX/2-1)))
+// so the BX/2-chunk thread stride of the window loads is conflict free.
+#include "pw_internal.h"
+
+namespace pw {
+namespace {
+
+template <int NX_, int BX_>
+struct MC {
+  static constexpr int NX = NX_, BX = BX_;
+  static constexpr int G = NX / BX;    // threads per stage group
+  static constexpr int NT = 3 * G;
+  static constexpr int RW = NX + 8;    // doubles per ring field row: cols [-4, NX+4)
+  static constexpr int CHR = RW / 2;   // 16-byte chunks per field row
+  static constexpr int SLOT = 3 * RW;  // doubles per ring slot (u, v, p)
+  static constexpr int NQ = 8, N1 = 3, N2 = 3;
+  static constexpr size_t SMEM = sizeof(double) * SLOT * (NQ + N1 + N2);
+  static constexpr int SWZ = BX / 2 - 1;
+  static constexpr int WN = BX + 8;    // window: cols [x-4, x+BX+4)
+  static constexpr int WC = WN / 2;    // window chunks
+  static constexpr int NCH = 3 * CHR;  // chunks per q row
+  static constexpr int NLD = (NCH + NT - 1) / NT;
+  static constexpr int MINB = (int)((227 * 1024) / (SMEM + 1024)) < 1 ? 1 : (int)((227 * 1024) / (SMEM + 1024));
+  static_assert(G % 32 == 0, "stage groups must be whole warps");
+  static_assert(BX == 4 || BX == 8, "BX is 4 or 8");
+  static_assert(CHR % 4 == 0, "row chunks must be a multiple of the swizzle block");
+};
+
+// lags: stage S consumes row t - LAG[S] in tick t; it is active for rows [LO, HI + TY]
+__host__ __device__ constexpr int lag_of(int S) { return S == 0 ? 6 : S == 1 ? 9 : 12; }
+__host__ __device__ constexpr int lo_of(int S) { return S == 0 ? -6 : S == 1 ? -4 : -2; }
+__host__ __device__ constexpr int hi_of(int S) { return S == 0 ? 5 : S == 1 ? 3 : 1; }
+
+__device__ __forceinline__ int swz(int c, int m) { return c ^ ((c >> 3) & m); }
+
+__device__ __forceinline__ void bar_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void ld_chunks(double (&w)[2 * N], const double* row, const int* off) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double2 t = *reinterpret_cast<const double2*>(row + off[j]);
+    w[2 * j] = t.x;
+    w[2 * j + 1] = t.y;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void st_chunks(double* row, const int* off, const double (&v)[2 * N]) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) *reinterpret_cast<double2*>(row + off[j]) = make_double2(v[2 * j], v[2 * j + 1]);
+}
+
+// One stage thread's state: accumulators of rows k-1..k+1 (u, p) and k-2..k+2 (v)
+// relative to the row k it consumes next.
+template <class K>
+struct Acc {
+  double u[3][K::BX], p[3][K::BX], v[5][K::BX];
+};
+
+// Consume input row `in` (3 field rows, RW apart).  base_up / base_v: q rows k+1 and
+// k+2 (S > 0; the births of rows k+1 (u, p) and k+2 (v) start from q there).
+template <class K, int S>
+__device__ __forceinline__ void consume(Acc<K>& A, const double* in, const double* base_up,
+                                        const double* base_v, const int* woff, const StageCoef& C) {
+  constexpr int BX = K::BX;
+  double w[K::WN];
+  // ---- v: x stencil of row k; v_x (mixed damping of u) and v itself (p's v_y, v_yy)
+  //      go to rows k+-1 / k+-2; births of rows k+1 (u, p) and k+2 (v)
+  ld_chunks<K::WC>(w, in + K::RW, woff);
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+#pragma unroll
+    for (int c = 0; c < BX; ++c) A.v[2][c] = fma(C.cxv[m], w[c + 1 + m], A.v[2][c]);
+  {
+    double b[BX];
+    if constexpr (S > 0) ld_chunks<BX / 2>(b, base_up, woff + 2);
+#pragma unroll
+    for (int c = 0; c < BX; ++c) {
+      const double t1 = C.cuv * (w[c + 5] - w[c + 3]);
+      A.u[0][c] += t1;
+      A.u[2][c] = (S > 0) ? b[c] - t1 : -t1;
+    }
+  }
+  {
+    double b[BX];
+    if constexpr (S > 0) ld_chunks<BX / 2>(b, base_up + 2 * K::RW, woff + 2);
+#pragma unroll
+    for (int c = 0; c < BX; ++c) {
+      A.p[0][c] = fma(C.pv, w[c + 4], A.p[0][c]);
+      A.p[2][c] = (S > 0) ? fma(-C.pv, w[c + 4], b[c]) : -C.pv * w[c + 4];
+    }
+  }
+  {
+    double b[BX];
+    if constexpr (S > 0) ld_chunks<BX / 2>(b, base_v + K::RW, woff + 2);
+#pragma unroll
+    for (int c = 0; c < BX; ++c) {
+      A.v[0][c] = fma(C.dv2, w[c + 4], A.v[0][c]);
+      A.v[4][c] = (S > 0) ? fma(C.dv2, w[c + 4], b[c]) : C.dv2 * w[c + 4];
+    }
+  }
+  // ---- u: x stencil of row k, u_x for p(k) and the mixed damping of v(k+-1)
+  double t2[BX];
+  ld_chunks<K::WC>(w, in, woff);
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+#pragma unroll
+    for (int c = 0; c < BX; ++c) A.u[1][c] = fma(C.cxu[m], w[c + 1 + m], A.u[1][c]);
+#pragma unroll
+  for (int c = 0; c < BX; ++c) {
+    const double bx = w[c + 5] - w[c + 3];
+    A.p[1][c] = fma(C.pu, bx, A.p[1][c]);
+    t2[c] = C.cvu * bx;
+  }
+  // ---- p: x stencil of row k, p_x for u(k), p_y for v(k+-1)
+  ld_chunks<K::WC>(w, in + 2 * K::RW, woff);
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+#pragma unroll
+    for (int c = 0; c < BX; ++c) A.p[1][c] = fma(C.cxp[m], w[c + 1 + m], A.p[1][c]);
+#pragma unroll
+  for (int c = 0; c < BX; ++c) {
+    A.u[1][c] = fma(C.pgx, w[c + 5] - w[c + 3], A.u[1][c]);
+    t2[c] = fma(C.pgy, w[c + 4], t2[c]);
+    A.v[1][c] += t2[c];
+    A.v[3][c] -= t2[c];
+  }
+}
+
+template <class K>
+__device__ __forceinline__ void rotate(Acc<K>& A) {
+#pragma unroll
+  for (int c = 0; c < K::BX; ++c) {
+    A.u[0][c] = A.u[1][c];
+    A.u[1][c] = A.u[2][c];
+    A.p[0][c] = A.p[1][c];
+    A.p[1][c] = A.p[2][c];
+    A.v[0][c] = A.v[1][c];
+    A.v[1][c] = A.v[2][c];
+    A.v[2][c] = A.v[3][c];
+    A.v[3][c] = A.v[4][c];
+  }
+}
+
+struct Seg {
+  const double* src;
+  double* dst;
+  long long n;  // nx * ny
+  int ny, y0, TY;
+};
+
+// Consume row k and store the completed rows (k-1: u, p; k-2: v) of stage S.
+template <class K, int S>
+__device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg, const FusedParams& P,
+                                           int g, int k, int z, const int* woff, int goff0,
+                                           int goff1, bool ghost) {
+  constexpr int BX = K::BX;
+  double* qring = sm;
+  double* r1 = qring + K::NQ * K::SLOT;
+  double* r2 = r1 + K::N1 * K::SLOT;
+  const double* in;
+  if constexpr (S == 0) in = qring + (size_t)(k & 7) * K::SLOT;
+  else if constexpr (S == 1) in = r1 + (size_t)((k + 30) % 3) * K::SLOT;
+  else in = r2 + (size_t)((k + 30) % 3) * K::SLOT;
+  const double* bup = qring + (size_t)((k + 1) & 7) * K::SLOT;
+  const double* bv = qring + (size_t)((k + 2) & 7) * K::SLOT;
+  // z == 0 but opaque: the 3 stages' 84 coefficients are read from the parameter bank
+  // inside the tick (uniform registers) instead of being hoisted out of the loop
+  consume<K, S>(A, in, bup, bv, woff, P.st[S + z]);
+  if constexpr (S < 2) {
+    double* out = (S == 0 ? r1 : r2);
+    double* o1 = out + (size_t)((k + 29) % 3) * K::SLOT;
+    double* o2 = out + (size_t)((k + 28) % 3) * K::SLOT;
+    st_chunks<BX / 2>(o1, woff + 2, A.u[0]);
+    st_chunks<BX / 2>(o1 + 2 * K::RW, woff + 2, A.p[0]);
+    st_chunks<BX / 2>(o2 + K::RW, woff + 2, A.v[0]);
+    if (ghost) {
+      // mirrored columns: the first 4 of thread 0's block, the last 4 of the last thread's
+      const bool first = (g == 0);
+      double gu[4], gp[4], gv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        gu[j] = first ? A.u[0][j] : A.u[0][BX - 4 + j];
+        gp[j] = first ? A.p[0][j] : A.p[0][BX - 4 + j];
+        gv[j] = first ? A.v[0][j] : A.v[0][BX - 4 + j];
+      }
+      *reinterpret_cast<double2*>(o1 + goff0) = make_double2(gu[0], gu[1]);
+      *reinterpret_cast<double2*>(o1 + goff1) = make_double2(gu[2], gu[3]);
+      *reinterpret_cast<double2*>(o1 + 2 * K::RW + goff0) = make_double2(gp[0], gp[1]);
+      *reinterpret_cast<double2*>(o1 + 2 * K::RW + goff1) = make_double2(gp[2], gp[3]);
+      *reinterpret_cast<double2*>(o2 + K::RW + goff0) = make_double2(gv[0], gv[1]);
+      *reinterpret_cast<double2*>(o2 + K::RW + goff1) = make_double2(gv[2], gv[3]);
+    }
+  } else {
+    const int x = g * BX;
+    if (k - 1 >= 0 && k - 1 < sg.TY) {
+      double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NX + x;
+#pragma unroll
+      for (int c = 0; c < BX; c += 2) {
+        *reinterpret_cast<double2*>(o + c) = make_double2(A.u[0][c], A.u[0][c + 1]);
+        *reinterpret_cast<double2*>(o + 2 * sg.n + c) = make_double2(A.p[0][c], A.p[0][c + 1]);
+      }
+    }
+    if (k - 2 >= 0 && k - 2 < sg.TY) {
+      double* o = sg.dst + sg.n + (long long)(sg.y0 + k - 2) * K::NX + x;
+#pragma unroll
+      for (int c = 0; c < BX; c += 2) *reinterpret_cast<double2*>(o + c) = make_double2(A.v[0][c], A.v[0][c + 1]);
+    }
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double* __restrict__ in,
+                                                                  double* __restrict__ out,
+                                                                  FusedParams P, int nseg) {
+  extern __shared__ __align__(16) double sm[];
+  const int ny = P.ny;
+  Seg sg;
+  sg.n = (long long)K::NX * ny;
+  sg.ny = ny;
+  sg.y0 = (int)((long long)blockIdx.x * ny / nseg);
+  sg.TY = (int)((long long)(blockIdx.x + 1) * ny / nseg) - sg.y0;
+  sg.src = in + (long long)blockIdx.y * P.ld_in;
+  sg.dst = out + (long long)blockIdx.y * P.ld_out;
+  const int tid = threadIdx.x;
+  // q-row copy assignment: chunk e = tid + j*NT of the 3 x CHR chunks of a row
+  int ld_soff[K::NLD];
+  int ld_goff[K::NLD];
+  int nld = 0;
+#pragma unroll
+  for (int j = 0; j < K::NLD; ++j) {
+    const int e = tid + j * K::NT;
+    if (e < K::NCH) {
+      const int f = e / K::CHR, c = e - f * K::CHR;
+      int col = 2 * c - 4;
+      col += (col < 0) ? K::NX : 0;
+      col -= (col >= K::NX) ? K::NX : 0;
+      ld_soff[j] = f * K::RW + 2 * swz(c, K::SWZ);
+      ld_goff[j] = f * (int)sg.n + col;
+      nld = j + 1;
+    } else {
+      ld_soff[j] = 0;
+      ld_goff[j] = 0;
+    }
+  }
+  // prologue: q rows -6 and -5 (ticks 0 and 1 of stage 1)
+  for (int rr = -6; rr <= -5; ++rr) {
+    int gy = sg.y0 + rr;
+    gy += (gy < 0) ? ny : 0;
+    double* slot = sm + (size_t)(rr & 7) * K::SLOT;
+    const double* rowp = sg.src + (long long)gy * K::NX;
+#pragma unroll
+    for (int j = 0; j < K::NLD; ++j)
+      if (j < nld) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+    cp_commit();
+  }
+  const int S = tid / K::G;  // warp uniform
+  const int g = tid - S * K::G;
+  constexpr int BX = K::BX;
+  // this thread's window chunk offsets inside a field row (fixed for the whole march)
+  int woff[K::WC];
+#pragma unroll
+  for (int j = 0; j < K::WC; ++j) woff[j] = 2 * swz(g * (BX / 2) + j, K::SWZ);
+  // ghost chunk offsets: thread 0 mirrors cols [0,4) to [NX, NX+4), the last thread
+  // cols [NX-4, NX) to [-4, 0)
+  int goff0 = 0, goff1 = 0;
+  if (g == 0) {
+    goff0 = 2 * swz(K::NX / 2 + 2, K::SWZ);
+    goff1 = 2 * swz(K::NX / 2 + 3, K::SWZ);
+  } else if (g == K::G - 1) {
+    goff0 = 2 * swz(0, K::SWZ);
+    goff1 = 2 * swz(1, K::SWZ);
+  }
+  const bool ghost = (g == 0) || (g == K::G - 1);
+  Acc<K> A;
+#pragma unroll
+  for (int c = 0; c < BX; ++c) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) A.u[r][c] = A.p[r][c] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) A.v[r][c] = 0.0;
+  }
+  const int TY = sg.TY;
+  const int nt = TY + 14;
+  const int lag = S == 0 ? lag_of(0) : S == 1 ? lag_of(1) : lag_of(2);
+  const int lo = S == 0 ? lo_of(0) : S == 1 ? lo_of(1) : lo_of(2);
+  const int hi = TY + (S == 0 ? hi_of(0) : S == 1 ? hi_of(1) : hi_of(2));
+  for (int t = 0; t < nt; ++t) {
+    cp_wait1();
+    bar_sync();
+    // q row t-4 (needed by stage 1 in tick t+2) into slot (t-4) & 7
+    {
+      const int rr = t - 4;
+      if (rr <= TY + 5) {
+        int gy = sg.y0 + rr;
+        gy += (gy < 0) ? ny : 0;
+        gy -= (gy >= ny) ? ny : 0;
+        double* slot = sm + (size_t)(rr & 7) * K::SLOT;
+        const double* rowp = sg.src + (long long)gy * K::NX;
+#pragma unroll
+        for (int j = 0; j < K::NLD; ++j)
+          if (j < nld) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+      }
+      cp_commit();
+    }
+    const int k = t - lag;
+    if (k < lo || k > hi) continue;
+    const int z = t & P.zmask;
+    if (S == 0) stage_tick<K, 0>(A, sm, sg, P, g, k, z, woff, goff0, goff1, ghost);
+    else if (S == 1) stage_tick<K, 1>(A, sm, sg, P, g, k, z, woff, goff0, goff1, ghost);
+    else stage_tick<K, 2>(A, sm, sg, P, g, k, z, woff, goff0, goff1, ghost);
+    rotate(A);
+  }
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+
+template <class K>
+void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
+  auto kern = rk3_march_kernel<K>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM));
+    if (per_sm < 1) per_sm = 1;
+  }
+  // segments per state: minimise (CTAs per SM, rounded up) x (rows + warm-up) per CTA
+  int nseg = env_int("PW_MARCH_NSEG", 0);
+  if (nseg <= 0) {
+    const int sms = c.num_sms > 0 ? c.num_sms : 148;
+    double best = 1e300;
+    for (int s = 1; s <= fp.ny / 16; ++s) {
+      const long long ctas = (long long)batch * s;
+      const double waves = (double)((ctas + sms - 1) / sms);
+      double cost = waves * ((double)fp.ny / s + 8.0);
+      if (ctas < (long long)sms * per_sm && s * 2 <= fp.ny / 16) cost *= 1.0 + 0.25 * (1.0 - (double)ctas / ((double)sms * per_sm));
+      if (cost < best) {
+        best = cost;
+        nseg = s;
+      }
+    }
+  }
+  dim3 grid(nseg, batch);
+  kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp, nseg);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in,
+                     const void* out) {
+  if (env_int("PW_MARCH", 1) == 0) return false;
+  if (!(nx == 128 || nx == 256 || nx == 384 || nx == 512)) return false;
+  if (ny < 32) return false;
+  if ((ld_in & 1) || (ld_out & 1)) return false;
+  if (((uintptr_t)in & 15) || ((uintptr_t)out & 15)) return false;
+  return true;
+}
+
+void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
+  const int bx = env_int("PW_MARCH_BX", 4);
+  switch (fp.nx) {
+    case 128: return launch_march_cfg<MC<128, 4>>(c, fp, in, out, batch);
+    case 256:
+      if (bx == 8) return launch_march_cfg<MC<256, 8>>(c, fp, in, out, batch);
+      return launch_march_cfg<MC<256, 4>>(c, fp, in, out, batch);
+    case 384: return launch_march_cfg<MC<384, 4>>(c, fp, in, out, batch);
+    case 512:
+      if (bx == 8) return launch_march_cfg<MC<512, 8>>(c, fp, in, out, batch);
+      return launch_march_cfg<MC<512, 4>>(c, fp, in, out, batch);
+    default:
+      throw Error{PW_ERR_VALUE, "row-marching RK3 needs nx in {128, 256, 384, 512}"};
+  }
+}
+
+}  // namespace pw

@@ -76,6 +76,7 @@ struct StageCoef {
 };
 struct FusedParams {
   int nx, ny;
+  int zmask = 0;  // always 0: (tick & zmask) keeps per-tick coefficient loads in the loop
   long long ld_in, ld_out;
   double sx, sy;  // 0.5/dx, 0.5/dy
   StageCoef st[3];
@@ -135,6 +136,10 @@ void make_fused_params(FusedParams& fp, int nx, int ny, double dx, double dy, do
 void launch_rk3_fused(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch,
                       bool vadv);
 bool fused_supported(int nx, int ny);
+// fine_march.cu: row-marching variant for V = 0 and whole-row CTAs
+bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in,
+                     const void* out);
+void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch);
 
 // linalg.cu
 void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,
