@@ -359,21 +359,21 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
     PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM));
     if (per_sm < 1) per_sm = 1;
   }
-  // segments per state: minimise (CTAs per SM, rounded up) x (rows + warm-up) per CTA
+  // segments per state: minimise waves x ticks per CTA (TY + 14), waves = CTAs over
+  // the resident CTA slots (c2: 4 segments, one wave; c3: 2 segments, one wave)
   int nseg = env_int("PW_MARCH_NSEG", 0);
   if (nseg <= 0) {
-    const int sms = c.num_sms > 0 ? c.num_sms : 148;
+    const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
     double best = 1e300;
     for (int s = 1; s <= fp.ny / 16; ++s) {
-      const long long ctas = (long long)batch * s;
-      const double waves = (double)((ctas + sms - 1) / sms);
-      double cost = waves * ((double)fp.ny / s + 8.0);
-      if (ctas < (long long)sms * per_sm && s * 2 <= fp.ny / 16) cost *= 1.0 + 0.25 * (1.0 - (double)ctas / ((double)sms * per_sm));
-      if (cost < best) {
+      const long long waves = ((long long)batch * s + slots - 1) / slots;
+      const double cost = (double)waves * ((double)fp.ny / s + 14.0);
+      if (cost < best - 1e-9) {
         best = cost;
         nseg = s;
       }
     }
+    if (nseg <= 0) nseg = 1;
   }
   dim3 grid(nseg, batch);
   kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp, nseg);
@@ -394,16 +394,11 @@ bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const vo
 }
 
 void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
-  const int bx = env_int("PW_MARCH_BX", 4);
   switch (fp.nx) {
     case 128: return launch_march_cfg<MC<128, 4>>(c, fp, in, out, batch);
-    case 256:
-      if (bx == 8) return launch_march_cfg<MC<256, 8>>(c, fp, in, out, batch);
-      return launch_march_cfg<MC<256, 4>>(c, fp, in, out, batch);
+    case 256: return launch_march_cfg<MC<256, 4>>(c, fp, in, out, batch);
     case 384: return launch_march_cfg<MC<384, 4>>(c, fp, in, out, batch);
-    case 512:
-      if (bx == 8) return launch_march_cfg<MC<512, 8>>(c, fp, in, out, batch);
-      return launch_march_cfg<MC<512, 4>>(c, fp, in, out, batch);
+    case 512: return launch_march_cfg<MC<512, 4>>(c, fp, in, out, batch);
     default:
       throw Error{PW_ERR_VALUE, "row-marching RK3 needs nx in {128, 256, 384, 512}"};
   }

@@ -65,6 +65,18 @@ def bench_fine():
               f"{cu*48/1e9:.0f} GB/s algorithmic")
 
 
+def bench_fine_grid(n, batch):
+    """fine RK3 throughput on another grid (c3: 512^2 x 64, c4: 1024^2 x 64)"""
+    f, _ = specs(n)
+    xs = harness.fine_batch_states(n, batch, 7)
+    x = torch.as_tensor(xs).cuda()
+    y = torch.empty_like(x)
+    p = SlicePropagator(f, nsteps=4)
+    t = timeit(lambda: p.apply(x, out=y), reps=5)
+    cu = batch * n * n * 4 / t
+    print(f"fine fused {n}^2 x {batch}: 4 steps {t*1e3:.3f} ms  -> {cu/1e9:.2f} G cell-updates/s")
+
+
 def bench_coarse():
     _, c = specs(512)
     x = torch.as_tensor(harness.initial_state("c3")).cuda()[None, :].contiguous()
@@ -114,6 +126,10 @@ if __name__ == "__main__":
     torch.cuda.set_device(0)
     if what in ("fine", "all"):
         bench_fine()
+    if what in ("fine512", "all"):
+        bench_fine_grid(512, 64)
+    if what in ("fine1024", "all"):
+        bench_fine_grid(1024, 16)
     if what in ("coarse", "all"):
         bench_coarse()
     if what in ("qr", "all"):
