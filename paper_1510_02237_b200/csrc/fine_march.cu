@@ -102,7 +102,8 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
 #pragma unroll
   for (int m = 0; m < 7; ++m)
 #pragma unroll
-    for (int c = 0; c < BX; ++c) A.v[2][c] = fma(C.cxv[m], w[c + 1 + m], A.v[2][c]);
+    for (int c = 0; c < BX; ++c)  // cxv equals cxp off the centre (fewer coefficient loads)
+      A.v[2][c] = fma(m == 3 ? C.cxv[3] : C.cxp[m], w[c + 1 + m], A.v[2][c]);
   {
     double b[BX];
     if constexpr (S > 0) ld_chunks<BX / 2>(b, base_up, woff + 2);
@@ -137,7 +138,8 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
 #pragma unroll
   for (int m = 0; m < 7; ++m)
 #pragma unroll
-    for (int c = 0; c < BX; ++c) A.u[1][c] = fma(C.cxu[m], w[c + 1 + m], A.u[1][c]);
+    for (int c = 0; c < BX; ++c)  // cxu equals cxp at the odd offsets -3, -1, 1, 3
+      A.u[1][c] = fma((m & 1) ? C.cxu[m] : C.cxp[m], w[c + 1 + m], A.u[1][c]);
 #pragma unroll
   for (int c = 0; c < BX; ++c) {
     const double bx = w[c + 5] - w[c + 3];
@@ -152,8 +154,8 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
     for (int c = 0; c < BX; ++c) A.p[1][c] = fma(C.cxp[m], w[c + 1 + m], A.p[1][c]);
 #pragma unroll
   for (int c = 0; c < BX; ++c) {
-    A.u[1][c] = fma(C.pgx, w[c + 5] - w[c + 3], A.u[1][c]);
-    t2[c] = fma(C.pgy, w[c + 4], t2[c]);
+    A.u[1][c] = fma(C.pu, w[c + 5] - w[c + 3], A.u[1][c]);  // pgx == pu
+    t2[c] = fma(C.pv, w[c + 4], t2[c]);  // pgy == pv
     A.v[1][c] += t2[c];
     A.v[3][c] -= t2[c];
   }
@@ -184,16 +186,16 @@ struct Seg {
 // Consume row k and store the completed rows (k-1: u, p; k-2: v) of stage S.
 template <class K, int S>
 __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg, const FusedParams& P,
-                                           int g, int k, int z, const int* woff, int goff0,
-                                           int goff1, bool ghost) {
+                                           int g, int k, int k3, int z, const int* woff,
+                                           int goff0, int goff1, bool ghost) {
   constexpr int BX = K::BX;
   double* qring = sm;
   double* r1 = qring + K::NQ * K::SLOT;
   double* r2 = r1 + K::N1 * K::SLOT;
   const double* in;
   if constexpr (S == 0) in = qring + (size_t)(k & 7) * K::SLOT;
-  else if constexpr (S == 1) in = r1 + (size_t)((k + 30) % 3) * K::SLOT;
-  else in = r2 + (size_t)((k + 30) % 3) * K::SLOT;
+  else if constexpr (S == 1) in = r1 + (size_t)k3 * K::SLOT;
+  else in = r2 + (size_t)k3 * K::SLOT;
   const double* bup = qring + (size_t)((k + 1) & 7) * K::SLOT;
   const double* bv = qring + (size_t)((k + 2) & 7) * K::SLOT;
   // z == 0 but opaque: the 3 stages' 84 coefficients are read from the parameter bank
@@ -201,8 +203,9 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
   consume<K, S>(A, in, bup, bv, woff, P.st[S + z]);
   if constexpr (S < 2) {
     double* out = (S == 0 ? r1 : r2);
-    double* o1 = out + (size_t)((k + 29) % 3) * K::SLOT;
-    double* o2 = out + (size_t)((k + 28) % 3) * K::SLOT;
+    // k3 = k mod 3: rows k-1 and k-2 sit in slots (k3 + 2) mod 3 and (k3 + 1) mod 3
+    double* o1 = out + (size_t)(k3 == 0 ? 2 : k3 - 1) * K::SLOT;
+    double* o2 = out + (size_t)(k3 == 2 ? 0 : k3 + 1) * K::SLOT;
     st_chunks<BX / 2>(o1, woff + 2, A.u[0]);
     st_chunks<BX / 2>(o1 + 2 * K::RW, woff + 2, A.p[0]);
     st_chunks<BX / 2>(o2 + K::RW, woff + 2, A.v[0]);
@@ -317,7 +320,8 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   const int lag = S == 0 ? lag_of(0) : S == 1 ? lag_of(1) : lag_of(2);
   const int lo = S == 0 ? lo_of(0) : S == 1 ? lo_of(1) : lo_of(2);
   const int hi = TY + (S == 0 ? hi_of(0) : S == 1 ? hi_of(1) : hi_of(2));
-  for (int t = 0; t < nt; ++t) {
+  int t3 = 0;  // t mod 3 == k mod 3 (every lag is a multiple of 3)
+  for (int t = 0; t < nt; ++t, t3 = (t3 == 2 ? 0 : t3 + 1)) {
     cp_wait1();
     bar_sync();
     // q row t-4 (needed by stage 1 in tick t+2) into slot (t-4) & 7
@@ -338,9 +342,9 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     const int k = t - lag;
     if (k < lo || k > hi) continue;
     const int z = t & P.zmask;
-    if (S == 0) stage_tick<K, 0>(A, sm, sg, P, g, k, z, woff, goff0, goff1, ghost);
-    else if (S == 1) stage_tick<K, 1>(A, sm, sg, P, g, k, z, woff, goff0, goff1, ghost);
-    else stage_tick<K, 2>(A, sm, sg, P, g, k, z, woff, goff0, goff1, ghost);
+    if (S == 0) stage_tick<K, 0>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
+    else if (S == 1) stage_tick<K, 1>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
+    else stage_tick<K, 2>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
     rotate(A);
   }
 }
