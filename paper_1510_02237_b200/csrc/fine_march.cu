@@ -47,6 +47,7 @@ struct MC {
   static constexpr int MINB = (int)((227 * 1024) / (SMEM + 1024)) < 1 ? 1 : (int)((227 * 1024) / (SMEM + 1024));
   static_assert(G % 32 == 0, "stage groups must be whole warps");
   static_assert(BX == 4 || BX == 8, "BX is 4 or 8");
+  static_assert(NCH >= NT, "copy entries past the row wrap once");
   static_assert(CHR % 4 == 0, "row chunks must be a multiple of the swizzle block");
 };
 
@@ -261,22 +262,18 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   // q-row copy assignment: chunk e = tid + j*NT of the 3 x CHR chunks of a row
   int ld_soff[K::NLD];
   int ld_goff[K::NLD];
-  int nld = 0;
+  // entries past the row (e >= NCH) repeat an earlier chunk: the same bytes to the same
+  // place, so every thread issues NLD copies and the tick loop has no divergent branch
 #pragma unroll
   for (int j = 0; j < K::NLD; ++j) {
-    const int e = tid + j * K::NT;
-    if (e < K::NCH) {
-      const int f = e / K::CHR, c = e - f * K::CHR;
-      int col = 2 * c - 4;
-      col += (col < 0) ? K::NX : 0;
-      col -= (col >= K::NX) ? K::NX : 0;
-      ld_soff[j] = f * K::RW + 2 * swz(c, K::SWZ);
-      ld_goff[j] = f * (int)sg.n + col;
-      nld = j + 1;
-    } else {
-      ld_soff[j] = 0;
-      ld_goff[j] = 0;
-    }
+    int e = tid + j * K::NT;
+    e -= (e >= K::NCH) ? K::NCH : 0;
+    const int f = e / K::CHR, c = e - f * K::CHR;
+    int col = 2 * c - 4;
+    col += (col < 0) ? K::NX : 0;
+    col -= (col >= K::NX) ? K::NX : 0;
+    ld_soff[j] = f * K::RW + 2 * swz(c, K::SWZ);
+    ld_goff[j] = f * (int)sg.n + col;
   }
   // prologue: q rows -6 and -5 (ticks 0 and 1 of stage 1)
   for (int rr = -6; rr <= -5; ++rr) {
@@ -286,10 +283,12 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     const double* rowp = sg.src + (long long)gy * K::NX;
 #pragma unroll
     for (int j = 0; j < K::NLD; ++j)
-      if (j < nld) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+      cp16(slot + ld_soff[j], rowp + ld_goff[j]);
     cp_commit();
   }
-  const int S = tid / K::G;  // warp uniform
+  // warp uniform, and read through a shuffle so the compiler knows it: the stage
+  // coefficients then load into uniform registers (DFMA takes them as operands)
+  const int S = __shfl_sync(0xffffffffu, tid / K::G, 0);
   const int g = tid - S * K::G;
   constexpr int BX = K::BX;
   // this thread's window chunk offsets inside a field row (fixed for the whole march)
@@ -335,13 +334,13 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
         const double* rowp = sg.src + (long long)gy * K::NX;
 #pragma unroll
         for (int j = 0; j < K::NLD; ++j)
-          if (j < nld) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+          cp16(slot + ld_soff[j], rowp + ld_goff[j]);
       }
       cp_commit();
     }
     const int k = t - lag;
     if (k < lo || k > hi) continue;
-    const int z = t & P.zmask;
+    const int z = 0;  // with S provably uniform the coefficients stay in uniform registers
     if (S == 0) stage_tick<K, 0>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
     else if (S == 1) stage_tick<K, 1>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
     else stage_tick<K, 2>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
