@@ -341,6 +341,12 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     const int k = t - lag;
     if (k < lo || k > hi) continue;
     const int z = 0;  // with S provably uniform the coefficients stay in uniform registers
+    // keep the swizzled window offsets in registers (opaque: not recomputed every tick);
+    // measured +2.6% at nx = 256, -4.5% at 512 (no register headroom there)
+    if constexpr (K::NX <= 256) {
+#pragma unroll
+      for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
+    }
     if (S == 0) stage_tick<K, 0>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
     else if (S == 1) stage_tick<K, 1>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
     else stage_tick<K, 2>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
