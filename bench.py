@@ -48,7 +48,7 @@ TRAFFIC_FILE = os.path.join(ROOT, "profiles", "fine_traffic.json")
 
 
 def load_traffic():
-    """DRAM bytes per rk3_fused_kernel launch from the committed ncu --set full capture."""
+    """DRAM bytes per fine-kernel launch (rk3_march_kernel at c2) from the committed ncu --set full capture."""
     if os.path.exists(TRAFFIC_FILE):
         with open(TRAFFIC_FILE) as fh:
             d = json.load(fh)
@@ -445,7 +445,7 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "avg_launch_us": launch_s * 1e6,
-                         "kernel": "rk3_fused_kernel (one launch per RK3 step over all 64 states)",
+                         "kernel": "rk3_march_kernel (row-marching fused RK3; one launch per RK3 step over all 64 states)",
                          "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": (fp64_achieved / fp64_peak) if fp64_peak else None,
                                   "flop_per_cell_update": FLOP_PER_CELL_UPDATE,
