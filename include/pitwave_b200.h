@@ -165,6 +165,14 @@ typedef int (*pw_allgather_hook)(void* user, double* data, long long block, long
 int pw_ctx_set_comm(pw_ctx* ctx, int rank, int world, pw_allreduce_hook allreduce,
                     pw_allgather_hook allgather, void* user);
 int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards);
+/* Row-sharded subspace factorisation (distributed TSQR) for sharded sweeps
+ * (world > 1 or row shards > 1): each shard Householder-factors its row block of the
+ * snapshots, the m x m R factors are all-gathered (allgather hook, block m*m) and factored
+ * once more, and each shard forms its own rows of Q.  Across ranks the projection
+ * alpha = Q^T qk becomes a per-rank partial plus an allreduce of r x n_c doubles.
+ * Replaces src/subspace.py:60-74 (the scipy qr of all snapshots) in that setting.
+ * on = 0 (default; env PW_TSQR) keeps the replicated factorisation. */
+int pw_ctx_set_tsqr(pw_ctx* ctx, int on);
 
 /* ---- memory helper ------------------------------------------------------
  * stream-ordered copy of nbytes between any host/device pointers (UVA,

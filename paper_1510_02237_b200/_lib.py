@@ -85,6 +85,7 @@ SIGNATURES = [
     ("pw_ctx_set_comm", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ALLREDUCE_HOOK, ALLGATHER_HOOK,
                                        c_vp]),
     ("pw_ctx_set_row_shards", ctypes.c_int, [c_vp, ctypes.c_int]),
+    ("pw_ctx_set_tsqr", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
     ("pw_probe_fp64_peak", ctypes.c_int, [c_vp, ctypes.c_int, c_dp]),
@@ -179,6 +180,10 @@ class Context:
         """Run the serial correction as n row shards in this process (tests of the
         multi-GPU arithmetic); 1 restores the single-shard loop."""
         check(self.lib.pw_ctx_set_row_shards(self.handle, int(n)))
+
+    def set_tsqr(self, on: bool):
+        """Factor the subspace by row-sharded TSQR in sharded sweeps."""
+        check(self.lib.pw_ctx_set_tsqr(self.handle, int(bool(on))))
 
     def fp64_peak_tflops(self, iters: int = 4096) -> float:
         """DFMA-throughput probe (TFLOP/s, FMA = 2 flop): the fp64 roofline denominator."""

@@ -236,6 +236,12 @@ struct pw_basis {
   DBuf S, M, W, Q, Y;      // d x cap (S, M, W); d x r (Q, Y)
   DBuf Rs, tau1, tau2, diag, Q2, X, cs_work, lazy_fq, lazy_img, tmp, alpha;
   DBuf R1;                 // unpivoted R of all snapshots (cap x cap)
+  // row-sharded (TSQR) factorisation: per-shard tau, the stacked shard R factors and
+  // their own QR, the small Z = Q_RR [Q2; 0], and per-shard T scratch
+  DBuf tauS, RR, RG, tauRR, Trr, Zq, Tg;
+  bool sweep_tsqr = false;  // set by pw_sweep: factor by TSQR when the context is sharded
+  int tsqr_g0 = 0, tsqr_g1 = 0, tsqr_nsh = 1;
+  long long tsqr_blk = 0;
   DBuf T, wy1, wy2;        // compact-WY T of all reflectors (cap x cap) and two cap x cap temps
   std::vector<char> cs_host;  // cuSOLVER host workspace (X API)
   int v_cols = 0;          // reflectors held in W (explicit unit-lower V); incremental path
@@ -429,6 +435,119 @@ static void factor_append(pw_basis* B, int m_old) {
   B->v_cols = m_old + k;
 }
 
+
+// ---- row-sharded subspace factorisation (distributed TSQR) --------------
+// Shard g owns rows [g blk, (g+1) blk) of S (the serial correction's row blocks).  Each
+// shard factors its row block of S by Householder QR (reflectors left in W's rows), the
+// shards' m x m R factors are stacked (all-gathered across ranks) and factored once more:
+// that R is the R1 of the whole S (unique up to row signs, which the pivoted QR of R1
+// absorbs).  Q = diag(Q_g) Q_RR [Q2; 0] is then formed shard by shard.  Across ranks each
+// rank factors and forms only its own rows; the collectives are one all-gather of m x m
+// doubles per update.  Returns false (caller uses the replicated QR) when the sweep is not
+// sharded, the basis is lean, or a shard has fewer rows than there are snapshots.
+static bool tsqr_applicable(pw_basis* B) {
+  Ctx& c = B->ctx->c;
+  if (!B->sweep_tsqr || !c.tsqr || B->lean) return false;
+  const bool comm = c.comm_world > 1;
+  const int nsh = comm ? c.comm_world : c.vshards;
+  if (nsh <= 1) return false;
+  const long long d = B->dim;
+  const long long blk = ((d + nsh - 1) / nsh + 1) / 2 * 2;
+  if (d - (long long)(nsh - 1) * blk < B->m) return false;
+  B->tsqr_nsh = nsh;
+  B->tsqr_blk = blk;
+  B->tsqr_g0 = comm ? c.comm_rank : 0;
+  B->tsqr_g1 = comm ? c.comm_rank + 1 : nsh;
+  return true;
+}
+
+static void factor_tsqr(pw_basis* B) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const int m = B->m, nsh = B->tsqr_nsh;
+  const long long blk = B->tsqr_blk;
+  const size_t capc = (size_t)B->cap;
+  const long long nm = (long long)nsh * m;  // rows of the stacked R
+  alloc_factor(B);
+  copy_cols(c, B->W.p, d, B->S.p, d, d, m);
+  double* tauS = B->tauS.ensure(c, (size_t)nsh * capc);
+  double* RR = B->RR.ensure(c, (size_t)nsh * capc * capc);
+  double* RG = B->RG.ensure(c, (size_t)nsh * capc * capc);
+  int* info = B->info.ensure(c, 1);
+  for (int g = B->tsqr_g0; g < B->tsqr_g1; ++g) {
+    const long long lo = g * blk, rows = std::min<long long>(d, lo + blk) - lo;
+    PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, m, CUDA_R_64F, B->W.p + lo, d, CUDA_R_64F,
+                               tauS + (size_t)g * capc, CUDA_R_64F, B->cs_work.p,
+                               B->cs_work.n * sizeof(double), B->cs_host.data(), B->cs_host.size(), info));
+    pw::launch_extract_upper(c, B->W.p + lo, d, m, m, RG + (size_t)g * m * m);  // m x m, ld m
+  }
+  mark("tsqr.local");
+  if (c.comm_world > 1)
+    PW_CHECK(c.allgather_hook(c.comm_user, RG, (long long)m * m, (long long)nsh * m * m) == 0, PW_ERR_STATE,
+             "all-gather hook failed (TSQR R factors)");
+  for (int g = 0; g < nsh; ++g)  // stack: RR[g m : (g+1) m, :] = R_g
+    PW_CUDA(cudaMemcpy2DAsync(RR + (size_t)g * m, nm * sizeof(double), RG + (size_t)g * m * m,
+                              m * sizeof(double), m * sizeof(double), m, cudaMemcpyDeviceToDevice, c.stream));
+  double* tauRR = B->tauRR.ensure(c, capc);
+  PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), nm, m, CUDA_R_64F, RR, nm, CUDA_R_64F, tauRR,
+                             CUDA_R_64F, B->cs_work.p, B->cs_work.n * sizeof(double), B->cs_host.data(),
+                             B->cs_host.size(), info));
+  double* tmp = B->Rs.ensure(c, capc * capc);
+  pw::launch_extract_upper(c, RR, nm, m, m, tmp);
+  PW_CUDA(cudaMemcpy2DAsync(B->R1.p, capc * sizeof(double), tmp, m * sizeof(double), m * sizeof(double), m,
+                            cudaMemcpyDeviceToDevice, c.stream));
+  B->v_cols = -1;  // W holds per-shard reflectors: the next update refactors in full
+  mark("tsqr.stack");
+}
+
+// T of the k explicit unit-lower reflectors V (rows x k, ld ldv): T = larft(V^T V, tau)
+static void wy_t(pw_basis* B, const double* V, long long ldv, long long rows, int k, const double* tau,
+                 double* T, int ldt) {
+  Ctx& c = B->ctx->c;
+  double* G = B->wy1.ensure(c, (size_t)B->cap * B->cap);
+  gemm(c, true, false, k, k, rows, 1.0, V, ldv, V, ldv, 0.0, G, k);
+  PW_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * (size_t)ldt * k, c.stream));
+  pw::launch_larft_cols(c, T, ldt, G, tau, 0, k);
+}
+
+// Q rows of the own shards: Q[lo:hi] = Q_g [Z_g; 0] with Z = Q_RR [Q2; 0]
+static void form_q_tsqr(pw_basis* B, const double* Q2, int r, double* Q) {
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const int m = B->m, nsh = B->tsqr_nsh;
+  const long long blk = B->tsqr_blk;
+  const size_t capc = (size_t)B->cap;
+  const long long nm = (long long)nsh * m;
+  double* X1 = B->wy2.ensure(c, capc * capc);
+  double* X2 = B->tmp.ensure(c, capc * capc);
+  // Z = [Q2; 0] - V_RR (T_RR (V_RR[0:m]^T Q2))
+  double* RR = B->RR.p;
+  pw::launch_make_unit_lower(c, RR, nm, 0, m);
+  double* Trr = B->Trr.ensure(c, capc * capc);
+  wy_t(B, RR, nm, nm, m, B->tauRR.p, Trr, m);
+  double* Z = B->Zq.ensure(c, (size_t)nm * capc);
+  gemm(c, true, false, m, r, m, 1.0, RR, nm, Q2, m, 0.0, X1, m);
+  gemm(c, false, false, m, r, m, 1.0, Trr, m, X1, m, 0.0, X2, m);
+  PW_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * (size_t)nm * r, c.stream));
+  copy_cols(c, Z, nm, Q2, m, m, r);
+  gemm(c, false, false, nm, r, m, -1.0, RR, nm, X2, m, 1.0, Z, nm);
+  mark("tsqr.Z");
+  PW_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * (size_t)d * r, c.stream));
+  double* Tg = B->Tg.ensure(c, capc * capc);
+  for (int g = B->tsqr_g0; g < B->tsqr_g1; ++g) {
+    const long long lo = g * blk, rows = std::min<long long>(d, lo + blk) - lo;
+    double* V = B->W.p + lo;
+    pw::launch_make_unit_lower(c, V, d, 0, m);
+    wy_t(B, V, d, rows, m, B->tauS.p + (size_t)g * capc, Tg, m);
+    const double* Zg = Z + (size_t)g * m;
+    gemm(c, true, false, m, r, m, 1.0, V, d, Zg, nm, 0.0, X1, m);
+    gemm(c, false, false, m, r, m, 1.0, Tg, m, X1, m, 0.0, X2, m);
+    copy_cols(c, Q + lo, d, Zg, nm, m, r);
+    gemm(c, false, false, rows, r, m, -1.0, V, d, X2, m, 1.0, Q + lo, d);
+  }
+  mark("tsqr.Q");
+}
+
 // Everything of the refactorisation that depends on the snapshots only: the QR of S, the
 // pivoted QR of R1 and the rank, Q, and the scattered R11^-1 (X).  The sweep runs it on the
 // side stream while the fine propagator runs (the images are not needed until Y).
@@ -447,13 +566,15 @@ void basis_factor(pw_basis* B, int m_old) {
     B->R1.ensure(c, capc * capc);
     PW_CUDA(cudaMemsetAsync(B->R1.p, 0, capc * capc * sizeof(double), c.stream));
   }
-  const bool incremental = m <= d && m_old > 0 && B->v_cols == m_old;
+  const bool tsqr = tsqr_applicable(B);
+  const bool incremental = !tsqr && m <= d && m_old > 0 && B->v_cols == m_old;
   PW_CHECK(!B->lean || incremental || m_old == 0, PW_ERR_STATE,
            "lean subspace cannot be refactored from scratch (snapshots not retained)");
   g_clk = clk.on ? &clk : nullptr;
-  if (incremental) factor_append(B, m_old);
+  if (tsqr) factor_tsqr(B);
+  else if (incremental) factor_append(B, m_old);
   else factor_full(B, mr);
-  clk.mark(incremental ? "append(total)" : "full(total)");
+  clk.mark(tsqr ? "tsqr(total)" : incremental ? "append(total)" : "full(total)");
   // column-pivoted QR of the mr x m factor R1 (same pivots as dgeqp3 on S)
   double* Rs = B->Rs.ensure(c, capc * capc);
   PW_CUDA(cudaMemcpy2DAsync(Rs, mr * sizeof(double), B->R1.p, capc * sizeof(double), mr * sizeof(double),
@@ -474,7 +595,9 @@ void basis_factor(pw_basis* B, int m_old) {
   double* Q2 = B->Q2.ensure(c, capc * capc);
   pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
   double* Q = B->Q.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
-  {
+  if (tsqr) {
+    form_q_tsqr(B, Q2, r, Q);
+  } else {
     const int k = B->v_cols;  // == mr
     double* X1 = B->wy1.ensure(c, capc * capc);
     double* X2 = B->wy2.ensure(c, capc * capc);
@@ -626,6 +749,7 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     if (const char* e = std::getenv("PW_ROW_SHARDS")) ctx->c.vshards = std::atoi(e);
     PW_CUDA(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
     if (const char* e = std::getenv("PW_QR_OVERLAP")) ctx->c.qr_overlap = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PW_TSQR")) ctx->c.tsqr = std::atoi(e) != 0;
     *out = ctx.release();
   });
 }
@@ -666,6 +790,13 @@ int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards) {
   return guarded([&] {
     PW_CHECK(ctx && nshards >= 1, PW_ERR_VALUE, "bad argument");
     ctx->c.vshards = nshards;
+  });
+}
+
+int pw_ctx_set_tsqr(pw_ctx* ctx, int on) {
+  return guarded([&] {
+    PW_CHECK(ctx != nullptr, PW_ERR_VALUE, "bad argument");
+    ctx->c.tsqr = on != 0;
   });
 }
 
@@ -986,6 +1117,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       B.reset(basis_new(ctx, d, rank_tol, n_c * n_it));
       B->diff_mode = true;
       B->coarse = coarse;
+      B->sweep_tsqr = true;
       // lean mode when the d x cap matrices (S, M, W, Q, Y) plus propagator temporaries
       // would not fit next to the sweep buffers (c4 on one GPU: 5 x 25.8 GB)
       size_t free_b = 0, total_b = 0;
@@ -1074,7 +1206,17 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         if (ranks) ranks[k] = r;
         if (r > 0) {
           double* ab = bAlpha.ensure(c, (size_t)std::min<long long>(B->cap, d) * (n_c + 2));
-          gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
+          if (B->v_cols == -1 && c.comm_world > 1) {
+            // row-sharded (TSQR) basis: Q holds this rank's rows only; alpha is their
+            // partial Q_g^T qk_g summed over ranks (Y = M X is complete on every rank)
+            const long long lo = std::min<long long>(d, (long long)c.comm_rank * B->tsqr_blk);
+            const long long hi = std::min<long long>(d, lo + B->tsqr_blk);
+            gemm(c, true, false, r, n_c, hi - lo, 1.0, B->Q.p + lo, d, QK + lo, d, 0.0, ab, r);
+            PW_CHECK(c.allreduce_hook(c.comm_user, ab, (long long)r * n_c) == 0, PW_ERR_STATE,
+                     "allreduce hook failed (TSQR projection)");
+          } else {
+            gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
+          }
           gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           alpha = ab;                             // column 0 = Q^T q0
           alpha_next = ab + (size_t)r * n_c;      // scratch pair after the block

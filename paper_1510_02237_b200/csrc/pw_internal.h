@@ -100,6 +100,7 @@ struct Ctx {
   int coop_blocks_per_sm = 0;        // cap for cooperative G launches (0 = occupancy max)
   cudaStream_t side = nullptr;       // second stream: subspace QR beside the fine sweep
   bool qr_overlap = true;            // PW_QR_OVERLAP=0: QR after the fine sweep, one stream
+  bool tsqr = false;                 // row-sharded (TSQR) subspace factorisation in sharded sweeps
   // row-sharded serial correction: across ranks through the comm hooks (pw_ctx_set_comm),
   // or vshards > 1 row shards in one process (tests, PW_ROW_SHARDS)
   int comm_rank = 0, comm_world = 1, vshards = 1;

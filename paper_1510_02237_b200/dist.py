@@ -9,8 +9,13 @@ The rest of the window -- subspace refactorisation and serial correction
 sweep -- runs replicated on every rank with identical inputs and
 deterministic kernels, so all ranks hold bitwise-identical iterates.
 
-The row-sharded basis of SURVEY.md 8(e) (distributed TSQR, allreduce of the
-r inner products per serial step) is the next step and is not built yet.
+Row-sharded pieces of SURVEY.md 8(e), through the C-ABI comm hooks
+(pw_ctx_set_comm, RowShardComm below): the serial correction streams each
+rank's row block of D and Q with one allreduce of r inner products and one
+all-gather of qn rows per step, and (pw_ctx_set_tsqr) the subspace is factored
+by TSQR: local Householder QR of each rank's rows, one all-gather of the m x m
+R factors, their QR replicated.  ``tsqr`` below is that decomposition on torch
+tensors (the gloo tests check it against the unsharded QR).
 """
 from __future__ import annotations
 
@@ -99,6 +104,28 @@ class RowShardComm:
 
     def allgather(self, ptr: int, block: int, total: int) -> None:
         gather_rows(device_vector(ptr, total, self.device), block, self.group)
+
+
+def tsqr(local: torch.Tensor, group=None):
+    """Row-sharded QR of A = [A_0; A_1; ...] (A_g = ``local`` on rank g, rows_g >= m).
+
+    The decomposition of the device path (csrc/api.cu factor_tsqr / form_q_tsqr):
+    A_g = Q_g R_g locally (Householder), the R_g are all-gathered and stacked,
+    [R_0; R_1; ...] = Q_R R.  Returns (R, this rank's rows of Q = Q_g Q_R[g m:(g+1) m]).
+    R is the R of A up to row signs; pivoted QR of R gives dgeqp3's pivots on A.
+    """
+    m = local.shape[1]
+    if local.shape[0] < m:
+        raise ValueError("TSQR needs at least as many rows per rank as columns")
+    q_loc, r_loc = torch.linalg.qr(local)
+    world = tdist.get_world_size(group) if tdist.is_initialized() else 1
+    rank = tdist.get_rank(group) if tdist.is_initialized() else 0
+    if world == 1:
+        return r_loc, q_loc
+    parts = [torch.empty_like(r_loc) for _ in range(world)]
+    tdist.all_gather(parts, r_loc.contiguous(), group=group)
+    q_r, r = torch.linalg.qr(torch.cat(parts))
+    return r, q_loc @ q_r[rank * m:(rank + 1) * m]
 
 
 def row_block(total: int, block: int, rank: int):

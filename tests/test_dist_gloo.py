@@ -128,3 +128,67 @@ def test_row_sharded_serial_correction_matches_unsharded(world):
     assert len(results) == world
     for _, dq, da in results:
         assert dq <= 1e-13 and da <= 1e-13
+
+
+def _tsqr_worker(rank, world, port, out_q):
+    """Row-sharded TSQR (dist.tsqr, the decomposition of the device factor_tsqr) over gloo
+    against the unsharded factorisation of the whole snapshot matrix."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import scipy.linalg as sla
+
+        from paper_1510_02237_b200.dist import row_block, tsqr
+
+        g = torch.Generator().manual_seed(11)
+        d, m = 997, 24
+        # Parareal-like snapshots: a few near-duplicate and dependent columns
+        a = torch.randn(d, m, generator=g, dtype=torch.float64)
+        a[:, 5] = a[:, 1] + 1e-12 * a[:, 7]
+        a[:, 9] = 2.0 * a[:, 3] - a[:, 4]
+        a[:, 17] = a[:, 2]
+        block = ((d + world - 1) // world + 1) // 2 * 2
+        lo, hi = row_block(d, block, rank)
+        r, q_rows = tsqr(a[lo:hi].contiguous())
+        # this rank's rows of Q, gathered: Q spans what A's QR spans, Q^T Q = I, A = Q R
+        full_q = torch.zeros(d, m, dtype=torch.float64)
+        full_q[lo:hi] = q_rows
+        dist.all_reduce(full_q)
+        recon = float((full_q @ r - a).norm() / a.norm())
+        ortho = float((full_q.T @ full_q - torch.eye(m, dtype=torch.float64)).norm())
+        # R is A's R up to row signs (not unique past a dependent column): R^T R = A^T A
+        gram = a.T @ a
+        rdiff = float((r.T @ r - gram).norm() / gram.norm())
+        # the reference's rank rule on pivoted QR (subspace.py): R of TSQR vs A itself
+        _, rr, piv = sla.qr(r.numpy(), pivoting=True, mode="economic")
+        _, ra, piva = sla.qr(a.numpy(), pivoting=True, mode="economic")
+        tol = 1e-10
+        rank_t = int(np.sum(np.abs(np.diag(rr)) > tol * abs(rr[0, 0])))
+        rank_a = int(np.sum(np.abs(np.diag(ra)) > tol * abs(ra[0, 0])))
+        # kept columns: ties between duplicate columns may pick either copy, so compare the
+        # spans of the kept columns of A
+        qa_t = np.linalg.qr(a.numpy()[:, piv[:rank_t]])[0]
+        qa_a = np.linalg.qr(a.numpy()[:, piva[:rank_a]])[0]
+        same_span = bool(np.linalg.norm(qa_t @ (qa_t.T @ qa_a) - qa_a) <= 1e-10 * np.sqrt(rank_a))
+        out_q.put((rank, recon, ortho, rdiff, rank_t, rank_a, same_span))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tsqr_matches_unsharded_factorisation(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tsqr_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert len(results) == world
+    for _, recon, ortho, rdiff, rank_t, rank_a, same_span in results:
+        assert recon <= 1e-14 and ortho <= 1e-13 and rdiff <= 1e-13
+        assert rank_t == rank_a == 21   # 3 dependent columns dropped by the rank rule
+        assert same_span

@@ -250,6 +250,34 @@ def test_c1_kse_row_sharded_serial_correction(dev, nsh):
     np.testing.assert_allclose(res, g["kse_res"], rtol=1e-10)
 
 
+@pytest.mark.parametrize("nsh", [2, 3])
+def test_c1_kse_tsqr_row_sharded_factorisation(dev, nsh):
+    """Row-sharded subspace factorisation (distributed TSQR) with nsh shards in
+    one process: every shard factors its rows, the stacked R factors are factored once more.
+    Same ranks as the reference and the same window within the parity bound."""
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    g = golden("c1_kse.npz")
+    wl, fine, coarse = c1_props()
+    ends1, res1, sub1 = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    dev.set_row_shards(nsh)
+    dev.set_tsqr(True)
+    try:
+        for k in range(1, wl.n_it + 1):
+            ends, res, sub = kse_sweep(g["q0"], fine, coarse, wl.n_p, k)
+            assert sub.rank == g["kse_ranks"][k - 1]
+            worst = max(rel(ends[i], g["kse_hist"][k - 1][i]) for i in range(wl.n_p))
+            assert worst <= 1e-10, (k, worst)
+            np.testing.assert_allclose(res, g["kse_res"][:k], rtol=1e-10)
+        # the span of Q is the replicated one's (Q Q^T equal), columns may differ in sign
+        qa, qb = sub.q, sub1.q
+        proj = qa @ (qa.T @ qb)
+        assert np.linalg.norm(proj - qb) <= 1e-10 * np.linalg.norm(qb)
+    finally:
+        dev.set_tsqr(False)
+        dev.set_row_shards(1)
+
+
 def test_c1_original_matches_reference():
     from paper_1510_02237_b200.parareal import parareal_sweep
 

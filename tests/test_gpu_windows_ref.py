@@ -72,6 +72,22 @@ def test_c3_window_matches_reference_run():
     check_window("c3", [max(1e-10, 10 * f) for f in C3_FLOOR])
 
 
+def test_c3_window_tsqr_two_row_shards_matches_reference_run():
+    """The c3 window with the row-sharded (TSQR) factorisation and row-sharded serial
+    correction over 2 shards in one process: ranks equal to the reference run, states
+    within the same bound as the replicated path."""
+    from paper_1510_02237_b200 import _lib
+
+    ctx = _lib.Context.get(0)
+    ctx.set_row_shards(2)
+    ctx.set_tsqr(True)
+    try:
+        check_window("c3", [max(1e-10, 10 * f) for f in C3_FLOOR])
+    finally:
+        ctx.set_tsqr(False)
+        ctx.set_row_shards(1)
+
+
 def test_c4_first_iteration_matches_reference_run():
     """c4 iteration 1: ranks equal (142) but the rank gap is tight -- kept min |R_jj|/|R_11|
     1.36e-10 against dropped max 9.45e-11, so cond(R11) ~ 7e9 and eps * cond ~ 1.6e-6.
