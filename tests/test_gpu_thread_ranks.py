@@ -1,0 +1,155 @@
+"""The multi-rank (pw_ctx_set_comm) code paths of pw_sweep, run as host-thread ranks.
+
+Each rank is a Python thread with its own library context, stream and
+propagators on cuda:0.  Its comm hooks exchange device vectors through host
+barriers, summing allreduce partials in rank order.  No kernel waits on another
+rank's kernels: every exchange happens on the host between kernel launches.  So
+this checks the arithmetic and the collective protocol of the row-sharded serial
+correction and of the TSQR factorisation with world > 1. The
+in-process row shards of test_gpu_sweeps.py take a different branch and cannot
+check these. It is a correctness test and says nothing about multi-GPU speed.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_1510_02237_b200 import harness
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+class ThreadComm:
+    """allreduce / all-gather hooks for `world` thread ranks (pw_allreduce_hook semantics)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.bar = threading.Barrier(world, timeout=120)
+        self.slots = [None] * world
+        self.errors = []
+
+    def hooks(self, rank, device):
+        from paper_1510_02237_b200 import _lib
+        from paper_1510_02237_b200.dist import device_vector, row_block
+
+        def allreduce(user, p, count):
+            try:
+                v = device_vector(p, count, device)
+                self.slots[rank] = v.clone()
+                torch.cuda.current_stream(device).synchronize()
+                self.bar.wait()
+                tot = self.slots[0].clone()
+                for r in range(1, self.world):  # rank order: identical sums on every rank
+                    tot += self.slots[r]
+                torch.cuda.current_stream(device).synchronize()
+                self.bar.wait()
+                v.copy_(tot)
+                return 0
+            except Exception as exc:  # noqa: BLE001 - reported by the test
+                self.errors.append(exc)
+                return 1
+
+        def allgather(user, p, block, total):
+            try:
+                v = device_vector(p, total, device)
+                lo, hi = row_block(total, block, rank)
+                self.slots[rank] = v[lo:hi].clone()
+                torch.cuda.current_stream(device).synchronize()
+                self.bar.wait()
+                for r in range(self.world):
+                    rlo, rhi = row_block(total, block, r)
+                    if rhi > rlo:
+                        v[rlo:rhi].copy_(self.slots[r])
+                torch.cuda.current_stream(device).synchronize()
+                self.bar.wait()
+                return 0
+            except Exception as exc:  # noqa: BLE001
+                self.errors.append(exc)
+                return 1
+
+        return _lib.ALLREDUCE_HOOK(allreduce), _lib.ALLGATHER_HOOK(allgather)
+
+
+def c1_props():
+    from paper_1510_02237_b200.integrators import RK3, SPLIT_FE_FB, SlicePropagator, make_propagator
+    from paper_1510_02237_b200.mesh import ACOUSTIC, ConstantVelocity, build_grid
+    from paper_1510_02237_b200.physics import ModelSpec
+
+    wl = harness.WORKLOADS["c1"]
+    g = build_grid(wl.n, wl.n)
+    vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
+    fine = make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), g, 0.5)
+    coarse = make_propagator(SPLIT_FE_FB, ModelSpec(ACOUSTIC, vel, 1, 1.0, 0.1, 1.0), g, 4.0, 16)
+    return wl, SlicePropagator(fine, wl.slice_span), SlicePropagator(coarse, wl.slice_span)
+
+
+_build_lock = threading.Lock()
+
+
+def rank_main(rank, world, comm, tsqr, q0, results):
+    from paper_1510_02237_b200 import _lib
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    device = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device)
+    try:
+        with torch.cuda.stream(stream):
+            ctx = _lib.Context(0)  # this rank's own context on this thread's stream
+            with _build_lock:      # propagators of this context (Context.get returns it meanwhile)
+                saved = _lib.Context._instances.get(0)
+                _lib.Context._instances[0] = ctx
+                try:
+                    wl, fine, coarse = c1_props()
+                finally:
+                    if saved is None:
+                        _lib.Context._instances.pop(0, None)
+                    else:
+                        _lib.Context._instances[0] = saved
+            ar, ag = comm.hooks(rank, device)
+            _lib.check(ctx.lib.pw_ctx_set_comm(ctx.handle, rank, world, ar, ag, None))
+            ctx.set_tsqr(tsqr)
+            out = []
+            for k in range(1, wl.n_it + 1):
+                ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, k)
+                out.append((np.array(ends), list(res), sub.rank))
+            results[rank] = out
+            ctx.lib.pw_ctx_set_comm(ctx.handle, 0, 1, _lib.ALLREDUCE_HOOK(), _lib.ALLGATHER_HOOK(), None)
+            del fine, coarse, sub
+    except Exception as exc:  # noqa: BLE001
+        results[rank] = exc
+        comm.bar.abort()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("tsqr", [False, True])
+def test_thread_ranks_c1_window_matches_reference(world, tsqr):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    g = golden("c1_kse.npz")
+    comm = ThreadComm(world)
+    results = [None] * world
+    threads = [threading.Thread(target=rank_main, args=(r, world, comm, tsqr, g["q0"], results))
+               for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not comm.errors, comm.errors
+    for r in range(world):
+        assert not isinstance(results[r], Exception), results[r]
+        assert results[r] is not None
+    n_it = len(results[0])
+    for k in range(n_it):
+        ends0 = results[0][k][0]
+        for r in range(world):
+            ends, res, rank = results[r][k]
+            assert rank == g["kse_ranks"][k]
+            # every rank holds the same iterates (rows gathered, identical rank-order sums)
+            np.testing.assert_array_equal(ends, ends0)
+            worst = max(np.linalg.norm(ends[i] - g["kse_hist"][k][i]) / np.linalg.norm(g["kse_hist"][k][i])
+                        for i in range(ends.shape[0]))
+            assert worst <= 1e-10, (r, k, worst)
+            np.testing.assert_allclose(res, g["kse_res"][:k + 1], rtol=1e-10)
