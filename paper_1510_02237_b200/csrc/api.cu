@@ -240,6 +240,10 @@ struct pw_basis {
   // their own QR, the small Z = Q_RR [Q2; 0], and per-shard T scratch
   DBuf tauS, RR, RG, tauRR, Trr, Zq, Tg;
   bool sweep_tsqr = false;  // set by pw_sweep: factor by TSQR when the context is sharded
+  // row-local storage (multi-rank TSQR sweeps): the basis holds only this rank's rows
+  // [row_lo, row_lo + dim) of the global_dim-row snapshots, images, Q and Y
+  bool local_rows = false;
+  long long row_lo = 0, global_dim = 0;
   int tsqr_g0 = 0, tsqr_g1 = 0, tsqr_nsh = 1;
   long long tsqr_blk = 0;
   DBuf T, wy1, wy2;        // compact-WY T of all reflectors (cap x cap) and two cap x cap temps
@@ -451,9 +455,15 @@ static bool tsqr_applicable(pw_basis* B) {
   const bool comm = c.comm_world > 1;
   const int nsh = comm ? c.comm_world : c.vshards;
   if (nsh <= 1) return false;
-  const long long d = B->dim;
+  const long long d = B->local_rows ? B->global_dim : B->dim;
   const long long blk = ((d + nsh - 1) / nsh + 1) / 2 * 2;
-  if (d - (long long)(nsh - 1) * blk < B->m) return false;
+  if (d - (long long)(nsh - 1) * blk < B->m) {
+    // the same test on every rank: a row-local basis has no replicated fallback
+    PW_CHECK(!B->local_rows, PW_ERR_STATE,
+             "row-sharded subspace: the smallest row block has fewer rows than the " +
+                 std::to_string(B->m) + " snapshots");
+    return false;
+  }
   B->tsqr_nsh = nsh;
   B->tsqr_blk = blk;
   B->tsqr_g0 = comm ? c.comm_rank : 0;
@@ -461,11 +471,21 @@ static bool tsqr_applicable(pw_basis* B) {
   return true;
 }
 
+// storage rows of shard g: its block of the replicated arrays, or all rows of a row-local basis
+static void tsqr_rows(const pw_basis* B, int g, long long& lo, long long& rows) {
+  if (B->local_rows) {
+    lo = 0;
+    rows = B->dim;
+    return;
+  }
+  lo = g * B->tsqr_blk;
+  rows = std::min<long long>(B->dim, lo + B->tsqr_blk) - lo;
+}
+
 static void factor_tsqr(pw_basis* B) {
   Ctx& c = B->ctx->c;
   const long long d = B->dim;
   const int m = B->m, nsh = B->tsqr_nsh;
-  const long long blk = B->tsqr_blk;
   const size_t capc = (size_t)B->cap;
   const long long nm = (long long)nsh * m;  // rows of the stacked R
   alloc_factor(B);
@@ -475,7 +495,8 @@ static void factor_tsqr(pw_basis* B) {
   double* RG = B->RG.ensure(c, (size_t)nsh * capc * capc);
   int* info = B->info.ensure(c, 1);
   for (int g = B->tsqr_g0; g < B->tsqr_g1; ++g) {
-    const long long lo = g * blk, rows = std::min<long long>(d, lo + blk) - lo;
+    long long lo, rows;
+    tsqr_rows(B, g, lo, rows);
     PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, m, CUDA_R_64F, B->W.p + lo, d, CUDA_R_64F,
                                tauS + (size_t)g * capc, CUDA_R_64F, B->cs_work.p,
                                B->cs_work.n * sizeof(double), B->cs_host.data(), B->cs_host.size(), info));
@@ -515,7 +536,6 @@ static void form_q_tsqr(pw_basis* B, const double* Q2, int r, double* Q) {
   Ctx& c = B->ctx->c;
   const long long d = B->dim;
   const int m = B->m, nsh = B->tsqr_nsh;
-  const long long blk = B->tsqr_blk;
   const size_t capc = (size_t)B->cap;
   const long long nm = (long long)nsh * m;
   double* X1 = B->wy2.ensure(c, capc * capc);
@@ -535,7 +555,8 @@ static void form_q_tsqr(pw_basis* B, const double* Q2, int r, double* Q) {
   PW_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * (size_t)d * r, c.stream));
   double* Tg = B->Tg.ensure(c, capc * capc);
   for (int g = B->tsqr_g0; g < B->tsqr_g1; ++g) {
-    const long long lo = g * blk, rows = std::min<long long>(d, lo + blk) - lo;
+    long long lo, rows;
+    tsqr_rows(B, g, lo, rows);
     double* V = B->W.p + lo;
     pw::launch_make_unit_lower(c, V, d, 0, m);
     wy_t(B, V, d, rows, m, B->tauS.p + (size_t)g * capc, Tg, m);
@@ -1114,10 +1135,22 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     double* scr = bScr.ensure(c, pw::residual_scratch_doubles(n_c, d));
     std::unique_ptr<pw_basis> B;
     if (kse) {
-      B.reset(basis_new(ctx, d, rank_tol, n_c * n_it));
+      // multi-rank TSQR sweeps keep only this rank's rows of the basis (memory / world)
+      const bool local = c.comm_world > 1 && c.tsqr;
+      long long lo = 0, nrow = d;
+      if (local) {
+        const long long blk = ((d + c.comm_world - 1) / c.comm_world + 1) / 2 * 2;
+        lo = std::min<long long>(d, (long long)c.comm_rank * blk);
+        nrow = std::min<long long>(d, lo + blk) - lo;
+        PW_CHECK(nrow >= 1, PW_ERR_VALUE, "row-sharded subspace: this rank has no rows");
+      }
+      B.reset(basis_new(ctx, nrow, rank_tol, n_c * n_it));
       B->diff_mode = true;
       B->coarse = coarse;
       B->sweep_tsqr = true;
+      B->local_rows = local;
+      B->row_lo = lo;
+      B->global_dim = d;
       // lean mode when the d x cap matrices (S, M, W, Q, Y) plus propagator temporaries
       // would not fit next to the sweep buffers (c4 on one GPU: 5 x 25.8 GB)
       size_t free_b = 0, total_b = 0;
@@ -1130,14 +1163,14 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         PW_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
         if (reserved > used) free_b += (size_t)(reserved - used);
       }
-      const double col = 8.0 * (double)d;
-      const double need = col * std::min<long long>(B->cap, d) * 5.0 + col * n_c * 3.0 +
+      const double col = 8.0 * (double)d, bcol = 8.0 * (double)B->dim;
+      const double need = bcol * std::min<long long>(B->cap, B->dim) * 5.0 + col * n_c * 3.0 +
                           std::max(4.0 * (1ull << 30), 0.06 * (double)total_b);
       const char* e = getenv("PW_SWEEP_LEAN");
-      B->lean = (e && *e == '1') || need > (double)free_b;
+      B->lean = !B->local_rows && ((e && *e == '1') || need > (double)free_b);
       // even lean (4 d x cap matrices) must fit, or fail now instead of after the first fine
       // sweep (c5 on one GPU: 4 x 96 GiB; it needs the row-sharded basis of SURVEY 8(e))
-      const double need_lean = need - col * std::min<long long>(B->cap, d);
+      const double need_lean = need - (B->local_rows ? 0.0 : bcol * std::min<long long>(B->cap, B->dim));
       PW_CHECK(need_lean <= (double)free_b, PW_ERR_MEMORY,
                "KSE sweep needs ~" + std::to_string((long long)(need_lean / (1 << 30))) +
                    " GiB for its d x " + std::to_string(B->cap) + " basis even without a snapshot copy; " +
@@ -1189,7 +1222,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       if (kse) {
         StreamScope side(c, c.qr_overlap ? c.side : c.stream);
         PW_CUDA(cudaStreamWaitEvent(c.stream, sync.snap, 0));
-        basis_append_snapshots(B.get(), QK, d, n_c);
+        basis_append_snapshots(B.get(), QK + B->row_lo, d, n_c);
         basis_factor(B.get(), m_old);  // blocks the host at the rank read; the fine sweep runs on
         PW_CUDA(cudaEventRecord(sync.fact, c.stream));
       }
@@ -1199,25 +1232,26 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       double* alpha = nullptr;
       double* alpha_next = nullptr;
       if (kse) {
-        basis_append_images(B.get(), m_old, PRED, d, n_c);
+        basis_append_images(B.get(), m_old, PRED + B->row_lo, d, n_c);
         PW_CUDA(cudaStreamWaitEvent(c.stream, sync.fact, 0));
         basis_images_gemm(B.get());
         r = B->r;
         if (ranks) ranks[k] = r;
         if (r > 0) {
           double* ab = bAlpha.ensure(c, (size_t)std::min<long long>(B->cap, d) * (n_c + 2));
-          if (B->v_cols == -1 && c.comm_world > 1) {
-            // row-sharded (TSQR) basis: Q holds this rank's rows only; alpha is their
-            // partial Q_g^T qk_g summed over ranks (Y = M X is complete on every rank)
-            const long long lo = std::min<long long>(d, (long long)c.comm_rank * B->tsqr_blk);
-            const long long hi = std::min<long long>(d, lo + B->tsqr_blk);
-            gemm(c, true, false, r, n_c, hi - lo, 1.0, B->Q.p + lo, d, QK + lo, d, 0.0, ab, r);
+          if (B->local_rows) {
+            // row-local (TSQR) basis: Q and Y hold this rank's rows; alpha is the sum over
+            // ranks of Q_g^T qk_g, and only this rank's rows of c_i are corrected (the serial
+            // correction reads no others)
+            const long long lo = B->row_lo, nr = B->dim;
+            gemm(c, true, false, r, n_c, nr, 1.0, B->Q.p, nr, QK + lo, d, 0.0, ab, r);
             PW_CHECK(c.allreduce_hook(c.comm_user, ab, (long long)r * n_c) == 0, PW_ERR_STATE,
                      "allreduce hook failed (TSQR projection)");
+            gemm(c, false, false, nr, n_c, r, -1.0, B->Y.p, nr, ab, r, 1.0, PRED + lo, d);
           } else {
             gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
+            gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           }
-          gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           alpha = ab;                             // column 0 = Q^T q0
           alpha_next = ab + (size_t)r * n_c;      // scratch pair after the block
         }
@@ -1261,9 +1295,11 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
               PW_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * r, c.stream));
               continue;
             }
-            pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d + lo, B->Y.p + lo, r,
-                                    PRED + (size_t)i * d + lo, a_cur, B->Q.p + lo, r, hi - lo,
-                                    QN + (size_t)(i + 1) * d + lo, dst, part, 0, d);
+            // row-local basis: this rank's rows start at row 0 of Y and Q (ld = their rows)
+            const long long boff = B->local_rows ? 0 : lo, bld = B->local_rows ? B->dim : d;
+            pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d + lo, B->Y.p + boff, r,
+                                    PRED + (size_t)i * d + lo, a_cur, B->Q.p + boff, r, hi - lo,
+                                    QN + (size_t)(i + 1) * d + lo, dst, part, 0, bld);
           }
           if (comm) {
             PW_CHECK(c.allreduce_hook(c.comm_user, a_nxt, r) == 0, PW_ERR_STATE, "allreduce hook failed");
