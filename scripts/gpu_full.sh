@@ -10,5 +10,5 @@ echo "bench rc=$?" >> gpurun_out/bench_full.log
 if [ "${PROF:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 1 --no-parareal --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
   timeout 300 python scripts/prof_target.py fine > gpurun_out/plain_fine.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:rk3_fused -c 1 -o gpurun_out/fine_v6 python scripts/prof_target.py fine > gpurun_out/ncu_fine.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:rk3_march -s 1 -c 1 -o gpurun_out/fine_march python scripts/prof_target.py fine > gpurun_out/ncu_fine.log 2>&1
 fi
