@@ -92,10 +92,14 @@ struct Acc {
 
 // Consume input row `in` (3 field rows, RW apart).  base_up / base_v: q rows k+1 and
 // k+2 (S > 0; the births of rows k+1 (u, p) and k+2 (v) start from q there).
-template <class K, int S>
+template <class K, int S, int PH>
 __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const double* base_up,
                                         const double* base_v, const int* woff, const StageCoef& C) {
   constexpr int BX = K::BX;
+  // u, p of rows k-1, k, k+1 in slots (PH+2)%3, PH, (PH+1)%3 (PH = k mod 3, compile time),
+  // or in slots 0, 1, 2 shifted after every row (PH = 3); v of rows k-2 .. k+2 in v[0..4]
+  // (shifted after every row)
+  constexpr int U0 = PH == 3 ? 0 : (PH + 2) % 3, U1 = PH == 3 ? 1 : PH, U2 = PH == 3 ? 2 : (PH + 1) % 3;
   double w[K::WN];
   // ---- v: x stencil of row k; v_x (mixed damping of u) and v itself (p's v_y, v_yy)
   //      go to rows k+-1 / k+-2; births of rows k+1 (u, p) and k+2 (v)
@@ -111,8 +115,8 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
 #pragma unroll
     for (int c = 0; c < BX; ++c) {
       const double t1 = C.cuv * (w[c + 5] - w[c + 3]);
-      A.u[0][c] += t1;
-      A.u[2][c] = (S > 0) ? b[c] - t1 : -t1;
+      A.u[U0][c] += t1;
+      A.u[U2][c] = (S > 0) ? b[c] - t1 : -t1;
     }
   }
   {
@@ -120,8 +124,8 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
     if constexpr (S > 0) ld_chunks<BX / 2>(b, base_up + 2 * K::RW, woff + 2);
 #pragma unroll
     for (int c = 0; c < BX; ++c) {
-      A.p[0][c] = fma(C.pv, w[c + 4], A.p[0][c]);
-      A.p[2][c] = (S > 0) ? fma(-C.pv, w[c + 4], b[c]) : -C.pv * w[c + 4];
+      A.p[U0][c] = fma(C.pv, w[c + 4], A.p[U0][c]);
+      A.p[U2][c] = (S > 0) ? fma(-C.pv, w[c + 4], b[c]) : -C.pv * w[c + 4];
     }
   }
   {
@@ -140,11 +144,11 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
   for (int m = 0; m < 7; ++m)
 #pragma unroll
     for (int c = 0; c < BX; ++c)  // cxu equals cxp at the odd offsets -3, -1, 1, 3
-      A.u[1][c] = fma((m & 1) ? C.cxu[m] : C.cxp[m], w[c + 1 + m], A.u[1][c]);
+      A.u[U1][c] = fma((m & 1) ? C.cxu[m] : C.cxp[m], w[c + 1 + m], A.u[U1][c]);
 #pragma unroll
   for (int c = 0; c < BX; ++c) {
     const double bx = w[c + 5] - w[c + 3];
-    A.p[1][c] = fma(C.pu, bx, A.p[1][c]);
+    A.p[U1][c] = fma(C.pu, bx, A.p[U1][c]);
     t2[c] = C.cvu * bx;
   }
   // ---- p: x stencil of row k, p_x for u(k), p_y for v(k+-1)
@@ -152,10 +156,10 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
 #pragma unroll
   for (int m = 0; m < 7; ++m)
 #pragma unroll
-    for (int c = 0; c < BX; ++c) A.p[1][c] = fma(C.cxp[m], w[c + 1 + m], A.p[1][c]);
+    for (int c = 0; c < BX; ++c) A.p[U1][c] = fma(C.cxp[m], w[c + 1 + m], A.p[U1][c]);
 #pragma unroll
   for (int c = 0; c < BX; ++c) {
-    A.u[1][c] = fma(C.pu, w[c + 5] - w[c + 3], A.u[1][c]);  // pgx == pu
+    A.u[U1][c] = fma(C.pu, w[c + 5] - w[c + 3], A.u[U1][c]);  // pgx == pu
     t2[c] = fma(C.pv, w[c + 4], t2[c]);  // pgy == pv
     A.v[1][c] += t2[c];
     A.v[3][c] -= t2[c];
@@ -163,13 +167,20 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
 }
 
 template <class K>
-__device__ __forceinline__ void rotate(Acc<K>& A) {
+__device__ __forceinline__ void rotate_up(Acc<K>& A) {
 #pragma unroll
   for (int c = 0; c < K::BX; ++c) {
     A.u[0][c] = A.u[1][c];
     A.u[1][c] = A.u[2][c];
     A.p[0][c] = A.p[1][c];
     A.p[1][c] = A.p[2][c];
+  }
+}
+
+template <class K>
+__device__ __forceinline__ void rotate_v(Acc<K>& A) {
+#pragma unroll
+  for (int c = 0; c < K::BX; ++c) {
     A.v[0][c] = A.v[1][c];
     A.v[1][c] = A.v[2][c];
     A.v[2][c] = A.v[3][c];
@@ -185,10 +196,13 @@ struct Seg {
 };
 
 // Consume row k and store the completed rows (k-1: u, p; k-2: v) of stage S.
-template <class K, int S>
+template <class K, int S, int PH>
 __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg, const FusedParams& P,
-                                           int g, int k, int k3, int z, const int* woff,
-                                           int goff0, int goff1, bool ghost) {
+                                           int g, int k, int z, const int* woff, int goff0, int goff1,
+                                           bool ghost, int k3_rt = 0) {
+  // ring slot of row k: k mod 3 (compile time, or k3_rt in the rotating mode PH = 3)
+  const int k3 = PH == 3 ? k3_rt : PH;
+  constexpr int U0 = PH == 3 ? 0 : (PH + 2) % 3;
   constexpr int BX = K::BX;
   double* qring = sm;
   double* r1 = qring + K::NQ * K::SLOT;
@@ -201,14 +215,14 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
   const double* bv = qring + (size_t)((k + 2) & 7) * K::SLOT;
   // z == 0 but opaque: the 3 stages' 84 coefficients are read from the parameter bank
   // inside the tick (uniform registers) instead of being hoisted out of the loop
-  consume<K, S>(A, in, bup, bv, woff, P.st[S + z]);
+  consume<K, S, PH>(A, in, bup, bv, woff, P.st[S + z]);
   if constexpr (S < 2) {
     double* out = (S == 0 ? r1 : r2);
     // k3 = k mod 3: rows k-1 and k-2 sit in slots (k3 + 2) mod 3 and (k3 + 1) mod 3
     double* o1 = out + (size_t)(k3 == 0 ? 2 : k3 - 1) * K::SLOT;
     double* o2 = out + (size_t)(k3 == 2 ? 0 : k3 + 1) * K::SLOT;
-    st_chunks<BX / 2>(o1, woff + 2, A.u[0]);
-    st_chunks<BX / 2>(o1 + 2 * K::RW, woff + 2, A.p[0]);
+    st_chunks<BX / 2>(o1, woff + 2, A.u[U0]);
+    st_chunks<BX / 2>(o1 + 2 * K::RW, woff + 2, A.p[U0]);
     st_chunks<BX / 2>(o2 + K::RW, woff + 2, A.v[0]);
     if (ghost) {
       // mirrored columns: the first 4 of thread 0's block, the last 4 of the last thread's
@@ -216,8 +230,8 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
       double gu[4], gp[4], gv[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        gu[j] = first ? A.u[0][j] : A.u[0][BX - 4 + j];
-        gp[j] = first ? A.p[0][j] : A.p[0][BX - 4 + j];
+        gu[j] = first ? A.u[U0][j] : A.u[U0][BX - 4 + j];
+        gp[j] = first ? A.p[U0][j] : A.p[U0][BX - 4 + j];
         gv[j] = first ? A.v[0][j] : A.v[0][BX - 4 + j];
       }
       *reinterpret_cast<double2*>(o1 + goff0) = make_double2(gu[0], gu[1]);
@@ -233,8 +247,8 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
       double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NX + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) {
-        *reinterpret_cast<double2*>(o + c) = make_double2(A.u[0][c], A.u[0][c + 1]);
-        *reinterpret_cast<double2*>(o + 2 * sg.n + c) = make_double2(A.p[0][c], A.p[0][c + 1]);
+        *reinterpret_cast<double2*>(o + c) = make_double2(A.u[U0][c], A.u[U0][c + 1]);
+        *reinterpret_cast<double2*>(o + 2 * sg.n + c) = make_double2(A.p[U0][c], A.p[U0][c + 1]);
       }
     }
     if (k - 2 >= 0 && k - 2 < sg.TY) {
@@ -242,6 +256,63 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
 #pragma unroll
       for (int c = 0; c < BX; c += 2) *reinterpret_cast<double2*>(o + c) = make_double2(A.v[0][c], A.v[0][c + 1]);
     }
+  }
+}
+
+// One tick of stage S: the CTA barrier, the q-row load two ticks ahead, then row
+// k = t - lag.  I = t mod 3 = k mod 3 (the lags are multiples of 3) is a compile-time
+// constant, so the u/p accumulator slots and the s-ring slots are too.
+template <class K, int S, int I>
+__device__ __forceinline__ void tick(Acc<K>& A, double* sm, const Seg& sg, const FusedParams& P, int g,
+                                     int t, const int* ld_soff, const int* ld_goff, int* woff,
+                                     int goff0, int goff1, bool ghost) {
+  const int TY = sg.TY;
+  cp_wait1();
+  bar_sync();
+  {
+    const int rr = t - 4;  // q row needed by stage 1 in tick t+2, into slot rr & 7
+    if (rr <= TY + 5) {
+      int gy = sg.y0 + rr;
+      gy += (gy < 0) ? sg.ny : 0;
+      gy -= (gy >= sg.ny) ? sg.ny : 0;
+      double* slot = sm + (size_t)(rr & 7) * K::SLOT;
+      const double* rowp = sg.src + (long long)gy * K::NX;
+#pragma unroll
+      for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+    }
+    cp_commit();
+  }
+  const int k = t - lag_of(S);
+  if (k < lo_of(S) || k > TY + hi_of(S)) return;
+  // keep the swizzled window offsets in registers (opaque: not recomputed every tick)
+  if constexpr (K::NX <= 256) {
+#pragma unroll
+    for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
+  }
+  // z = t & zmask = 0, opaque: the stage's coefficients load inside the tick (uniform
+  // registers) instead of 28 doubles being hoisted out of the loop
+  stage_tick<K, S, I>(A, sm, sg, P, g, k, t & P.zmask, woff, goff0, goff1, ghost);
+  rotate_v(A);
+}
+
+template <class K, int S>
+__device__ __forceinline__ void stage_loop(double* sm, const Seg& sg, const FusedParams& P, int g,
+                                           const int* ld_soff, const int* ld_goff, int* woff,
+                                           int goff0, int goff1, bool ghost) {
+  Acc<K> A;
+#pragma unroll
+  for (int c = 0; c < K::BX; ++c) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) A.u[r][c] = A.p[r][c] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) A.v[r][c] = 0.0;
+  }
+  // tick count rounded up to the unroll (the same for every warp: equal barrier counts)
+  const int nt = (sg.TY + 14 + 2) / 3 * 3;
+  for (int t = 0; t < nt; t += 3) {
+    tick<K, S, 0>(A, sm, sg, P, g, t, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    tick<K, S, 1>(A, sm, sg, P, g, t + 1, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    tick<K, S, 2>(A, sm, sg, P, g, t + 2, ld_soff, ld_goff, woff, goff0, goff1, ghost);
   }
 }
 
@@ -306,51 +377,54 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     goff1 = 2 * swz(1, K::SWZ);
   }
   const bool ghost = (g == 0) || (g == K::G - 1);
-  Acc<K> A;
+  if constexpr (K::G >= 128) {  // four warps per stage group: per-stage loops, unrolled 3x
+    if (S == 0) stage_loop<K, 0>(sm, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    else if (S == 1) stage_loop<K, 1>(sm, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    else stage_loop<K, 2>(sm, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+  } else {  // two CTAs of 6 warps per SM: one loop, the stage branch inside (measured faster)
+    Acc<K> A;
 #pragma unroll
-  for (int c = 0; c < BX; ++c) {
+    for (int c = 0; c < BX; ++c) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) A.u[r][c] = A.p[r][c] = 0.0;
+      for (int r = 0; r < 3; ++r) A.u[r][c] = A.p[r][c] = 0.0;
 #pragma unroll
-    for (int r = 0; r < 5; ++r) A.v[r][c] = 0.0;
-  }
-  const int TY = sg.TY;
-  const int nt = TY + 14;
-  const int lag = S == 0 ? lag_of(0) : S == 1 ? lag_of(1) : lag_of(2);
-  const int lo = S == 0 ? lo_of(0) : S == 1 ? lo_of(1) : lo_of(2);
-  const int hi = TY + (S == 0 ? hi_of(0) : S == 1 ? hi_of(1) : hi_of(2));
-  int t3 = 0;  // t mod 3 == k mod 3 (every lag is a multiple of 3)
-  for (int t = 0; t < nt; ++t, t3 = (t3 == 2 ? 0 : t3 + 1)) {
-    cp_wait1();
-    bar_sync();
-    // q row t-4 (needed by stage 1 in tick t+2) into slot (t-4) & 7
-    {
-      const int rr = t - 4;
-      if (rr <= TY + 5) {
-        int gy = sg.y0 + rr;
-        gy += (gy < 0) ? ny : 0;
-        gy -= (gy >= ny) ? ny : 0;
-        double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-        const double* rowp = sg.src + (long long)gy * K::NX;
-#pragma unroll
-        for (int j = 0; j < K::NLD; ++j)
-          cp16(slot + ld_soff[j], rowp + ld_goff[j]);
-      }
-      cp_commit();
+      for (int r = 0; r < 5; ++r) A.v[r][c] = 0.0;
     }
-    const int k = t - lag;
-    if (k < lo || k > hi) continue;
-    const int z = 0;  // with S provably uniform the coefficients stay in uniform registers
-    // keep the swizzled window offsets in registers (opaque: not recomputed every tick);
-    // measured +2.6% at nx = 256, -4.5% at 512 (no register headroom there)
-    if constexpr (K::NX <= 256) {
+    const int TY = sg.TY;
+    const int nt = TY + 14;
+    const int lag = S == 0 ? lag_of(0) : S == 1 ? lag_of(1) : lag_of(2);
+    const int lo = S == 0 ? lo_of(0) : S == 1 ? lo_of(1) : lo_of(2);
+    const int hi = TY + (S == 0 ? hi_of(0) : S == 1 ? hi_of(1) : hi_of(2));
+    int t3 = 0;  // t mod 3 == k mod 3 (every lag is a multiple of 3)
+    for (int t = 0; t < nt; ++t, t3 = (t3 == 2 ? 0 : t3 + 1)) {
+      cp_wait1();
+      bar_sync();
+      {  // q row t-4 (needed by stage 1 in tick t+2) into slot (t-4) & 7
+        const int rr = t - 4;
+        if (rr <= TY + 5) {
+          int gy = sg.y0 + rr;
+          gy += (gy < 0) ? ny : 0;
+          gy -= (gy >= ny) ? ny : 0;
+          double* slot = sm + (size_t)(rr & 7) * K::SLOT;
+          const double* rowp = sg.src + (long long)gy * K::NX;
+#pragma unroll
+          for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+        }
+        cp_commit();
+      }
+      const int k = t - lag;
+      if (k < lo || k > hi) continue;
+      // keep the swizzled window offsets in registers (opaque: not recomputed every tick);
+      // measured +2.6% at nx = 256
 #pragma unroll
       for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
+      // S is provably uniform: the coefficients stay in uniform registers (z = 0)
+      if (S == 0) stage_tick<K, 0, 3>(A, sm, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
+      else if (S == 1) stage_tick<K, 1, 3>(A, sm, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
+      else stage_tick<K, 2, 3>(A, sm, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
+      rotate_up(A);
+      rotate_v(A);
     }
-    if (S == 0) stage_tick<K, 0>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
-    else if (S == 1) stage_tick<K, 1>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
-    else stage_tick<K, 2>(A, sm, sg, P, g, k, t3, z, woff, goff0, goff1, ghost);
-    rotate(A);
   }
 }
 
