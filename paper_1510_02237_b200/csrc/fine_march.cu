@@ -24,26 +24,32 @@
 //
 // Shared-memory rows are chunk-swizzled (chunk c at c ^ ((c >> 3) & (BX/2-1)))
 // so the BX/2-chunk thread stride of the window loads is conflict free.
+#include <type_traits>
+
 #include "pw_internal.h"
 
 namespace pw {
 namespace {
 
-template <int NX_, int BX_>
+template <int NX_, int BX_, int NS_ = 1>
 struct MC {
-  static constexpr int NX = NX_, BX = BX_;
-  static constexpr int G = NX / BX;    // threads per stage group
+  static constexpr int NX = NX_, BX = BX_, NS = NS_;  // NS states side by side per CTA
+  static constexpr int GS = NX / BX;   // threads per state row
+  static constexpr int G = NS * GS;    // threads per stage group
   static constexpr int NT = 3 * G;
   static constexpr int RW = NX + 8;    // doubles per ring field row: cols [-4, NX+4)
   static constexpr int CHR = RW / 2;   // 16-byte chunks per field row
-  static constexpr int SLOT = 3 * RW;  // doubles per ring slot (u, v, p)
+  static constexpr int SROW = 3 * RW;  // one state's row (u, v, p)
+  static constexpr int SLOT = NS * SROW;  // doubles per ring slot
   static constexpr int NQ = 8, N1 = 3, N2 = 3;
   static constexpr size_t SMEM = sizeof(double) * SLOT * (NQ + N1 + N2);
   static constexpr int SWZ = BX / 2 - 1;
   static constexpr int WN = BX + 8;    // window: cols [x-4, x+BX+4)
   static constexpr int WC = WN / 2;    // window chunks
-  static constexpr int NCH = 3 * CHR;  // chunks per q row
+  static constexpr int NCH = NS * 3 * CHR;  // chunks per ring slot
   static constexpr int NLD = (NCH + NT - 1) / NT;
+  // element offset of a copied chunk from the group's first state (32-bit for one state)
+  using GOff = typename std::conditional<(NS > 1), long long, int>::type;
   static constexpr int MINB = (int)((227 * 1024) / (SMEM + 1024)) < 1 ? 1 : (int)((227 * 1024) / (SMEM + 1024));
   static_assert(G % 32 == 0, "stage groups must be whole warps");
   static_assert(BX == 4 || BX == 8, "BX is 4 or 8");
@@ -189,10 +195,11 @@ __device__ __forceinline__ void rotate_v(Acc<K>& A) {
 }
 
 struct Seg {
-  const double* src;
-  double* dst;
-  long long n;  // nx * ny
+  const double* src;  // first state of the CTA's group (loads add each chunk's state offset)
+  double* dst;        // this thread's state (stage 3 stores)
+  long long n;        // nx * ny
   int ny, y0, TY;
+  bool st_ok;         // this thread's state exists (the last group may be short)
 };
 
 // Consume row k and store the completed rows (k-1: u, p; k-2: v) of stage S.
@@ -243,7 +250,7 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
     }
   } else {
     const int x = g * BX;
-    if (k - 1 >= 0 && k - 1 < sg.TY) {
+    if (sg.st_ok && k - 1 >= 0 && k - 1 < sg.TY) {
       double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NX + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) {
@@ -251,7 +258,7 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
         *reinterpret_cast<double2*>(o + 2 * sg.n + c) = make_double2(A.p[U0][c], A.p[U0][c + 1]);
       }
     }
-    if (k - 2 >= 0 && k - 2 < sg.TY) {
+    if (sg.st_ok && k - 2 >= 0 && k - 2 < sg.TY) {
       double* o = sg.dst + sg.n + (long long)(sg.y0 + k - 2) * K::NX + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) *reinterpret_cast<double2*>(o + c) = make_double2(A.v[0][c], A.v[0][c + 1]);
@@ -263,8 +270,8 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
 // k = t - lag.  I = t mod 3 = k mod 3 (the lags are multiples of 3) is a compile-time
 // constant, so the u/p accumulator slots and the s-ring slots are too.
 template <class K, int S, int I>
-__device__ __forceinline__ void tick(Acc<K>& A, double* sm, const Seg& sg, const FusedParams& P, int g,
-                                     int t, const int* ld_soff, const int* ld_goff, int* woff,
+__device__ __forceinline__ void tick(Acc<K>& A, double* sm, double* smj, const Seg& sg, const FusedParams& P, int g,
+                                     int t, const int* ld_soff, const typename K::GOff* ld_goff, int* woff,
                                      int goff0, int goff1, bool ghost) {
   const int TY = sg.TY;
   cp_wait1();
@@ -284,20 +291,15 @@ __device__ __forceinline__ void tick(Acc<K>& A, double* sm, const Seg& sg, const
   }
   const int k = t - lag_of(S);
   if (k < lo_of(S) || k > TY + hi_of(S)) return;
-  // keep the swizzled window offsets in registers (opaque: not recomputed every tick)
-  if constexpr (K::NX <= 256) {
-#pragma unroll
-    for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
-  }
   // z = t & zmask = 0, opaque: the stage's coefficients load inside the tick (uniform
   // registers) instead of 28 doubles being hoisted out of the loop
-  stage_tick<K, S, I>(A, sm, sg, P, g, k, t & P.zmask, woff, goff0, goff1, ghost);
+  stage_tick<K, S, I>(A, smj, sg, P, g, k, t & P.zmask, woff, goff0, goff1, ghost);
   rotate_v(A);
 }
 
 template <class K, int S>
-__device__ __forceinline__ void stage_loop(double* sm, const Seg& sg, const FusedParams& P, int g,
-                                           const int* ld_soff, const int* ld_goff, int* woff,
+__device__ __forceinline__ void stage_loop(double* sm, double* smj, const Seg& sg, const FusedParams& P, int g,
+                                           const int* ld_soff, const typename K::GOff* ld_goff, int* woff,
                                            int goff0, int goff1, bool ghost) {
   Acc<K> A;
 #pragma unroll
@@ -310,16 +312,16 @@ __device__ __forceinline__ void stage_loop(double* sm, const Seg& sg, const Fuse
   // tick count rounded up to the unroll (the same for every warp: equal barrier counts)
   const int nt = (sg.TY + 14 + 2) / 3 * 3;
   for (int t = 0; t < nt; t += 3) {
-    tick<K, S, 0>(A, sm, sg, P, g, t, ld_soff, ld_goff, woff, goff0, goff1, ghost);
-    tick<K, S, 1>(A, sm, sg, P, g, t + 1, ld_soff, ld_goff, woff, goff0, goff1, ghost);
-    tick<K, S, 2>(A, sm, sg, P, g, t + 2, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    tick<K, S, 0>(A, sm, smj, sg, P, g, t, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    tick<K, S, 1>(A, sm, smj, sg, P, g, t + 1, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    tick<K, S, 2>(A, sm, smj, sg, P, g, t + 2, ld_soff, ld_goff, woff, goff0, goff1, ghost);
   }
 }
 
 template <class K>
 __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double* __restrict__ in,
                                                                   double* __restrict__ out,
-                                                                  FusedParams P, int nseg) {
+                                                                  FusedParams P, int nseg, int batch) {
   extern __shared__ __align__(16) double sm[];
   const int ny = P.ny;
   Seg sg;
@@ -327,24 +329,28 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   sg.ny = ny;
   sg.y0 = (int)((long long)blockIdx.x * ny / nseg);
   sg.TY = (int)((long long)(blockIdx.x + 1) * ny / nseg) - sg.y0;
-  sg.src = in + (long long)blockIdx.y * P.ld_in;
-  sg.dst = out + (long long)blockIdx.y * P.ld_out;
+  const int grp0 = blockIdx.y * K::NS;  // first state of this CTA
+  sg.src = in + (long long)grp0 * P.ld_in;
   const int tid = threadIdx.x;
   // q-row copy assignment: chunk e = tid + j*NT of the 3 x CHR chunks of a row
   int ld_soff[K::NLD];
-  int ld_goff[K::NLD];
+  typename K::GOff ld_goff[K::NLD];
   // entries past the row (e >= NCH) repeat an earlier chunk: the same bytes to the same
   // place, so every thread issues NLD copies and the tick loop has no divergent branch
 #pragma unroll
   for (int j = 0; j < K::NLD; ++j) {
     int e = tid + j * K::NT;
     e -= (e >= K::NCH) ? K::NCH : 0;
-    const int f = e / K::CHR, c = e - f * K::CHR;
+    const int js = e / (3 * K::CHR);
+    const int r = e - js * 3 * K::CHR;
+    const int f = r / K::CHR, c = r - f * K::CHR;
     int col = 2 * c - 4;
     col += (col < 0) ? K::NX : 0;
     col -= (col >= K::NX) ? K::NX : 0;
-    ld_soff[j] = f * K::RW + 2 * swz(c, K::SWZ);
-    ld_goff[j] = f * (int)sg.n + col;
+    // a missing state of a short last group copies the group's first state (never stored)
+    const int jsrc = (grp0 + js < batch) ? js : 0;
+    ld_soff[j] = js * K::SROW + f * K::RW + 2 * swz(c, K::SWZ);
+    ld_goff[j] = (typename K::GOff)((long long)jsrc * P.ld_in + f * sg.n + col);
   }
   // prologue: q rows -6 and -5 (ticks 0 and 1 of stage 1)
   for (int rr = -6; rr <= -5; ++rr) {
@@ -360,7 +366,13 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   // warp uniform, and read through a shuffle so the compiler knows it: the stage
   // coefficients then load into uniform registers (DFMA takes them as operands)
   const int S = __shfl_sync(0xffffffffu, tid / K::G, 0);
-  const int g = tid - S * K::G;
+  // this thread's state within the group and its column group within the state row (one
+  // state: compile-time 0, so dst and the ring base stay CTA-uniform)
+  const int jst = K::NS > 1 ? (tid - S * K::G) / K::GS : 0;
+  const int g = tid - S * K::G - jst * K::GS;
+  sg.dst = out + (long long)(grp0 + jst) * P.ld_out;
+  sg.st_ok = K::NS > 1 ? grp0 + jst < batch : true;
+  double* smj = sm + jst * K::SROW;  // ring rows of this thread's state
   constexpr int BX = K::BX;
   // this thread's window chunk offsets inside a field row (fixed for the whole march)
   int woff[K::WC];
@@ -372,15 +384,15 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   if (g == 0) {
     goff0 = 2 * swz(K::NX / 2 + 2, K::SWZ);
     goff1 = 2 * swz(K::NX / 2 + 3, K::SWZ);
-  } else if (g == K::G - 1) {
+  } else if (g == K::GS - 1) {
     goff0 = 2 * swz(0, K::SWZ);
     goff1 = 2 * swz(1, K::SWZ);
   }
-  const bool ghost = (g == 0) || (g == K::G - 1);
+  const bool ghost = (g == 0) || (g == K::GS - 1);
   if constexpr (K::G >= 128) {  // four warps per stage group: per-stage loops, unrolled 3x
-    if (S == 0) stage_loop<K, 0>(sm, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
-    else if (S == 1) stage_loop<K, 1>(sm, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
-    else stage_loop<K, 2>(sm, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    if (S == 0) stage_loop<K, 0>(sm, smj, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    else if (S == 1) stage_loop<K, 1>(sm, smj, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+    else stage_loop<K, 2>(sm, smj, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
   } else {  // two CTAs of 6 warps per SM: one loop, the stage branch inside (measured faster)
     Acc<K> A;
 #pragma unroll
@@ -419,9 +431,9 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
 #pragma unroll
       for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
       // S is provably uniform: the coefficients stay in uniform registers (z = 0)
-      if (S == 0) stage_tick<K, 0, 3>(A, sm, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
-      else if (S == 1) stage_tick<K, 1, 3>(A, sm, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
-      else stage_tick<K, 2, 3>(A, sm, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
+      if (S == 0) stage_tick<K, 0, 3>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
+      else if (S == 1) stage_tick<K, 1, 3>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
+      else stage_tick<K, 2, 3>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
       rotate_up(A);
       rotate_v(A);
     }
@@ -449,7 +461,8 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
     const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
     double best = 1e300;
     for (int s = 1; s <= fp.ny / 16; ++s) {
-      const long long waves = ((long long)batch * s + slots - 1) / slots;
+      const long long ngrp = (batch + K::NS - 1) / K::NS;
+      const long long waves = (ngrp * s + slots - 1) / slots;
       const double cost = (double)waves * ((double)fp.ny / s + 14.0);
       if (cost < best - 1e-9) {
         best = cost;
@@ -458,8 +471,8 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
     }
     if (nseg <= 0) nseg = 1;
   }
-  dim3 grid(nseg, batch);
-  kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp, nseg);
+  dim3 grid(nseg, (batch + K::NS - 1) / K::NS);
+  kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp, nseg, batch);
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }
@@ -479,6 +492,8 @@ bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const vo
 void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
   switch (fp.nx) {
     case 128: return launch_march_cfg<MC<128, 4>>(c, fp, in, out, batch);
+    // MC<256, 4, 2> (two states per 12-warp CTA) passes the parity tests but spills and
+    // measured 42.7 G/s against 53.7 for two 6-warp CTAs per SM
     case 256: return launch_march_cfg<MC<256, 4>>(c, fp, in, out, batch);
     case 384: return launch_march_cfg<MC<384, 4>>(c, fp, in, out, batch);
     case 512: return launch_march_cfg<MC<512, 4>>(c, fp, in, out, batch);
