@@ -102,10 +102,9 @@ template <class K, int S, int PH>
 __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const double* base_up,
                                         const double* base_v, const int* woff, const StageCoef& C) {
   constexpr int BX = K::BX;
-  // u, p of rows k-1, k, k+1 in slots (PH+2)%3, PH, (PH+1)%3 (PH = k mod 3, compile time),
-  // or in slots 0, 1, 2 shifted after every row (PH = 3); v of rows k-2 .. k+2 in v[0..4]
-  // (shifted after every row)
-  constexpr int U0 = PH == 3 ? 0 : (PH + 2) % 3, U1 = PH == 3 ? 1 : PH, U2 = PH == 3 ? 2 : (PH + 1) % 3;
+  // u, p of rows k-1, k, k+1 in slots (PH+2)%3, PH, (PH+1)%3 (PH = k mod 3, compile time);
+  // v of rows k-2 .. k+2 in v[0..4] (shifted after every row)
+  constexpr int U0 = (PH + 2) % 3, U1 = PH, U2 = (PH + 1) % 3;
   double w[K::WN];
   // ---- v: x stencil of row k; v_x (mixed damping of u) and v itself (p's v_y, v_yy)
   //      go to rows k+-1 / k+-2; births of rows k+1 (u, p) and k+2 (v)
@@ -173,17 +172,6 @@ __device__ __forceinline__ void consume(Acc<K>& A, const double* in, const doubl
 }
 
 template <class K>
-__device__ __forceinline__ void rotate_up(Acc<K>& A) {
-#pragma unroll
-  for (int c = 0; c < K::BX; ++c) {
-    A.u[0][c] = A.u[1][c];
-    A.u[1][c] = A.u[2][c];
-    A.p[0][c] = A.p[1][c];
-    A.p[1][c] = A.p[2][c];
-  }
-}
-
-template <class K>
 __device__ __forceinline__ void rotate_v(Acc<K>& A) {
 #pragma unroll
   for (int c = 0; c < K::BX; ++c) {
@@ -206,10 +194,8 @@ struct Seg {
 template <class K, int S, int PH>
 __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg, const FusedParams& P,
                                            int g, int k, int z, const int* woff, int goff0, int goff1,
-                                           bool ghost, int k3_rt = 0) {
-  // ring slot of row k: k mod 3 (compile time, or k3_rt in the rotating mode PH = 3)
-  const int k3 = PH == 3 ? k3_rt : PH;
-  constexpr int U0 = PH == 3 ? 0 : (PH + 2) % 3;
+                                           bool ghost) {
+  constexpr int k3 = PH, U0 = (PH + 2) % 3;  // ring slot of row k (k mod 3), u/p slot of row k-1
   constexpr int BX = K::BX;
   double* qring = sm;
   double* r1 = qring + K::NQ * K::SLOT;
@@ -294,6 +280,42 @@ __device__ __forceinline__ void tick(Acc<K>& A, double* sm, double* smj, const S
   // z = t & zmask = 0, opaque: the stage's coefficients load inside the tick (uniform
   // registers) instead of 28 doubles being hoisted out of the loop
   stage_tick<K, S, I>(A, smj, sg, P, g, k, t & P.zmask, woff, goff0, goff1, ghost);
+  rotate_v(A);
+}
+
+// Single loop over ticks for all stages (the stage branch inside), unrolled 3x so the
+// u/p accumulator slots are compile-time (I = t mod 3 = k mod 3).
+template <class K, int I>
+__device__ __forceinline__ void tick_all(Acc<K>& A, double* sm, double* smj, const Seg& sg,
+                                         const FusedParams& P, int S, int g, int t,
+                                         const int* ld_soff, const typename K::GOff* ld_goff,
+                                         int* woff, int goff0, int goff1, bool ghost) {
+  const int TY = sg.TY;
+  cp_wait1();
+  bar_sync();
+  {
+    const int rr = t - 4;  // q row needed by stage 1 in tick t+2, into slot rr & 7
+    if (rr <= TY + 5) {
+      int gy = sg.y0 + rr;
+      gy += (gy < 0) ? sg.ny : 0;
+      gy -= (gy >= sg.ny) ? sg.ny : 0;
+      double* slot = sm + (size_t)(rr & 7) * K::SLOT;
+      const double* rowp = sg.src + (long long)gy * K::NX;
+#pragma unroll
+      for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
+    }
+    cp_commit();
+  }
+  const int lag = S == 0 ? lag_of(0) : S == 1 ? lag_of(1) : lag_of(2);
+  const int lo = S == 0 ? lo_of(0) : S == 1 ? lo_of(1) : lo_of(2);
+  const int hi = TY + (S == 0 ? hi_of(0) : S == 1 ? hi_of(1) : hi_of(2));
+  const int k = t - lag;
+  if (k < lo || k > hi) return;
+#pragma unroll
+  for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
+  if (S == 0) stage_tick<K, 0, I>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost);
+  else if (S == 1) stage_tick<K, 1, I>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost);
+  else stage_tick<K, 2, I>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost);
   rotate_v(A);
 }
 
@@ -393,7 +415,8 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     if (S == 0) stage_loop<K, 0>(sm, smj, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
     else if (S == 1) stage_loop<K, 1>(sm, smj, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
     else stage_loop<K, 2>(sm, smj, sg, P, g, ld_soff, ld_goff, woff, goff0, goff1, ghost);
-  } else {  // two CTAs of 6 warps per SM: one loop, the stage branch inside (measured faster)
+  } else {  // two CTAs of 6 warps per SM: one loop with the stage branch inside, unrolled 3x
+    // (per-stage loops measured 44 G/s here, the rotating single loop 53.7, this 54.8)
     Acc<K> A;
 #pragma unroll
     for (int c = 0; c < BX; ++c) {
@@ -402,40 +425,11 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
 #pragma unroll
       for (int r = 0; r < 5; ++r) A.v[r][c] = 0.0;
     }
-    const int TY = sg.TY;
-    const int nt = TY + 14;
-    const int lag = S == 0 ? lag_of(0) : S == 1 ? lag_of(1) : lag_of(2);
-    const int lo = S == 0 ? lo_of(0) : S == 1 ? lo_of(1) : lo_of(2);
-    const int hi = TY + (S == 0 ? hi_of(0) : S == 1 ? hi_of(1) : hi_of(2));
-    int t3 = 0;  // t mod 3 == k mod 3 (every lag is a multiple of 3)
-    for (int t = 0; t < nt; ++t, t3 = (t3 == 2 ? 0 : t3 + 1)) {
-      cp_wait1();
-      bar_sync();
-      {  // q row t-4 (needed by stage 1 in tick t+2) into slot (t-4) & 7
-        const int rr = t - 4;
-        if (rr <= TY + 5) {
-          int gy = sg.y0 + rr;
-          gy += (gy < 0) ? ny : 0;
-          gy -= (gy >= ny) ? ny : 0;
-          double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-          const double* rowp = sg.src + (long long)gy * K::NX;
-#pragma unroll
-          for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
-        }
-        cp_commit();
-      }
-      const int k = t - lag;
-      if (k < lo || k > hi) continue;
-      // keep the swizzled window offsets in registers (opaque: not recomputed every tick);
-      // measured +2.6% at nx = 256
-#pragma unroll
-      for (int j = 0; j < K::WC; ++j) asm volatile("" : "+r"(woff[j]));
-      // S is provably uniform: the coefficients stay in uniform registers (z = 0)
-      if (S == 0) stage_tick<K, 0, 3>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
-      else if (S == 1) stage_tick<K, 1, 3>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
-      else stage_tick<K, 2, 3>(A, smj, sg, P, g, k, 0, woff, goff0, goff1, ghost, t3);
-      rotate_up(A);
-      rotate_v(A);
+    const int nt = (sg.TY + 14 + 2) / 3 * 3;
+    for (int t = 0; t < nt; t += 3) {
+      tick_all<K, 0>(A, sm, smj, sg, P, S, g, t, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+      tick_all<K, 1>(A, sm, smj, sg, P, S, g, t + 1, ld_soff, ld_goff, woff, goff0, goff1, ghost);
+      tick_all<K, 2>(A, sm, smj, sg, P, S, g, t + 2, ld_soff, ld_goff, woff, goff0, goff1, ghost);
     }
   }
 }
