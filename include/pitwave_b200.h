@@ -147,6 +147,16 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
 typedef int (*pw_fine_hook)(void* user, const double* qk, double* pred, int n_c, long long dim);
 int pw_ctx_set_fine_hook(pw_ctx* ctx, pw_fine_hook hook, void* user);
 
+/* Row-local variant for multi-rank TSQR sweeps (pw_ctx_set_tsqr with world > 1), where
+ * the fine and coarse images are kept as this rank's rows only: the hook fills
+ * pred_rows (rows x n_c, ld = rows) with rows [row_lo, row_lo + rows) of the n_c fine
+ * images of qk (ld = dim).  Across ranks that is the all-to-all of SURVEY 8(e): each rank
+ * propagates its slices and sends every other rank that rank's rows.  Without it such a
+ * sweep propagates all slices itself and keeps its rows. */
+typedef int (*pw_fine_rows_hook)(void* user, const double* qk, double* pred_rows, int n_c, long long dim,
+                                 long long row_lo, long long rows);
+int pw_ctx_set_fine_rows_hook(pw_ctx* ctx, pw_fine_rows_hook hook, void* user);
+
 /* ---- row-sharded serial correction --------------------------
  * With world > 1 every rank keeps the whole subspace (replicated, deterministic
  * refactorisation) but streams only its row block [rank*blk, (rank+1)*blk) of D

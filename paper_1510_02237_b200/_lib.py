@@ -28,6 +28,8 @@ c_dp = ctypes.POINTER(ctypes.c_double)
 c_ip = ctypes.POINTER(ctypes.c_int)
 c_vp = ctypes.c_void_p
 FINE_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong)
+FINE_ROWS_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong,
+                                  ctypes.c_longlong, ctypes.c_longlong)
 ALLREDUCE_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, ctypes.c_longlong)
 ALLGATHER_HOOK = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong)
 
@@ -82,6 +84,7 @@ SIGNATURES = [
                                 ctypes.c_double, ctypes.c_double, c_vp, c_dp, c_ip, c_dp, c_ip,
                                 ctypes.POINTER(c_vp)]),
     ("pw_ctx_set_fine_hook", ctypes.c_int, [c_vp, FINE_HOOK, c_vp]),
+    ("pw_ctx_set_fine_rows_hook", ctypes.c_int, [c_vp, FINE_ROWS_HOOK, c_vp]),
     ("pw_ctx_set_comm", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ALLREDUCE_HOOK, ALLGATHER_HOOK,
                                        c_vp]),
     ("pw_ctx_set_row_shards", ctypes.c_int, [c_vp, ctypes.c_int]),

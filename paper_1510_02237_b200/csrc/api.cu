@@ -503,9 +503,15 @@ static void factor_tsqr(pw_basis* B) {
     pw::launch_extract_upper(c, B->W.p + lo, d, m, m, RG + (size_t)g * m * m);  // m x m, ld m
   }
   mark("tsqr.local");
-  if (c.comm_world > 1)
+  if (c.comm_world > 1) {
+    // the hooks work on the context's main stream; this runs on the side stream (overlapped
+    // with the fine sweep), so hand the R factors over and take the gathered ones back with
+    // device-wide syncs (once per update)
+    PW_CUDA(cudaDeviceSynchronize());
     PW_CHECK(c.allgather_hook(c.comm_user, RG, (long long)m * m, (long long)nsh * m * m) == 0, PW_ERR_STATE,
              "all-gather hook failed (TSQR R factors)");
+    PW_CUDA(cudaDeviceSynchronize());
+  }
   for (int g = 0; g < nsh; ++g)  // stack: RR[g m : (g+1) m, :] = R_g
     PW_CUDA(cudaMemcpy2DAsync(RR + (size_t)g * m, nm * sizeof(double), RG + (size_t)g * m * m,
                               m * sizeof(double), m * sizeof(double), m, cudaMemcpyDeviceToDevice, c.stream));
@@ -811,6 +817,14 @@ int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards) {
   return guarded([&] {
     PW_CHECK(ctx && nshards >= 1, PW_ERR_VALUE, "bad argument");
     ctx->c.vshards = nshards;
+  });
+}
+
+int pw_ctx_set_fine_rows_hook(pw_ctx* ctx, pw_fine_rows_hook hook, void* user) {
+  return guarded([&] {
+    PW_CHECK(ctx != nullptr, PW_ERR_VALUE, "bad argument");
+    ctx->c.fine_rows_hook = hook;
+    ctx->c.fine_rows_user = user;
   });
 }
 
@@ -1125,25 +1139,30 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     const long long d = fine->dim;
     const bool kse = mode == PW_MODE_KSE;
     // buffers (column-major, ld = d)
-    DBuf bQK, bQN, bPred, bGK, bGN, bRes, bScr, bAlpha, bPart, bAlphaPart;
+    // Row-local sweep (multi-rank KSE with TSQR): the basis, the fine images (PRED) and the
+    // coarse images (GK, GN) hold only this rank's rows [lo, lo + ldr); the iterates QK,
+    // QN stay whole (G and the fine sweep need whole states).  Otherwise ldr = d, roff = 0.
+    const bool local = kse && c.comm_world > 1 && c.tsqr;
+    long long roff = 0, ldr = d;
+    if (local) {
+      const long long blk = ((d + c.comm_world - 1) / c.comm_world + 1) / 2 * 2;
+      roff = std::min<long long>(d, (long long)c.comm_rank * blk);
+      ldr = std::min<long long>(d, roff + blk) - roff;
+      PW_CHECK(ldr >= 1, PW_ERR_VALUE, "row-sharded sweep: this rank has no rows");
+    }
+    DBuf bQK, bQN, bPred, bGK, bGN, bGF, bRes, bScr, bAlpha, bPart, bAlphaPart;
     double* QK = bQK.ensure(c, (size_t)d * (n_c + 1));
     double* QN = bQN.ensure(c, (size_t)d * (n_c + 1));
-    double* PRED = bPred.ensure(c, (size_t)d * n_c);
-    double* GK = bGK.ensure(c, (size_t)d * n_c);
-    double* GN = bGN.ensure(c, (size_t)d * n_c);
+    double* PRED = bPred.ensure(c, (size_t)ldr * n_c);
+    double* GK = bGK.ensure(c, (size_t)ldr * n_c);
+    double* GN = bGN.ensure(c, (size_t)ldr * n_c);
+    double* GF = local ? bGF.ensure(c, (size_t)d) : nullptr;  // one whole G(qn_i) (row-local)
     double* res_dev = bRes.ensure(c, n_it);
     double* scr = bScr.ensure(c, pw::residual_scratch_doubles(n_c, d));
     std::unique_ptr<pw_basis> B;
     if (kse) {
       // multi-rank TSQR sweeps keep only this rank's rows of the basis (memory / world)
-      const bool local = c.comm_world > 1 && c.tsqr;
-      long long lo = 0, nrow = d;
-      if (local) {
-        const long long blk = ((d + c.comm_world - 1) / c.comm_world + 1) / 2 * 2;
-        lo = std::min<long long>(d, (long long)c.comm_rank * blk);
-        nrow = std::min<long long>(d, lo + blk) - lo;
-        PW_CHECK(nrow >= 1, PW_ERR_VALUE, "row-sharded subspace: this rank has no rows");
-      }
+      const long long lo = roff, nrow = ldr;
       B.reset(basis_new(ctx, nrow, rank_tol, n_c * n_it));
       B->diff_mode = true;
       B->coarse = coarse;
@@ -1164,7 +1183,8 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         if (reserved > used) free_b += (size_t)(reserved - used);
       }
       const double col = 8.0 * (double)d, bcol = 8.0 * (double)B->dim;
-      const double need = bcol * std::min<long long>(B->cap, B->dim) * 5.0 + col * n_c * 3.0 +
+      const double need = bcol * std::min<long long>(B->cap, B->dim) * 5.0 + col * n_c * 2.0 +
+                          bcol * n_c * 3.0 +
                           std::max(4.0 * (1ull << 30), 0.06 * (double)total_b);
       const char* e = getenv("PW_SWEEP_LEAN");
       B->lean = !B->local_rows && ((e && *e == '1') || need > (double)free_b);
@@ -1198,7 +1218,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
     copy_cols(c, QK, d, q0, d, d, 1);
     for (int i = 0; i < n_c; ++i) prop_apply(coarse, QK + (size_t)i * d, QK + (size_t)(i + 1) * d, 1, d);
-    copy_cols(c, GK, d, QK + d, d, d, n_c);  // G(qk[i]) for the first correction
+    copy_cols(c, GK, ldr, QK + d + roff, d, ldr, n_c);  // G(qk[i]) for the first correction
     if (timed) {
       PW_CUDA(cudaEventRecord(ev[1], c.stream));
       t_coarse += elapsed(ev[0], ev[1]);
@@ -1211,7 +1231,19 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       // the fine propagator runs on the main one (only Y needs the fine images)
       if (kse) PW_CUDA(cudaEventRecord(sync.snap, c.stream));
       // fine predictor over all slices at once (_fine_all, parareal.py:62-65)
-      if (c.fine_hook) {
+      if (local && c.fine_rows_hook) {  // this rank's rows of all fine images (all-to-all)
+        const int rc = c.fine_rows_hook(c.fine_rows_user, QK, PRED, n_c, d, roff, ldr);
+        PW_CHECK(rc == 0, PW_ERR_STATE, "fine rows hook failed (rc=" + std::to_string(rc) + ")");
+      } else if (local) {  // propagate every slice here, keep this rank's rows
+        const int chunk = (int)std::max<long long>(1, std::min<long long>(n_c, (1ll << 27) / d));
+        double* tmp = bGF.ensure(c, (size_t)d * chunk);
+        GF = tmp;
+        for (int i0 = 0; i0 < n_c; i0 += chunk) {
+          const int nb = std::min(chunk, n_c - i0);
+          prop_apply(fine, QK + (size_t)i0 * d, tmp, nb, d);
+          copy_cols(c, PRED + (size_t)i0 * ldr, ldr, tmp + roff, d, ldr, nb);
+        }
+      } else if (c.fine_hook) {
         const int rc = c.fine_hook(c.fine_hook_user, QK, PRED, n_c, d);
         PW_CHECK(rc == 0, PW_ERR_STATE, "fine hook failed (rc=" + std::to_string(rc) + ")");
       } else {
@@ -1227,12 +1259,12 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         PW_CUDA(cudaEventRecord(sync.fact, c.stream));
       }
       // c_i = F(qk[i]) - G(qk[i])  [- D Q^T qk[i] in KSE mode]
-      pw::launch_axpby_cols(c, PRED, PRED, GK, 1.0, -1.0, (size_t)d * n_c);
+      pw::launch_axpby_cols(c, PRED, PRED, GK, 1.0, -1.0, (size_t)ldr * n_c);
       int r = 0;
       double* alpha = nullptr;
       double* alpha_next = nullptr;
       if (kse) {
-        basis_append_images(B.get(), m_old, PRED + B->row_lo, d, n_c);
+        basis_append_images(B.get(), m_old, PRED, ldr, n_c);  // rows roff.. (all rows: ldr = d)
         PW_CUDA(cudaStreamWaitEvent(c.stream, sync.fact, 0));
         basis_images_gemm(B.get());
         r = B->r;
@@ -1247,7 +1279,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             gemm(c, true, false, r, n_c, nr, 1.0, B->Q.p, nr, QK + lo, d, 0.0, ab, r);
             PW_CHECK(c.allreduce_hook(c.comm_user, ab, (long long)r * n_c) == 0, PW_ERR_STATE,
                      "allreduce hook failed (TSQR projection)");
-            gemm(c, false, false, nr, n_c, r, -1.0, B->Y.p, nr, ab, r, 1.0, PRED + lo, d);
+            gemm(c, false, false, nr, n_c, r, -1.0, B->Y.p, nr, ab, r, 1.0, PRED, ldr);
           } else {
             gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
             gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
@@ -1263,7 +1295,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       double* a_cur = alpha;
       double* a_buf[2] = {alpha_next, alpha_next ? alpha_next + r : nullptr};
       const bool comm = c.comm_world > 1;
-      const int nsh = (r > 0) ? (comm ? c.comm_world : std::max(1, c.vshards)) : 1;
+      const int nsh = local ? c.comm_world : (r > 0) ? (comm ? c.comm_world : std::max(1, c.vshards)) : 1;
       if (nsh > 1) {
         // Row-sharded serial correction: shard s owns rows [s blk, (s+1) blk)
         // of D and Q.  Per step: G(qn_i) (replicated), the combine pass over the shard's rows
@@ -1272,7 +1304,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         // an allreduce of r doubles and the gather an all-gather of d doubles; a single
         // process with vshards > 1 runs every shard itself and sums in shard order (tests).
         const long long blk = ((d + nsh - 1) / nsh + 1) / 2 * 2;  // even: 16-byte row blocks
-        double* a_part = bAlphaPart.ensure(c, (size_t)r * nsh);
+        double* a_part = bAlphaPart.ensure(c, (size_t)std::max(r, 1) * nsh);
         if (comm) {  // every replica must have found the same rank
           double* rr = a_part;
           const double rv = (double)r;
@@ -1285,7 +1317,9 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
                    "replicas disagree on the subspace rank (" + std::to_string(r) + " here)");
         }
         for (int i = 0; i < n_c; ++i) {
-          prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
+          // G(qn_i): whole, into GN's column (or GF, whose rows GN keeps, row-local)
+          double* gi = local ? GF : GN + (size_t)i * d;
+          prop_apply(coarse, QN + (size_t)i * d, gi, 1, d);
           double* a_nxt = a_buf[i % 2];
           const int s0 = comm ? c.comm_rank : 0, s1 = comm ? c.comm_rank + 1 : nsh;
           for (int sh = s0; sh < s1; ++sh) {
@@ -1297,9 +1331,13 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             }
             // row-local basis: this rank's rows start at row 0 of Y and Q (ld = their rows)
             const long long boff = B->local_rows ? 0 : lo, bld = B->local_rows ? B->dim : d;
-            pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d + lo, B->Y.p + boff, r,
-                                    PRED + (size_t)i * d + lo, a_cur, B->Q.p + boff, r, hi - lo,
+            const double* ci = local ? PRED + (size_t)i * ldr : PRED + (size_t)i * d + lo;
+            pw::launch_combine_gemv(c, c.stream, gi + lo, r > 0 ? B->Y.p + boff : nullptr, r, ci, a_cur,
+                                    r > 0 ? B->Q.p + boff : nullptr, r, hi - lo,
                                     QN + (size_t)(i + 1) * d + lo, dst, part, 0, bld);
+            if (local)
+              PW_CUDA(cudaMemcpyAsync(GN + (size_t)i * ldr, gi + lo, sizeof(double) * (size_t)ldr,
+                                      cudaMemcpyDeviceToDevice, c.stream));
           }
           if (comm) {
             PW_CHECK(c.allreduce_hook(c.comm_user, a_nxt, r) == 0, PW_ERR_STATE, "allreduce hook failed");

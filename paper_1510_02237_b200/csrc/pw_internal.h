@@ -108,6 +108,8 @@ struct Ctx {
   pw_allgather_hook allgather_hook = nullptr;
   void* comm_user = nullptr;
   pw_fine_hook fine_hook = nullptr;  // slice-sharded fine predictor (multi-GPU), see header
+  pw_fine_rows_hook fine_rows_hook = nullptr;  // ... delivering this rank's rows (row-local sweeps)
+  void* fine_rows_user = nullptr;
   void* fine_hook_user = nullptr;
 };
 

@@ -69,6 +69,33 @@ class ShardedFine:
                 out[rlo:rhi] = blocks[r][: rhi - rlo]
         return out
 
+    def rows(self, qk: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
+        """Rows [lo, hi) of all n fine images (n, hi - lo) on this rank: the all-to-all of
+        SURVEY 8(e).  Each rank propagates its block of slices and sends every rank g the
+        rows of g's block (row blocks of ``row_block`` with the sweep's even block size)."""
+        world, rank = self.world, self.rank
+        n, d = qk.shape
+        if world == 1:
+            return self.apply_fn(qk)[:, lo:hi].contiguous()
+        slo, shi = shard_range(n, rank, world)
+        width = (n + world - 1) // world
+        blk = ((d + world - 1) // world + 1) // 2 * 2
+        send = torch.zeros((world, width, blk), dtype=qk.dtype, device=qk.device)
+        if shi > slo:
+            mine = self.apply_fn(qk[slo:shi].contiguous())
+            for g in range(world):
+                glo, ghi = row_block(d, blk, g)
+                if ghi > glo:
+                    send[g, : shi - slo, : ghi - glo] = mine[:, glo:ghi]
+        recv = torch.empty_like(send)
+        tdist.all_to_all_single(recv, send, group=self.group)
+        out = torch.empty((n, hi - lo), dtype=qk.dtype, device=qk.device)
+        for src in range(world):
+            s_lo, s_hi = shard_range(n, src, world)
+            if s_hi > s_lo:
+                out[s_lo:s_hi] = recv[src, : s_hi - s_lo, : hi - lo]
+        return out
+
     # the oracle sweeps (tests) call fine.batch(states) on numpy arrays
     def batch(self, states):
         t = torch.as_tensor(states)

@@ -72,6 +72,33 @@ class ThreadComm:
 
         return _lib.ALLREDUCE_HOOK(allreduce), _lib.ALLGATHER_HOOK(allgather)
 
+    def fine_rows_hook(self, rank, device, fine):
+        """pw_fine_rows_hook: each rank propagates its block of slices; every rank then
+        takes its rows of all slices (the all-to-all of dist.ShardedFine.rows)."""
+        from paper_1510_02237_b200 import _lib
+        from paper_1510_02237_b200.dist import device_vector, shard_range
+
+        def hook(user, qk_ptr, pred_ptr, n_c, d, lo, rows):
+            try:
+                qk = device_vector(qk_ptr, n_c * d, device).view(n_c, d)
+                pred = device_vector(pred_ptr, n_c * rows, device).view(n_c, rows)
+                slo, shi = shard_range(n_c, rank, self.world)
+                self.slots[rank] = fine.apply(qk[slo:shi].contiguous()) if shi > slo else None
+                torch.cuda.current_stream(device).synchronize()
+                self.bar.wait()
+                for r in range(self.world):
+                    rlo, rhi = shard_range(n_c, r, self.world)
+                    if rhi > rlo:
+                        pred[rlo:rhi].copy_(self.slots[r][:, lo:lo + rows])
+                torch.cuda.current_stream(device).synchronize()
+                self.bar.wait()
+                return 0
+            except Exception as exc:  # noqa: BLE001
+                self.errors.append(exc)
+                return 1
+
+        return _lib.FINE_ROWS_HOOK(hook)
+
 
 def c1_props():
     from paper_1510_02237_b200.integrators import RK3, SPLIT_FE_FB, SlicePropagator, make_propagator
@@ -89,7 +116,7 @@ def c1_props():
 _build_lock = threading.Lock()
 
 
-def rank_main(rank, world, comm, tsqr, q0, results):
+def rank_main(rank, world, comm, tsqr, q0, results, rows_hook=False):
     from paper_1510_02237_b200 import _lib
     from paper_1510_02237_b200.parareal import kse_sweep
 
@@ -110,6 +137,8 @@ def rank_main(rank, world, comm, tsqr, q0, results):
                         _lib.Context._instances[0] = saved
             ar, ag = comm.hooks(rank, device)
             _lib.check(ctx.lib.pw_ctx_set_comm(ctx.handle, rank, world, ar, ag, None))
+            fh = comm.fine_rows_hook(rank, device, fine) if rows_hook else _lib.FINE_ROWS_HOOK()
+            _lib.check(ctx.lib.pw_ctx_set_fine_rows_hook(ctx.handle, fh, None))
             ctx.set_tsqr(tsqr)
             out = []
             for k in range(1, wl.n_it + 1):
@@ -124,14 +153,17 @@ def rank_main(rank, world, comm, tsqr, q0, results):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("tsqr", [False, True])
-def test_thread_ranks_c1_window_matches_reference(world, tsqr):
+@pytest.mark.parametrize("tsqr,rows_hook", [(False, False), (True, False), (True, True)])
+def test_thread_ranks_c1_window_matches_reference(world, tsqr, rows_hook):
+    """tsqr: row-sharded factorisation with a row-local basis and row-local fine/coarse
+    images; rows_hook: the fine images arrive through the all-to-all hook (each rank
+    propagates only its slices) instead of every rank propagating all of them."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     g = golden("c1_kse.npz")
     comm = ThreadComm(world)
     results = [None] * world
-    threads = [threading.Thread(target=rank_main, args=(r, world, comm, tsqr, g["q0"], results))
+    threads = [threading.Thread(target=rank_main, args=(r, world, comm, tsqr, g["q0"], results, rows_hook))
                for r in range(world)]
     for t in threads:
         t.start()
