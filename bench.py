@@ -197,7 +197,9 @@ def parareal_window(name="c3", warm=True, group=None):
     """One KSE-Parareal window of config `name` (c3: 512^2, P=64, K=5; c4: 1024^2, P=256,
     K=4): per-iteration device time and phases.  Under torchrun (`group`) the fine sweep
     is slice-sharded over the ranks (dist.ShardedFine, NCCL all-gather of the end states)
-    and the serial correction is replicated; the window time is the max over ranks."""
+    and the serial correction row-sharded (comm hooks); with --tsqr (PW_TSQR=1) the
+    subspace is factored by distributed TSQR and kept row-local, and the fine images
+    arrive by all-to-all.  The window time is the max over ranks."""
     import torch
 
     from paper_1510_02237_b200 import harness
@@ -474,10 +476,14 @@ def main():
     ap.add_argument("--parareal", dest="parareal", action="store_true", default=True)
     ap.add_argument("--no-parareal", dest="parareal", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tsqr", action="store_true",
+                    help="multi-rank Parareal windows: distributed TSQR, row-local basis (PW_TSQR=1)")
     ap.add_argument("--c4", dest="c4", action="store_true", default=True,
                     help="also time one c4 window (1024^2, P=256, K=4; ~20 s)")
     ap.add_argument("--no-c4", dest="c4", action="store_false")
     args = ap.parse_args()
+    if args.tsqr:
+        os.environ["PW_TSQR"] = "1"  # read when the library context is created
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
