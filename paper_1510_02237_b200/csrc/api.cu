@@ -1183,8 +1183,9 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         if (reserved > used) free_b += (size_t)(reserved - used);
       }
       const double col = 8.0 * (double)d, bcol = 8.0 * (double)B->dim;
-      const double need = bcol * std::min<long long>(B->cap, B->dim) * 5.0 + col * n_c * 2.0 +
-                          bcol * n_c * 3.0 +
+      // (the sweep buffers are allocated already: col * n_c * 3 is headroom for propagator
+      // temporaries, calibrated on c4)
+      const double need = bcol * std::min<long long>(B->cap, B->dim) * 5.0 + col * n_c * 3.0 +
                           std::max(4.0 * (1ull << 30), 0.06 * (double)total_b);
       const char* e = getenv("PW_SWEEP_LEAN");
       B->lean = !B->local_rows && ((e && *e == '1') || need > (double)free_b);
