@@ -45,6 +45,8 @@ BYTES_PER_CELL_UPDATE = 48  # read (u,v,p) + write (u,v,p), fp64 (SURVEY.md 8(d)
 # recompute excluded): stage 1 = 65, stages 2 and 3 = 68 (+ the q base)
 FLOP_PER_CELL_UPDATE = 201
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "fine_traffic.json")
+C2_WORKLOAD = ("c2: 64 states x 256^2 periodic x 200 RK3 steps (CFL 0.5, order 6, nu 0.005, cs=1, U=0.1), "
+               "seeded random-mode fields")
 
 
 def load_traffic():
@@ -185,7 +187,8 @@ def run_reference(args, rank, world):
     line = {"metric": "fine RK-3 fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "impl": "reference", "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c2: 64 states x 256^2 x 200 RK3 steps, cs=1, U=0.1",
+            "config": {"workload": C2_WORKLOAD, "global_batch_states": BATCH, "grid": N_GRID,
+                       "rk3_steps_per_state": STEPS_PER_SAMPLE,
                        "implementation": "CPU port of the reference kernels (oracle/pw_oracle.c)"},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -435,8 +438,7 @@ def run_ours(args, rank, world, local_rank):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "c2: 64 states x 256^2 periodic x 200 RK3 steps (CFL 0.5, order 6, "
-                                   "nu 0.005, cs=1, U=0.1), seeded random-mode fields",
+            "config": {"workload": C2_WORKLOAD,
                        "global_batch_states": BATCH * world, "grid": N_GRID,
                        "rk3_steps_per_state": STEPS_PER_SAMPLE, "parallelism": f"slice-sharded x{world}",
                        "l2": "256 MiB flush between timed steps; the 200 chained RK3 launches inside a "
