@@ -187,3 +187,24 @@ def test_damping_coefficient_known_values():
     assert a1 == pytest.approx(0.01875, rel=1e-10)
     with pytest.raises(ValueError, match="timescale"):
         damping_coefficients(0.1, 0.025, 0.025, 0.0)
+
+
+def test_bench_reference_arm_json_contract():
+    """bench.py --impl reference (the CPU arm the driver runs next to ours) prints one JSON
+    line with the device arm's metric, unit, config and the cpu_baseline / e2e keys."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["metric"] == "fine RK-3 fp64 cell-updates/s"
+    assert d["unit"] == "cell-updates/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["config"]["workload"].startswith("c2: 64 states x 256^2")
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
