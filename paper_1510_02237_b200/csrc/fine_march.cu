@@ -21,6 +21,15 @@
 //   windows come from shared memory: 3 fields x (BX+8) doubles per BX cells.
 // * q rows arrive by 16-byte cp.async two ticks ahead into an 8-row ring;
 //   stages 2/3 take their q base from it when a row's accumulator is born.
+// * The tick loop is unrolled 3x: u/p accumulators of row r live in slot
+//   r mod 3 (compile time), only v's five rows shift.  The stage index comes
+//   through __shfl_sync, so the compiler knows it is warp-uniform and keeps each
+//   stage's 28 coefficients in uniform registers (DFMA operands).  6-warp CTAs
+//   (nx <= 256) branch on the stage inside one loop; 12-warp CTAs (nx = 512)
+//   give each stage group its own loop.
+// * Segments: each state is cut into y-segments; the count minimises waves x
+//   (TY + 14) over the resident CTA slots.  (MC::NS > 1 would put NS states
+//   side by side in one CTA; measured slower, not dispatched.)
 //
 // Shared-memory rows are chunk-swizzled (chunk c at c ^ ((c >> 3) & (BX/2-1)))
 // so the BX/2-chunk thread stride of the window loads is conflict free.
@@ -206,8 +215,8 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
   else in = r2 + (size_t)k3 * K::SLOT;
   const double* bup = qring + (size_t)((k + 1) & 7) * K::SLOT;
   const double* bv = qring + (size_t)((k + 2) & 7) * K::SLOT;
-  // z == 0 but opaque: the 3 stages' 84 coefficients are read from the parameter bank
-  // inside the tick (uniform registers) instead of being hoisted out of the loop
+  // z is 0; the per-stage loops pass it opaque (t & zmask) so the stage's coefficients
+  // load inside the tick instead of being hoisted out of the loop
   consume<K, S, PH>(A, in, bup, bv, woff, P.st[S + z]);
   if constexpr (S < 2) {
     double* out = (S == 0 ? r1 : r2);
