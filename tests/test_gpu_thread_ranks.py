@@ -195,3 +195,97 @@ def test_thread_ranks_c1_window_matches_reference(world, tsqr, rows_hook):
             dev1 = max(np.linalg.norm(ends[i] - single[k][i]) / np.linalg.norm(single[k][i])
                        for i in range(ends.shape[0]))
             assert dev1 <= (1e-12 if not tsqr else 1e-10), (r, k, dev1)
+
+
+def c3_rank_main(rank, world, comm, q0, results):
+    """One thread rank of the c3 window with TSQR, the row-local basis and the all-to-all
+    fine hook; per iteration: ranks, residuals, per-slice norms and the sampled entries."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_1510_02237_b200 import _lib
+    from paper_1510_02237_b200.integrators import RK3, SPLIT_FE_FB, SlicePropagator, make_propagator
+    from paper_1510_02237_b200.mesh import ACOUSTIC, ConstantVelocity, build_grid
+    from paper_1510_02237_b200.parareal import kse_sweep
+    from paper_1510_02237_b200.physics import ModelSpec
+
+    device = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device)
+    try:
+        with torch.cuda.stream(stream):
+            ctx = _lib.Context(0)
+            with _build_lock:
+                saved = _lib.Context._instances.get(0)
+                _lib.Context._instances[0] = ctx
+                try:
+                    wl = harness.WORKLOADS["c3"]
+                    g = build_grid(wl.n, wl.n)
+                    vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
+                    fine = SlicePropagator(make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), g,
+                                                          0.5), wl.slice_span)
+                    coarse = SlicePropagator(make_propagator(SPLIT_FE_FB, ModelSpec(ACOUSTIC, vel, 1, 1.0, 0.1, 1.0),
+                                                            g, 4.0, 16), wl.slice_span)
+                finally:
+                    if saved is None:
+                        _lib.Context._instances.pop(0, None)
+                    else:
+                        _lib.Context._instances[0] = saved
+            ar, ag = comm.hooks(rank, device)
+            _lib.check(ctx.lib.pw_ctx_set_comm(ctx.handle, rank, world, ar, ag, None))
+            fh = comm.fine_rows_hook(rank, device, fine)
+            _lib.check(ctx.lib.pw_ctx_set_fine_rows_hook(ctx.handle, fh, None))
+            ctx.set_tsqr(True)
+            ref = np.load(os.path.join(GOLDEN, "c3_reference.npz"))
+            idx = torch.as_tensor(ref["idx"]).cuda()
+            q = torch.as_tensor(q0).cuda()
+            out = []
+            for k in range(1, len(ref["res"]) + 1):
+                ends, res, sub = kse_sweep(q, fine, coarse, wl.n_p, k, return_device=True)
+                st = ends.reshape(wl.n_p, -1)
+                out.append((sub.rank, list(res), torch.linalg.norm(st, dim=1).cpu().numpy(),
+                            st[:, idx].cpu().numpy()))
+                del ends, st, sub
+            results[rank] = out
+            ctx.lib.pw_ctx_set_comm(ctx.handle, 0, 1, _lib.ALLREDUCE_HOOK(), _lib.ALLGATHER_HOOK(), None)
+            del fine, coarse
+    except Exception as exc:  # noqa: BLE001
+        results[rank] = exc
+        comm.bar.abort()
+
+
+def test_thread_ranks_c3_window_tsqr_matches_reference_run():
+    """c3 (512^2, P=64, K=5) over 2 thread ranks with the multi-rank TSQR sweep (row-local
+    basis and fine/coarse images, all-to-all fine hook): the reference run's ranks, and
+    states within the c3 parity bound (as test_gpu_windows_ref.py)."""
+    import os
+
+    from conftest import GOLDEN
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    path = os.path.join(GOLDEN, "c3_reference.npz")
+    if not os.path.exists(path):
+        pytest.skip("c3_reference.npz not generated")
+    ref = np.load(path)
+    floor = [2.8e-9, 1.1e-8, 9.0e-9, 3.6e-8, 2.1e-7]  # test_gpu_windows_ref.C3_FLOOR
+    world = 2
+    comm = ThreadComm(world)
+    results = [None] * world
+    q0 = harness.initial_state("c3")
+    threads = [threading.Thread(target=c3_rank_main, args=(r, world, comm, q0, results)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=900)
+    assert not comm.errors, comm.errors
+    for r in range(world):
+        assert not isinstance(results[r], Exception), results[r]
+    for k, (rank_k, res, norms, samp) in enumerate(results[0]):
+        tol = max(1e-10, 10 * floor[k])
+        assert rank_k == ref["ranks"][k], (k, rank_k, ref["ranks"][k])
+        assert results[1][k][0] == rank_k
+        np.testing.assert_allclose(res, ref["res"][:k + 1], rtol=tol)
+        d_norm = np.max(np.abs(norms - ref["norms"][k]) / ref["norms"][k])
+        d_samp = np.max(np.linalg.norm(samp - ref["samples"][k], axis=1) / np.linalg.norm(ref["samples"][k], axis=1))
+        print(f"c3 thread ranks, iteration {k + 1}: rank {rank_k}, deviation {max(d_norm, d_samp):.3e}")
+        assert max(d_norm, d_samp) <= tol
