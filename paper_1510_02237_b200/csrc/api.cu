@@ -12,7 +12,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <memory>
+#include <mutex>
 
 #include "pw_internal.h"
 
@@ -335,6 +337,31 @@ static void presize_solver_ws(pw_basis* B) {
   B->cs_host.resize(std::max<size_t>(host, 1));
 }
 
+// Contexts alive in this process.  With more than one (several host threads driving the
+// same GPU, as the thread-rank tests do), concurrent cusolverDnXgeqrf calls on different
+// handles intermittently returned CUSOLVER_STATUS_INTERNAL_ERROR, so they are serialised
+// (call and completion) across contexts.  One context per process (the production layout,
+// one process per GPU) takes the plain path.
+static std::atomic<int> g_live_ctx{0};
+static std::mutex g_geqrf_mu;
+
+static void xgeqrf(pw_basis* B, long long rows, long long cols, double* A, long long lda, double* tau) {
+  Ctx& c = B->ctx->c;
+  int* info = B->info.ensure(c, 1);
+  auto call = [&] {
+    PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, cols, CUDA_R_64F, A, lda, CUDA_R_64F, tau,
+                               CUDA_R_64F, B->cs_work.p, B->cs_work.n * sizeof(double), B->cs_host.data(),
+                               B->cs_host.size(), info));
+  };
+  if (g_live_ctx.load() > 1) {
+    std::lock_guard<std::mutex> lock(g_geqrf_mu);
+    call();
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+  } else {
+    call();
+  }
+}
+
 // Householder QR of the panel W[row0:, col0:col0+p] (ld d) into tau1[col0..], its larft
 // block into T[col0.., col0..], then explicit unit-lower V for the panel (rows above the
 // panel's diagonal zeroed: R1 already holds them).  Returns the reflector count.
@@ -346,11 +373,8 @@ static int factor_panel(pw_basis* B, int col0, int p) {
   if (k <= 0) return 0;
   double* P = B->W.p + (size_t)col0 * d + col0;
   double* tau = B->tau1.p + col0;
-  int* info = B->info.ensure(c, 1);
   presize_solver_ws(B);
-  PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, p, CUDA_R_64F, P, d, CUDA_R_64F, tau,
-                             CUDA_R_64F, B->cs_work.p, B->cs_work.n * sizeof(double), B->cs_host.data(),
-                             B->cs_host.size(), info));
+  xgeqrf(B, rows, p, P, d, tau);
   mark("geqrf");
   return k;
 }
@@ -497,28 +521,24 @@ static void factor_tsqr(pw_basis* B) {
   for (int g = B->tsqr_g0; g < B->tsqr_g1; ++g) {
     long long lo, rows;
     tsqr_rows(B, g, lo, rows);
-    PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, m, CUDA_R_64F, B->W.p + lo, d, CUDA_R_64F,
-                               tauS + (size_t)g * capc, CUDA_R_64F, B->cs_work.p,
-                               B->cs_work.n * sizeof(double), B->cs_host.data(), B->cs_host.size(), info));
+    xgeqrf(B, rows, m, B->W.p + lo, d, tauS + (size_t)g * capc);
     pw::launch_extract_upper(c, B->W.p + lo, d, m, m, RG + (size_t)g * m * m);  // m x m, ld m
   }
   mark("tsqr.local");
   if (c.comm_world > 1) {
-    // the hooks work on the context's main stream; this runs on the side stream (overlapped
-    // with the fine sweep), so hand the R factors over and take the gathered ones back with
-    // device-wide syncs (once per update)
-    PW_CUDA(cudaDeviceSynchronize());
+    // the hooks work on the context's main stream; this may run on the side stream (beside
+    // the fine sweep): hand the R factors over and take the gathered ones back with syncs of
+    // the two streams (once per update)
+    PW_CUDA(cudaStreamSynchronize(c.stream));
     PW_CHECK(c.allgather_hook(c.comm_user, RG, (long long)m * m, (long long)nsh * m * m) == 0, PW_ERR_STATE,
              "all-gather hook failed (TSQR R factors)");
-    PW_CUDA(cudaDeviceSynchronize());
+    if (c.outer) PW_CUDA(cudaStreamSynchronize(c.outer));
   }
   for (int g = 0; g < nsh; ++g)  // stack: RR[g m : (g+1) m, :] = R_g
     PW_CUDA(cudaMemcpy2DAsync(RR + (size_t)g * m, nm * sizeof(double), RG + (size_t)g * m * m,
                               m * sizeof(double), m * sizeof(double), m, cudaMemcpyDeviceToDevice, c.stream));
   double* tauRR = B->tauRR.ensure(c, capc);
-  PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), nm, m, CUDA_R_64F, RR, nm, CUDA_R_64F, tauRR,
-                             CUDA_R_64F, B->cs_work.p, B->cs_work.n * sizeof(double), B->cs_host.data(),
-                             B->cs_host.size(), info));
+  xgeqrf(B, nm, m, RR, nm, tauRR);
   double* tmp = B->Rs.ensure(c, capc * capc);
   pw::launch_extract_upper(c, RR, nm, m, m, tmp);
   PW_CUDA(cudaMemcpy2DAsync(B->R1.p, capc * sizeof(double), tmp, m * sizeof(double), m * sizeof(double), m,
@@ -778,12 +798,14 @@ int pw_ctx_create(int device, void* stream, pw_ctx** out) {
     if (const char* e = std::getenv("PW_QR_OVERLAP")) ctx->c.qr_overlap = std::atoi(e) != 0;
     if (const char* e = std::getenv("PW_TSQR")) ctx->c.tsqr = std::atoi(e) != 0;
     *out = ctx.release();
+    g_live_ctx.fetch_add(1);
   });
 }
 
 int pw_ctx_destroy(pw_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
+    g_live_ctx.fetch_sub(1);
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.red) cudaFree(ctx->c.red);
     if (ctx->c.tma_done) cudaFree(ctx->c.tma_done);
@@ -1105,8 +1127,14 @@ namespace {
 struct StreamScope {
   Ctx& c;
   cudaStream_t saved;
-  StreamScope(Ctx& ctx, cudaStream_t s) : c(ctx), saved(ctx.stream) { set(s); }
-  ~StreamScope() { set(saved); }
+  StreamScope(Ctx& ctx, cudaStream_t s) : c(ctx), saved(ctx.stream) {
+    c.outer = saved;  // the stream the comm hooks work on (torch's current stream)
+    set(s);
+  }
+  ~StreamScope() {
+    set(saved);
+    c.outer = nullptr;
+  }
   void set(cudaStream_t s) {
     c.stream = s;
     cublasSetStream(blas(c), s);

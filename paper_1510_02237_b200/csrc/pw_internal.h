@@ -99,6 +99,7 @@ struct Ctx {
   bool strict = false;       // force reference-order kernels everywhere
   int coop_blocks_per_sm = 0;        // cap for cooperative G launches (0 = occupancy max)
   cudaStream_t side = nullptr;       // second stream: subspace QR beside the fine sweep
+  cudaStream_t outer = nullptr;      // while work runs on `side`: the context's own stream
   bool qr_overlap = true;            // PW_QR_OVERLAP=0: QR after the fine sweep, one stream
   bool tsqr = false;                 // row-sharded (TSQR) subspace factorisation in sharded sweeps
   // row-sharded serial correction: across ranks through the comm hooks (pw_ctx_set_comm),
