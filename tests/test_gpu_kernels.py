@@ -197,3 +197,17 @@ def test_blowup_is_not_an_error(dev):
     q0 = harness.fine_batch_states(n=32, batch=1, seed=8)
     out = SlicePropagator(cspec, nsteps=400)(q0[0])
     assert not np.isfinite(out).all()
+
+
+def test_fine_on_the_c5_grid_against_oracle(dev):
+    """Largest BASELINE grid (c5: 2048^2, ~100 MB per state): one seeded c5 state, 2 RK3
+    steps, fused kernel vs the oracle (<= 1e-12 relative)."""
+    from paper_1510_02237_b200.integrators import SlicePropagator
+
+    n = 2048
+    fspec, _ = make_specs(n)
+    q0 = harness.initial_state("c5")[None, :]
+    got = SlicePropagator(fspec, nsteps=2).batch(q0)
+    want = orc.SlicePropagator(orc.RK3, 2, nx=n, ny=n, cs=1.0, order=6, nu=0.005, cfl=0.5,
+                               velocity=("constant", 0.1, 0.0)).batch(q0)
+    assert rel(got[0], want[0]) <= 1e-12
