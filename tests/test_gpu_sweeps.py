@@ -450,3 +450,39 @@ def test_sharded_fine_hook_single_rank_group():
     ends, res, _ = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
     np.testing.assert_array_equal(np.array(ends_g), np.array(ends))
     assert res_g == res
+
+
+@pytest.mark.parametrize("tsqr_shards", [0, 2])
+def test_c5_shaped_window_against_oracle(dev, tsqr_shards):
+    """c5 physics and initial-state generator (all three fields random modes, |k| <= 32) on a
+    128^2 grid, P=16, K=3 (the full c5 needs 8 GPUs): ranks and states against the oracle,
+    replicated and with the row-sharded TSQR factorisation (2 in-process shards)."""
+    from paper_1510_02237_b200.integrators import RK3, SPLIT_FE_FB, SlicePropagator, make_propagator
+    from paper_1510_02237_b200.mesh import ACOUSTIC, ConstantVelocity, build_grid
+    from paper_1510_02237_b200.parareal import kse_sweep
+    from paper_1510_02237_b200.physics import ModelSpec
+
+    n, p, k, span = 128, 16, 3, 1.0 / 16
+    grid = build_grid(n, n)
+    vel = ConstantVelocity(0.1, 0.0)
+    fine = SlicePropagator(make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), grid, 0.5), span)
+    coarse = SlicePropagator(make_propagator(SPLIT_FE_FB, ModelSpec(ACOUSTIC, vel, 1, 1.0, 0.1, 1.0), grid, 4.0, 16), span)
+    q0 = harness.initial_state("c5", n=n)
+    if tsqr_shards:
+        dev.set_row_shards(tsqr_shards)
+        dev.set_tsqr(True)
+    try:
+        ends, res, sub = kse_sweep(q0, fine, coarse, p, k)
+    finally:
+        dev.set_tsqr(False)
+        dev.set_row_shards(1)
+    of = orc.SlicePropagator(orc.RK3, fine.nsteps, nx=n, ny=n, cs=1.0, order=6, nu=0.005, cfl=0.5,
+                             velocity=("constant", 0.1, 0.0))
+    oc = orc.SlicePropagator(orc.SPLIT_FE_FB, coarse.nsteps, nx=n, ny=n, cs=1.0, order=1, nu=0.1,
+                             cfl=4.0, n_sound=16, velocity=("constant", 0.1, 0.0))
+    ranks = []
+    o_ends, o_res, _ = orc.kse_sweep(q0, of, oc, p, k, ranks=ranks)
+    assert sub.ranks_history == ranks
+    worst = max(rel(a, b) for a, b in zip(ends, o_ends))
+    assert worst <= 1e-9, worst
+    np.testing.assert_allclose(res, o_res, rtol=1e-8)
