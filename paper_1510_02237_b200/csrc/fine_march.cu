@@ -33,16 +33,22 @@
 //
 // Shared-memory rows are chunk-swizzled (chunk c at c ^ ((c >> 3) & (BX/2-1)))
 // so the BX/2-chunk thread stride of the window loads is conflict free.
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "pw_internal.h"
 
+namespace cg = cooperative_groups;
+
 namespace pw {
 namespace {
 
-template <int NX_, int BX_, int NS_ = 1>
+template <int NX_, int BX_, int NS_ = 1, int CL_ = 1>
 struct MC {
   static constexpr int NX = NX_, BX = BX_, NS = NS_;  // NS states side by side per CTA
+  // CL CTAs of one thread-block cluster share each grid row (NX columns each; ghost
+  // columns exchanged through distributed shared memory): rows of NXT = CL * NX cells
+  static constexpr int CL = CL_, NXT = CL * NX;
   static constexpr int GS = NX / BX;   // threads per state row
   static constexpr int G = NS * GS;    // threads per stage group
   static constexpr int NT = 3 * G;
@@ -74,6 +80,15 @@ __host__ __device__ constexpr int hi_of(int S) { return S == 0 ? 5 : S == 1 ? 3 
 __device__ __forceinline__ int swz(int c, int m) { return c ^ ((c >> 3) & m); }
 
 __device__ __forceinline__ void bar_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
+// the tick barrier: the CTA, or the whole cluster when ghost columns come from other CTAs
+template <class K>
+__device__ __forceinline__ void tick_sync() {
+  if constexpr (K::CL > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    bar_sync();
+  }
+}
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -227,7 +242,15 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
     st_chunks<BX / 2>(o1 + 2 * K::RW, woff + 2, A.p[U0]);
     st_chunks<BX / 2>(o2 + K::RW, woff + 2, A.v[0]);
     if (ghost) {
-      // mirrored columns: the first 4 of thread 0's block, the last 4 of the last thread's
+      // mirrored columns: the first 4 of thread 0's block, the last 4 of the last thread's --
+      // into this CTA's ghost columns, or (cluster) the neighbouring CTA's on the same rows
+      if constexpr (K::CL > 1) {
+        const unsigned me = blockIdx.x;
+        const unsigned tgt = (g == 0) ? (me + K::CL - 1) % K::CL : (me + 1) % K::CL;
+        cg::cluster_group cl = cg::this_cluster();
+        o1 = cl.map_shared_rank(o1, tgt);
+        o2 = cl.map_shared_rank(o2, tgt);
+      }
       const bool first = (g == 0);
       double gu[4], gp[4], gv[4];
 #pragma unroll
@@ -244,9 +267,9 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
       *reinterpret_cast<double2*>(o2 + K::RW + goff1) = make_double2(gv[2], gv[3]);
     }
   } else {
-    const int x = g * BX;
+    const int x = (int)blockIdx.x * K::NX + g * BX;
     if (sg.st_ok && k - 1 >= 0 && k - 1 < sg.TY) {
-      double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NX + x;
+      double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NXT + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) {
         *reinterpret_cast<double2*>(o + c) = make_double2(A.u[U0][c], A.u[U0][c + 1]);
@@ -254,7 +277,7 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
       }
     }
     if (sg.st_ok && k - 2 >= 0 && k - 2 < sg.TY) {
-      double* o = sg.dst + sg.n + (long long)(sg.y0 + k - 2) * K::NX + x;
+      double* o = sg.dst + sg.n + (long long)(sg.y0 + k - 2) * K::NXT + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) *reinterpret_cast<double2*>(o + c) = make_double2(A.v[0][c], A.v[0][c + 1]);
     }
@@ -270,7 +293,7 @@ __device__ __forceinline__ void tick(Acc<K>& A, double* sm, double* smj, const S
                                      int goff0, int goff1, bool ghost) {
   const int TY = sg.TY;
   cp_wait1();
-  bar_sync();
+  tick_sync<K>();
   {
     const int rr = t - 4;  // q row needed by stage 1 in tick t+2, into slot rr & 7
     if (rr <= TY + 5) {
@@ -278,7 +301,7 @@ __device__ __forceinline__ void tick(Acc<K>& A, double* sm, double* smj, const S
       gy += (gy < 0) ? sg.ny : 0;
       gy -= (gy >= sg.ny) ? sg.ny : 0;
       double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-      const double* rowp = sg.src + (long long)gy * K::NX;
+      const double* rowp = sg.src + (long long)gy * K::NXT;
 #pragma unroll
       for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
     }
@@ -301,7 +324,7 @@ __device__ __forceinline__ void tick_all(Acc<K>& A, double* sm, double* smj, con
                                          int* woff, int goff0, int goff1, bool ghost) {
   const int TY = sg.TY;
   cp_wait1();
-  bar_sync();
+  tick_sync<K>();
   {
     const int rr = t - 4;  // q row needed by stage 1 in tick t+2, into slot rr & 7
     if (rr <= TY + 5) {
@@ -309,7 +332,7 @@ __device__ __forceinline__ void tick_all(Acc<K>& A, double* sm, double* smj, con
       gy += (gy < 0) ? sg.ny : 0;
       gy -= (gy >= sg.ny) ? sg.ny : 0;
       double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-      const double* rowp = sg.src + (long long)gy * K::NX;
+      const double* rowp = sg.src + (long long)gy * K::NXT;
 #pragma unroll
       for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
     }
@@ -356,11 +379,11 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   extern __shared__ __align__(16) double sm[];
   const int ny = P.ny;
   Seg sg;
-  sg.n = (long long)K::NX * ny;
+  sg.n = (long long)K::NXT * ny;
   sg.ny = ny;
-  sg.y0 = (int)((long long)blockIdx.x * ny / nseg);
-  sg.TY = (int)((long long)(blockIdx.x + 1) * ny / nseg) - sg.y0;
-  const int grp0 = blockIdx.y * K::NS;  // first state of this CTA
+  sg.y0 = (int)((long long)blockIdx.y * ny / nseg);
+  sg.TY = (int)((long long)(blockIdx.y + 1) * ny / nseg) - sg.y0;
+  const int grp0 = blockIdx.z * K::NS;  // first state of this CTA
   sg.src = in + (long long)grp0 * P.ld_in;
   const int tid = threadIdx.x;
   // q-row copy assignment: chunk e = tid + j*NT of the 3 x CHR chunks of a row
@@ -375,9 +398,9 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     const int js = e / (3 * K::CHR);
     const int r = e - js * 3 * K::CHR;
     const int f = r / K::CHR, c = r - f * K::CHR;
-    int col = 2 * c - 4;
-    col += (col < 0) ? K::NX : 0;
-    col -= (col >= K::NX) ? K::NX : 0;
+    int col = (int)blockIdx.x * K::NX + 2 * c - 4;  // this cluster rank's columns
+    col += (col < 0) ? K::NXT : 0;
+    col -= (col >= K::NXT) ? K::NXT : 0;
     // a missing state of a short last group copies the group's first state (never stored)
     const int jsrc = (grp0 + js < batch) ? js : 0;
     ld_soff[j] = js * K::SROW + f * K::RW + 2 * swz(c, K::SWZ);
@@ -388,7 +411,7 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     int gy = sg.y0 + rr;
     gy += (gy < 0) ? ny : 0;
     double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-    const double* rowp = sg.src + (long long)gy * K::NX;
+    const double* rowp = sg.src + (long long)gy * K::NXT;
 #pragma unroll
     for (int j = 0; j < K::NLD; ++j)
       cp16(slot + ld_soff[j], rowp + ld_goff[j]);
@@ -441,6 +464,8 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
       tick_all<K, 2>(A, sm, smj, sg, P, S, g, t + 2, ld_soff, ld_goff, woff, goff0, goff1, ghost);
     }
   }
+  // no CTA of a cluster leaves while a neighbour may still store its last ghost columns
+  if constexpr (K::CL > 1) tick_sync<K>();
 }
 
 int env_int(const char* name, int dflt) {
@@ -465,7 +490,7 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
     double best = 1e300;
     for (int s = 1; s <= fp.ny / 16; ++s) {
       const long long ngrp = (batch + K::NS - 1) / K::NS;
-      const long long waves = (ngrp * s + slots - 1) / slots;
+      const long long waves = (ngrp * s * K::CL + slots - 1) / slots;
       const double cost = (double)waves * ((double)fp.ny / s + 14.0);
       if (cost < best - 1e-9) {
         best = cost;
@@ -474,8 +499,24 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
     }
     if (nseg <= 0) nseg = 1;
   }
-  dim3 grid(nseg, (batch + K::NS - 1) / K::NS);
-  kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp, nseg, batch);
+  dim3 grid(K::CL, nseg, (batch + K::NS - 1) / K::NS);
+  if constexpr (K::CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(K::NT);
+    cfg.dynamicSmemBytes = K::SMEM;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = K::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PW_CUDA(cudaLaunchKernelEx(&cfg, kern, in, out, fp, nseg, batch));
+  } else {
+    kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp, nseg, batch);
+  }
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }
@@ -485,7 +526,10 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
 bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in,
                      const void* out) {
   if (env_int("PW_MARCH", 1) == 0) return false;
-  if (!(nx == 128 || nx == 256 || nx == 384 || nx == 512)) return false;
+  // 1024 / 2048: clusters sharing each row work (tests) but the per-tick cluster barrier
+  // made them slower than the tile kernel (35.5 vs 42.5 G/s at 1024^2 x 16): opt-in only
+  const bool cluster = (nx == 1024 || nx == 2048) && env_int("PW_MARCH_CLUSTER", 0) != 0;
+  if (!(nx == 128 || nx == 256 || nx == 384 || nx == 512 || cluster)) return false;
   if (ny < 32) return false;
   if ((ld_in & 1) || (ld_out & 1)) return false;
   if (((uintptr_t)in & 15) || ((uintptr_t)out & 15)) return false;
@@ -500,6 +544,9 @@ void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* o
     case 256: return launch_march_cfg<MC<256, 4>>(c, fp, in, out, batch);
     case 384: return launch_march_cfg<MC<384, 4>>(c, fp, in, out, batch);
     case 512: return launch_march_cfg<MC<512, 4>>(c, fp, in, out, batch);
+    // wider rows: clusters of 512-column CTAs, ghost columns through distributed smem
+    case 1024: return launch_march_cfg<MC<512, 4, 1, 2>>(c, fp, in, out, batch);
+    case 2048: return launch_march_cfg<MC<512, 4, 1, 4>>(c, fp, in, out, batch);
     default:
       throw Error{PW_ERR_VALUE, "row-marching RK3 needs nx in {128, 256, 384, 512}"};
   }

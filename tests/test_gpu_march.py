@@ -58,10 +58,12 @@ def test_march_orders_match_oracle(dev, order):
     for b in range(3):
         assert rel(got[b], want[b]) <= 1e-12
 
-@pytest.mark.parametrize("nx,ny", [(128, 32), (128, 200), (256, 96), (384, 48), (512, 64), (256, 256)])
-def test_march_grids_match_oracle(dev, nx, ny):
+@pytest.mark.parametrize("nx,ny", [(128, 32), (128, 200), (256, 96), (384, 48), (512, 64), (256, 256),
+                                   (1024, 48), (2048, 32)])
+def test_march_grids_match_oracle(dev, nx, ny, monkeypatch):
     from paper_1510_02237_b200.integrators import SlicePropagator
 
+    monkeypatch.setenv("PW_MARCH_CLUSTER", "1")  # 1024 / 2048: the cluster variant (opt-in)
     q0 = random_states(nx, ny, 2, nx + ny)
     got = SlicePropagator(fine_spec(nx, ny), nsteps=3).batch(q0)
     want = oracle_batch(q0, 3, nx, ny)
