@@ -10,5 +10,7 @@ done
 if [ -n "$AB_ENV" ]; then
   echo "== $AB_ENV" >> $L
   env $AB_ENV timeout 300 python -m pytest tests/test_gpu_march.py -q -x -m gpu 2>&1 | tail -1 >> $L
-  env $AB_ENV timeout 120 python scripts/microbench.py fine 2>&1 | grep -E "10 step" >> $L
+  for w in fine fine512; do
+    env $AB_ENV timeout 120 python scripts/microbench.py $w 2>&1 | grep -E "rel err|10 step|4 steps" >> $L
+  done
 fi
