@@ -99,6 +99,17 @@ int pw_prop_destroy(pw_prop* prop);
 long long pw_prop_dim(const pw_prop* prop);
 /* out[b] = P(in[b]) for b < batch; in/out device, stride ld (>= dim); in == out allowed. */
 int pw_prop_apply(pw_prop* prop, const double* in, double* out, int batch, long long ld);
+/* pw_prop_apply that also stores the result into npeer (<= 7) more buffers laid out
+ * like out (same ld): the slice-sharded fine sweep's all-gather of end states
+ * (replaces the gather of _fine_all's results, parareal.py:62-65, across
+ * ranks). peer_out[i] are device pointers usable from this context: other ranks'
+ * buffers mapped by pw_ipc_open (NVLink peer memory) or local buffers. For the
+ * row-marching RK3 grids (nx 128/256/384/512) the last step's kernel stores every
+ * output row to all of them as it is produced; otherwise the result is copied
+ * afterwards (cudaMemcpy2DAsync, peer to peer). Enqueued on the context stream: the
+ * caller synchronises and runs a cross-rank barrier before the peers read. */
+int pw_prop_apply_to_peers(pw_prop* prop, const double* in, double* out, int batch, long long ld,
+                           int npeer, double* const* peer_out);
 
 /* ---- Krylov subspace: subspace.Subspace (subspace.py:31-98) ----------- */
 /* capacity: max snapshot columns kept (the reference keeps all). */
@@ -183,6 +194,17 @@ int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards);
  * Replaces src/subspace.py:60-74 (the scipy qr of all snapshots) in that setting.
  * on = 0 (default; env PW_TSQR) keeps the replicated factorisation. */
 int pw_ctx_set_tsqr(pw_ctx* ctx, int on);
+
+/* ---- peer memory (CUDA IPC) for pw_prop_apply_to_peers -------------------
+ * pw_ipc_alloc: bytes of device memory of its own (cudaMalloc) and its 64-byte
+ * IPC handle, to send to the other ranks; pw_ipc_free releases it.
+ * pw_ipc_open maps another process's handle on this context's device (NVLink peer
+ * access enabled lazily); pw_ipc_close unmaps it. Same-process buffers need no
+ * mapping: pass their pointers directly. */
+int pw_ipc_alloc(pw_ctx* ctx, long long bytes, void** ptr, unsigned char handle[64]);
+int pw_ipc_free(pw_ctx* ctx, void* ptr);
+int pw_ipc_open(pw_ctx* ctx, const unsigned char handle[64], void** ptr);
+int pw_ipc_close(pw_ctx* ctx, void* ptr);
 
 /* ---- memory helper ------------------------------------------------------
  * stream-ordered copy of nbytes between any host/device pointers (UVA,

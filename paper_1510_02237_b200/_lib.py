@@ -67,6 +67,12 @@ SIGNATURES = [
     ("pw_prop_destroy", ctypes.c_int, [c_vp]),
     ("pw_prop_dim", ctypes.c_longlong, [c_vp]),
     ("pw_prop_apply", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong]),
+    ("pw_prop_apply_to_peers", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong,
+                                              ctypes.c_int, ctypes.POINTER(c_vp)]),
+    ("pw_ipc_alloc", ctypes.c_int, [c_vp, ctypes.c_longlong, ctypes.POINTER(c_vp), ctypes.c_char_p]),
+    ("pw_ipc_free", ctypes.c_int, [c_vp, c_vp]),
+    ("pw_ipc_open", ctypes.c_int, [c_vp, ctypes.c_char_p, ctypes.POINTER(c_vp)]),
+    ("pw_ipc_close", ctypes.c_int, [c_vp, c_vp]),
     ("pw_basis_create", ctypes.c_int, [c_vp, ctypes.c_longlong, ctypes.c_double, ctypes.c_int,
                                        ctypes.POINTER(c_vp)]),
     ("pw_basis_destroy", ctypes.c_int, [c_vp]),

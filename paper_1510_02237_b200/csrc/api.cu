@@ -160,12 +160,15 @@ bool use_fused(const pw_prop* P) {
          pw::fused_supported(P->desc.nx, P->desc.ny);
 }
 
-void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long ld) {
+// Returns true when the last fused step already stored the result into the npeer
+// peer buffers (row-marching epilogue); otherwise prop_apply copies it there.
+bool prop_apply_impl(pw_prop* P, const double* in, double* out, int batch, long long ld, int npeer,
+                     double* const* peers) {
   Ctx& c = P->ctx->c;
   const long long d = P->dim;
   PW_CHECK(batch >= 0, PW_ERR_VALUE, "batch must be non-negative");
   PW_CHECK(ld >= d, PW_ERR_VALUE, "ld must be >= state dimension");
-  if (batch == 0) return;
+  if (batch == 0) return true;
   if (P->kind == 1) {
     const double* src = in;
     if (in == out) {
@@ -174,13 +177,13 @@ void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long 
       src = t;
     }
     gemm(c, false, false, d, batch, d, 1.0, P->A.p, d, src, src == in ? ld : d, 0.0, out, ld);
-    return;
+    return false;
   }
   const pw_pde_desc& D = P->desc;
   const int nsteps = D.nsteps;
   if (nsteps == 0) {
     copy_cols(c, out, ld, in, ld, d, batch);
-    return;
+    return false;
   }
   if (use_fused(P)) {
     // ping-pong so that the last step lands in `out`; in != dst always
@@ -193,6 +196,7 @@ void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long 
       ld_src = d;
     }
     double* tmp = P->t2.ensure(c, (size_t)d * batch);
+    bool peers_done = false;
     for (int s = 0; s < nsteps; ++s) {
       const bool to_out = ((nsteps - 1 - s) % 2) == 0;
       double* dst = to_out ? out : tmp;
@@ -200,11 +204,18 @@ void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long 
       pw::FusedParams fp = P->fp;
       fp.ld_in = ld_src;
       fp.ld_out = ld_dst;
+      if (s == nsteps - 1 && npeer > 0 && !P->vadv && pw::march_peer_capable(fp.nx) &&
+          pw::march_supported(fp.nx, fp.ny, ld_src, ld_dst, src, dst)) {
+        fp.npeer = npeer;
+        for (int i = 0; i < npeer; ++i)
+          fp.peer_delta[i] = (long long)((uintptr_t)peers[i] - (uintptr_t)out);
+        peers_done = true;
+      }
       pw::launch_rk3_fused(c, fp, src, dst, batch, P->vadv);
       src = dst;
       ld_src = ld_dst;
     }
-    return;
+    return peers_done;
   }
   // reference-order kernels, in place on `out`
   copy_cols(c, out, ld, in, ld, d, batch);
@@ -221,6 +232,18 @@ void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long 
     double* w = P->work.ensure(c, pw::fefb_exact_work_doubles(P->ex, batch));
     pw::launch_fefb_exact(c, P->ex, out, batch, ld, nsteps, D.h, D.n_sound, w);
   }
+  return false;
+}
+
+void prop_apply(pw_prop* P, const double* in, double* out, int batch, long long ld, int npeer = 0,
+                double* const* peers = nullptr) {
+  PW_CHECK(npeer >= 0 && npeer <= pw::kMaxPeers, PW_ERR_VALUE, "npeer must be in [0, 7]");
+  for (int i = 0; i < npeer; ++i) PW_CHECK(peers && peers[i], PW_ERR_VALUE, "NULL peer buffer");
+  if (prop_apply_impl(P, in, out, batch, ld, npeer, peers) || batch == 0) return;
+  Ctx& c = P->ctx->c;
+  for (int i = 0; i < npeer; ++i)  // not fused: copy-engine stores into each peer (P2P)
+    PW_CUDA(cudaMemcpy2DAsync(peers[i], (size_t)ld * 8, out, (size_t)ld * 8, (size_t)P->dim * 8, batch,
+                              cudaMemcpyDeviceToDevice, c.stream));
 }
 
 }  // namespace
@@ -992,6 +1015,62 @@ int pw_prop_apply(pw_prop* prop, const double* in, double* out, int batch, long 
   return guarded([&] {
     PW_CHECK(prop && in && out, PW_ERR_VALUE, "NULL argument");
     prop_apply(prop, in, out, batch, ld);
+  });
+}
+
+int pw_prop_apply_to_peers(pw_prop* prop, const double* in, double* out, int batch, long long ld, int npeer,
+                           double* const* peer_out) {
+  return guarded([&] {
+    PW_CHECK(prop && in && out, PW_ERR_VALUE, "NULL argument");
+    prop_apply(prop, in, out, batch, ld, npeer, peer_out);
+  });
+}
+
+int pw_ipc_alloc(pw_ctx* ctx, long long bytes, void** ptr, unsigned char handle[64]) {
+  return guarded([&] {
+    PW_CHECK(ctx && ptr && handle && bytes > 0, PW_ERR_VALUE, "bad argument");
+    PW_CUDA(cudaSetDevice(ctx->c.device));
+    void* p = nullptr;
+    PW_CUDA(cudaMalloc(&p, (size_t)bytes));  // own allocation: IPC handles name its base
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      PW_CUDA(e);
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &h, 64);
+    *ptr = p;
+  });
+}
+
+int pw_ipc_free(pw_ctx* ctx, void* ptr) {
+  return guarded([&] {
+    PW_CHECK(ctx, PW_ERR_VALUE, "NULL context");
+    if (!ptr) return;
+    PW_CUDA(cudaSetDevice(ctx->c.device));
+    PW_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    PW_CUDA(cudaFree(ptr));
+  });
+}
+
+int pw_ipc_open(pw_ctx* ctx, const unsigned char handle[64], void** ptr) {
+  return guarded([&] {
+    PW_CHECK(ctx && handle && ptr, PW_ERR_VALUE, "NULL argument");
+    PW_CUDA(cudaSetDevice(ctx->c.device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    PW_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int pw_ipc_close(pw_ctx* ctx, void* ptr) {
+  return guarded([&] {
+    PW_CHECK(ctx, PW_ERR_VALUE, "NULL context");
+    if (!ptr) return;
+    PW_CUDA(cudaSetDevice(ctx->c.device));
+    PW_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    PW_CUDA(cudaIpcCloseMemHandle(ptr));
   });
 }
 

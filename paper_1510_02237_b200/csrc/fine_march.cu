@@ -43,9 +43,12 @@ namespace cg = cooperative_groups;
 namespace pw {
 namespace {
 
-template <int NX_, int BX_, int NS_ = 1, int CL_ = 1>
+template <int NX_, int BX_, int NS_ = 1, int CL_ = 1, int PR_ = 0>
 struct MC {
   static constexpr int NX = NX_, BX = BX_, NS = NS_;  // NS states side by side per CTA
+  // PR_: stage 3 also stores every output row into the peers' buffers (FusedParams
+  // npeer / peer_delta): the slice all-gather fused into the last RK3 step's epilogue
+  static constexpr bool PEERS = PR_ != 0;
   // CL CTAs of one thread-block cluster share each grid row (NX columns each; ghost
   // columns exchanged through distributed shared memory): rows of NXT = CL * NX cells
   static constexpr int CL = CL_, NXT = CL * NX;
@@ -275,11 +278,28 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
         *reinterpret_cast<double2*>(o + c) = make_double2(A.u[U0][c], A.u[U0][c + 1]);
         *reinterpret_cast<double2*>(o + 2 * sg.n + c) = make_double2(A.p[U0][c], A.p[U0][c + 1]);
       }
+      if constexpr (K::PEERS) {
+        for (int i = 0; i < P.npeer; ++i) {  // NVLink stores into the peers' copies
+          double* q = reinterpret_cast<double*>(reinterpret_cast<char*>(o) + P.peer_delta[i]);
+#pragma unroll
+          for (int c = 0; c < BX; c += 2) {
+            __stcg(reinterpret_cast<double2*>(q + c), make_double2(A.u[U0][c], A.u[U0][c + 1]));
+            __stcg(reinterpret_cast<double2*>(q + 2 * sg.n + c), make_double2(A.p[U0][c], A.p[U0][c + 1]));
+          }
+        }
+      }
     }
     if (sg.st_ok && k - 2 >= 0 && k - 2 < sg.TY) {
       double* o = sg.dst + sg.n + (long long)(sg.y0 + k - 2) * K::NXT + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) *reinterpret_cast<double2*>(o + c) = make_double2(A.v[0][c], A.v[0][c + 1]);
+      if constexpr (K::PEERS) {
+        for (int i = 0; i < P.npeer; ++i) {
+          double* q = reinterpret_cast<double*>(reinterpret_cast<char*>(o) + P.peer_delta[i]);
+#pragma unroll
+          for (int c = 0; c < BX; c += 2) __stcg(reinterpret_cast<double2*>(q + c), make_double2(A.v[0][c], A.v[0][c + 1]));
+        }
+      }
     }
   }
 }
@@ -536,7 +556,18 @@ bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const vo
   return true;
 }
 
+bool march_peer_capable(int nx) { return nx == 128 || nx == 256 || nx == 384 || nx == 512; }
+
 void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
+  if (fp.npeer > 0) {
+    switch (fp.nx) {
+      case 128: return launch_march_cfg<MC<128, 4, 1, 1, 1>>(c, fp, in, out, batch);
+      case 256: return launch_march_cfg<MC<256, 4, 1, 1, 1>>(c, fp, in, out, batch);
+      case 384: return launch_march_cfg<MC<384, 4, 1, 1, 1>>(c, fp, in, out, batch);
+      case 512: return launch_march_cfg<MC<512, 4, 1, 1, 1>>(c, fp, in, out, batch);
+      default: throw Error{PW_ERR_VALUE, "peer stores need nx in {128, 256, 384, 512}"};
+    }
+  }
   switch (fp.nx) {
     case 128: return launch_march_cfg<MC<128, 4>>(c, fp, in, out, batch);
     // MC<256, 4, 2> (two states per 12-warp CTA) passes the parity tests but spills and

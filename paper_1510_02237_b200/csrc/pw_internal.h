@@ -74,9 +74,14 @@ struct StageCoef {
   double pu;      // -beta cs sx     dp += pu (u_{i+1} - u_{i-1})
   double pv;      // -beta cs sy     dp += pv a_i
 };
+constexpr int kMaxPeers = 7;  // peers of one rank in an 8-GPU NVSwitch node
 struct FusedParams {
   int nx, ny;
   int zmask = 0;  // always 0: (tick & zmask) keeps per-tick coefficient loads in the loop
+  // fused slice all-gather (pw_prop_apply_to_peers): the row-marching kernel also stores
+  // each output row at out + peer_delta[i] bytes, i < npeer (peer-mapped buffers)
+  int npeer = 0;
+  long long peer_delta[kMaxPeers] = {};
   long long ld_in, ld_out;
   double sx, sy;  // 0.5/dx, 0.5/dy
   StageCoef st[3];
@@ -144,6 +149,7 @@ bool fused_supported(int nx, int ny);
 bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in,
                      const void* out);
 void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch);
+bool march_peer_capable(int nx);  // launch_rk3_march handles fp.npeer > 0 for this nx
 
 // linalg.cu
 void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,

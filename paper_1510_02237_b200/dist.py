@@ -16,8 +16,17 @@ all-gather of qn rows per step, and (pw_ctx_set_tsqr) the subspace is factored
 by TSQR: local Householder QR of each rank's rows, one all-gather of the m x m
 R factors, their QR replicated.  ``tsqr`` below is that decomposition on torch
 tensors (the gloo tests check it against the unsharded QR).
+
+``FusedShardedFine`` is the NVLink form of the slice all-gather: the last RK3
+step's kernel stores every output row into all ranks' gather buffers (peer
+memory mapped by CUDA IPC, ``PeerGather``), so the exchange overlaps the step's
+compute and no NCCL call sits on the data path.  ``kse_sweep(..., group=)`` uses
+it under the NCCL backend (PW_FUSED_GATHER=0 selects the NCCL all-gather).
 """
 from __future__ import annotations
+
+import ctypes
+import os
 
 import torch
 import torch.distributed as tdist
@@ -97,6 +106,114 @@ class ShardedFine:
         return out
 
     # the oracle sweeps (tests) call fine.batch(states) on numpy arrays
+    def batch(self, states):
+        t = torch.as_tensor(states)
+        return self(t).cpu().numpy()
+
+
+class PeerGather:
+    """Every rank's gather buffer of `numel` doubles, mapped on every rank.
+
+    Collective over `group`.  Rank r allocates its buffer with pw_ipc_alloc and
+    all-gathers (pid, address, IPC handle).  Buffers of other processes are mapped
+    with pw_ipc_open (NVLink peer memory on an NVSwitch node; CUDA IPC also maps
+    another process's buffer on the same GPU, which the tests use).  Buffers of the
+    same process (thread ranks) are used directly.
+    """
+
+    def __init__(self, ctx, numel: int, group=None):
+        from . import _lib
+
+        self.ctx, self.group, self.numel = ctx, group, int(numel)
+        lib = ctx.lib
+        ptr, handle = _lib.c_vp(), ctypes.create_string_buffer(64)
+        _lib.check(lib.pw_ipc_alloc(ctx.handle, self.numel * 8, ctypes.byref(ptr), handle))
+        self.ptr = int(ptr.value)
+        self.local = device_vector(self.ptr, self.numel, torch.device("cuda", ctx.device))
+        world, rank = tdist.get_world_size(group), tdist.get_rank(group)
+        info = [None] * world
+        tdist.all_gather_object(info, (os.getpid(), self.ptr, handle.raw), group=group)
+        self.peer_ptrs, self._mapped = [], []
+        for r, (pid, addr, h) in enumerate(info):
+            if r == rank:
+                continue
+            if pid == os.getpid():
+                self.peer_ptrs.append(int(addr))
+            else:
+                q = _lib.c_vp()
+                _lib.check(lib.pw_ipc_open(ctx.handle, h, ctypes.byref(q)))
+                self.peer_ptrs.append(int(q.value))
+                self._mapped.append(int(q.value))
+
+    def close(self):
+        """Collective: unmap the peers' buffers, then free this rank's once nobody maps it."""
+        from . import _lib
+
+        if self.ptr is None:
+            return
+        lib = self.ctx.lib
+        tdist.barrier(group=self.group)
+        for q in self._mapped:
+            _lib.check(lib.pw_ipc_close(self.ctx.handle, _lib.c_vp(q)))
+        tdist.barrier(group=self.group)
+        _lib.check(lib.pw_ipc_free(self.ctx.handle, _lib.c_vp(self.ptr)))
+        self.ptr, self.peer_ptrs, self._mapped, self.local = None, [], [], None
+
+
+class FusedShardedFine:
+    """ShardedFine with the all-gather fused into the fine kernel.
+
+    Rank r propagates its block of slices with ``prop.apply_to_peers``
+    (pw_prop_apply_to_peers).  The last RK3 step of the row-marching kernel stores
+    each output row into this rank's gather buffer and into every peer's, over
+    NVLink, while the other rows are still being computed.  There is no NCCL call
+    on the data path.  Two barriers per call order the buffer reuse: one before the
+    stores (everyone has read the previous contents) and one after (every rank's
+    stores have landed).
+    """
+
+    def __init__(self, prop, group=None):
+        self.prop = prop
+        self.group = group
+        self._buf = None
+
+    @property
+    def world(self):
+        return tdist.get_world_size(self.group) if tdist.is_initialized() else 1
+
+    @property
+    def rank(self):
+        return tdist.get_rank(self.group) if tdist.is_initialized() else 0
+
+    def _buffer(self, numel):
+        if self._buf is None or self._buf.numel < numel:
+            if self._buf is not None:
+                self._buf.close()
+            self._buf = PeerGather(self.prop.ctx, numel, self.group)
+        return self._buf
+
+    def close(self):
+        if self._buf is not None:
+            self._buf.close()
+            self._buf = None
+
+    def __call__(self, qk: torch.Tensor) -> torch.Tensor:
+        world, rank = self.world, self.rank
+        n, d = qk.shape
+        if world == 1:
+            return self.prop.apply(qk)
+        buf = self._buffer(n * d)
+        lo, hi = shard_range(n, rank, world)
+        stream = torch.cuda.current_stream(qk.device)
+        stream.synchronize()
+        tdist.barrier(group=self.group)
+        if hi > lo:
+            out = buf.local[lo * d:hi * d].view(hi - lo, d)
+            self.prop.apply_to_peers(qk[lo:hi], out, [p + lo * d * 8 for p in buf.peer_ptrs])
+        stream.synchronize()
+        tdist.barrier(group=self.group)
+        return buf.local[: n * d].view(n, d).clone()
+
     def batch(self, states):
         t = torch.as_tensor(states)
         return self(t).cpu().numpy()

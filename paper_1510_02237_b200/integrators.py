@@ -124,6 +124,21 @@ class DevicePropagator:
                                               x.shape[0], self.dim))
         return out
 
+    def apply_to_peers(self, x: torch.Tensor, out: torch.Tensor, peer_ptrs) -> torch.Tensor:
+        """apply(x, out) that also stores the result at each device address in peer_ptrs
+        (buffers laid out like `out`, e.g. other ranks' buffers mapped by dist.PeerGather):
+        pw_prop_apply_to_peers.  Enqueued, no sync."""
+        self.ctx.bind_stream()
+        if x.dim() != 2 or x.shape[1] != self.dim or x.dtype != torch.float64 or not x.is_cuda:
+            raise ValueError("apply_to_peers expects a (batch, dim) float64 CUDA tensor")
+        if out.shape != x.shape or out.stride(1) != 1 or out.stride(0) != self.dim:
+            raise ValueError("out must be a contiguous (batch, dim) tensor")
+        x = x.contiguous()
+        arr = (_lib.c_vp * max(1, len(peer_ptrs)))(*[_lib.c_vp(int(p)) for p in peer_ptrs])
+        _lib.check(self.ctx.lib.pw_prop_apply_to_peers(self.handle, _lib.ptr(x), _lib.ptr(out), x.shape[0],
+                                                       self.dim, len(peer_ptrs), arr))
+        return out
+
     def batch(self, states):
         """Host (B, d) -> host (B, d)."""
         t, _, _ = _as_device_batch(states, self.dim, self.device)
