@@ -111,6 +111,15 @@ class ShardedFine:
         return self(t).cpu().numpy()
 
 
+def same_host(group=None) -> bool:
+    """True when every rank of `group` runs on this host (CUDA IPC / NVLink peers)."""
+    import socket
+
+    names = [None] * tdist.get_world_size(group)
+    tdist.all_gather_object(names, socket.gethostname(), group=group)
+    return len(set(names)) == 1
+
+
 class PeerGather:
     """Every rank's gather buffer of `numel` doubles, mapped on every rank.
 
