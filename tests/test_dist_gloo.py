@@ -231,3 +231,30 @@ def test_sharded_fine_rows_all_to_all(world):
     assert len(results) == world
     for _, shape_ok, err in results:
         assert shape_ok and err <= 1e-12
+
+
+def _host_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_02237_b200.dist import same_host
+
+        out_q.put((rank, same_host()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_same_host_world2():
+    """The fused (peer-store) all-gather is chosen only when every rank shares the host."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert sorted(results) == [(0, True), (1, True)]
