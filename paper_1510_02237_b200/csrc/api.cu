@@ -151,6 +151,7 @@ struct pw_prop {
   bool vadv = false;
   DBuf A;  // dense
   DBuf t1, t2, work;
+  DBuf sync;  // persistent march: work counter + per-segment step counters (ints)
 };
 
 namespace {
@@ -196,6 +197,17 @@ bool prop_apply_impl(pw_prop* P, const double* in, double* out, int batch, long 
       ld_src = d;
     }
     double* tmp = P->t2.ensure(c, (size_t)d * batch);
+    if (npeer == 0 && nsteps >= 2 && !P->vadv && pw::march_persist_enabled(P->fp.nx) &&
+        pw::march_supported(P->fp.nx, P->fp.ny, ld_src, ld, src, out) &&
+        pw::march_supported(P->fp.nx, P->fp.ny, d, d, tmp, tmp)) {
+      int* sync = reinterpret_cast<int*>(
+          P->sync.ensure(c, (pw::march_persist_sync_ints(P->fp.ny, batch) + 1) / 2));
+      pw::FusedParams fp = P->fp;
+      fp.ld_in = ld_src;
+      fp.ld_out = ld;
+      pw::launch_rk3_march_persist(c, fp, src, out, tmp, batch, nsteps, d, sync);
+      return false;
+    }
     bool peers_done = false;
     for (int s = 0; s < nsteps; ++s) {
       const bool to_out = ((nsteps - 1 - s) % 2) == 0;

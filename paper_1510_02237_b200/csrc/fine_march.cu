@@ -38,6 +38,8 @@
 
 #include "pw_internal.h"
 
+#include <algorithm>
+
 namespace cg = cooperative_groups;
 
 namespace pw {
@@ -91,6 +93,13 @@ __device__ __forceinline__ void tick_sync() {
   } else {
     bar_sync();
   }
+}
+
+// this CTA's rank in its cluster (0 without clusters: blockIdx.x is then free)
+template <class K>
+__device__ __forceinline__ int crank() {
+  if constexpr (K::CL > 1) return (int)blockIdx.x;
+  else return 0;
 }
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
@@ -270,7 +279,7 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
       *reinterpret_cast<double2*>(o2 + K::RW + goff1) = make_double2(gv[2], gv[3]);
     }
   } else {
-    const int x = (int)blockIdx.x * K::NX + g * BX;
+    const int x = crank<K>() * K::NX + g * BX;
     if (sg.st_ok && k - 1 >= 0 && k - 1 < sg.TY) {
       double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NXT + x;
 #pragma unroll
@@ -392,19 +401,20 @@ __device__ __forceinline__ void stage_loop(double* sm, double* smj, const Seg& s
   }
 }
 
+// One CTA's march: segment segi of state group grpz (blockIdx.y / .z of the plain
+// launch; a work item of the persistent one).  ld_in / ld_out override P's (per step).
 template <class K>
-__global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double* __restrict__ in,
-                                                                  double* __restrict__ out,
-                                                                  FusedParams P, int nseg, int batch) {
-  extern __shared__ __align__(16) double sm[];
+__device__ __forceinline__ void march_body(double* sm, const double* __restrict__ in, double* __restrict__ out,
+                                           const FusedParams& P, long long ld_in, long long ld_out, int nseg,
+                                           int batch, int segi, int grpz) {
   const int ny = P.ny;
   Seg sg;
   sg.n = (long long)K::NXT * ny;
   sg.ny = ny;
-  sg.y0 = (int)((long long)blockIdx.y * ny / nseg);
-  sg.TY = (int)((long long)(blockIdx.y + 1) * ny / nseg) - sg.y0;
-  const int grp0 = blockIdx.z * K::NS;  // first state of this CTA
-  sg.src = in + (long long)grp0 * P.ld_in;
+  sg.y0 = (int)((long long)segi * ny / nseg);
+  sg.TY = (int)((long long)(segi + 1) * ny / nseg) - sg.y0;
+  const int grp0 = grpz * K::NS;  // first state of this CTA
+  sg.src = in + (long long)grp0 * ld_in;
   const int tid = threadIdx.x;
   // q-row copy assignment: chunk e = tid + j*NT of the 3 x CHR chunks of a row
   int ld_soff[K::NLD];
@@ -418,13 +428,13 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
     const int js = e / (3 * K::CHR);
     const int r = e - js * 3 * K::CHR;
     const int f = r / K::CHR, c = r - f * K::CHR;
-    int col = (int)blockIdx.x * K::NX + 2 * c - 4;  // this cluster rank's columns
+    int col = crank<K>() * K::NX + 2 * c - 4;  // this cluster rank's columns
     col += (col < 0) ? K::NXT : 0;
     col -= (col >= K::NXT) ? K::NXT : 0;
     // a missing state of a short last group copies the group's first state (never stored)
     const int jsrc = (grp0 + js < batch) ? js : 0;
     ld_soff[j] = js * K::SROW + f * K::RW + 2 * swz(c, K::SWZ);
-    ld_goff[j] = (typename K::GOff)((long long)jsrc * P.ld_in + f * sg.n + col);
+    ld_goff[j] = (typename K::GOff)((long long)jsrc * ld_in + f * sg.n + col);
   }
   // prologue: q rows -6 and -5 (ticks 0 and 1 of stage 1)
   for (int rr = -6; rr <= -5; ++rr) {
@@ -444,7 +454,7 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   // state: compile-time 0, so dst and the ring base stay CTA-uniform)
   const int jst = K::NS > 1 ? (tid - S * K::G) / K::GS : 0;
   const int g = tid - S * K::G - jst * K::GS;
-  sg.dst = out + (long long)(grp0 + jst) * P.ld_out;
+  sg.dst = out + (long long)(grp0 + jst) * ld_out;
   sg.st_ok = K::NS > 1 ? grp0 + jst < batch : true;
   double* smj = sm + jst * K::SROW;  // ring rows of this thread's state
   constexpr int BX = K::BX;
@@ -486,6 +496,73 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double*
   }
   // no CTA of a cluster leaves while a neighbour may still store its last ghost columns
   if constexpr (K::CL > 1) tick_sync<K>();
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_kernel(const double* __restrict__ in,
+                                                                  double* __restrict__ out,
+                                                                  FusedParams P, int nseg, int batch) {
+  extern __shared__ __align__(16) double sm[];
+  march_body<K>(sm, in, out, P, P.ld_in, P.ld_out, nseg, batch, blockIdx.y, blockIdx.z);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Persistent march over all nsteps RK3 steps (PW_MARCH_PERSIST): one launch, CTAs take
+// work items (step, state, segment) in order from an atomic counter.  Item (s, b, j)
+// reads step s-1's rows of segments j-1..j+1 of state b (the 6-row y halo) and
+// overwrites the buffer step s-2 wrote, which those same three items read: so it waits
+// until done[b][j-1..j+1] >= s.  Items are taken in order, so every item waited on was
+// taken by a running CTA: no deadlock, and no wave quantisation between steps.
+// sync[0]: the counter; sync[1 + b * nseg + j]: steps finished by segment j of state b.
+template <class K>
+__global__ void __launch_bounds__(K::NT, K::MINB) rk3_march_persist_kernel(
+    const double* __restrict__ in, double* out, double* tmp, FusedParams P, int nseg, int batch, int nsteps,
+    long long d, int* sync) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_item;
+  const int per_step = nseg * batch;
+  const long long total = (long long)per_step * nsteps;
+  int* done = sync + 1;
+  for (;;) {
+    __syncthreads();  // s_item of the previous item is no longer read
+    if (threadIdx.x == 0) s_item = atomicAdd(sync, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) break;
+    const int s = item / per_step;
+    const int r = item - s * per_step;
+    const int b = r / nseg, j = r - b * nseg;
+    if (s > 0 && threadIdx.x < 3) {  // three neighbours, one thread each
+      int jj = j + (int)threadIdx.x - 1;
+      jj += (jj < 0) ? nseg : 0;
+      jj -= (jj >= nseg) ? nseg : 0;
+      const int* f = done + b * nseg + jj;
+      long long spins = 0;
+      while (ld_acquire(f) < s) {
+        __nanosleep(100);
+        if (++spins > (1LL << 26)) __trap();  // a broken dependency fails, never hangs
+      }
+    }
+    __syncthreads();
+    // ping-pong so that the last step lands in out (as prop_apply)
+    const bool to_out = ((nsteps - 1 - s) % 2) == 0;
+    double* dst = to_out ? out : tmp;
+    const long long ld_dst = to_out ? P.ld_out : d;
+    const double* src = s == 0 ? in : (to_out ? tmp : out);
+    const long long ld_src = s == 0 ? P.ld_in : (to_out ? d : P.ld_out);
+    march_body<K>(sm, src, dst, P, ld_src, ld_dst, nseg, batch, j, b);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(done + b * nseg + j, s + 1);
+  }
 }
 
 int env_int(const char* name, int dflt) {
@@ -541,7 +618,58 @@ void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* o
   PW_LAUNCH_CHECK();
 }
 
+template <class K>
+void launch_march_persist_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp,
+                              int batch, int nsteps, long long d, int* sync) {
+  auto kern = rk3_march_persist_kernel<K>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
+    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
+  // segments per state: no waves here, so minimise ticks per item x max(1, items / slots)
+  // (the second factor: fewer items than CTA slots leave slots idle)
+  int nseg = env_int("PW_MARCH_NSEG", 0);
+  if (nseg <= 0) {
+    double best = 1e300;
+    for (int s = 1; s <= fp.ny / 16; ++s) {
+      const double items = (double)batch * s;
+      const double cost = ((double)fp.ny / s + 14.0) * std::max(1.0, items / (double)slots);
+      if (cost < best - 1e-9) {
+        best = cost;
+        nseg = s;
+      }
+    }
+    if (nseg <= 0) nseg = 1;
+  }
+  const long long items = (long long)batch * nseg * nsteps;
+  const int grid = (int)std::min<long long>(slots, items);
+  PW_CUDA(cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)batch * nseg), c.stream));
+  kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, tmp, fp, nseg, batch, nsteps, d, sync);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
 }  // namespace
+
+bool march_persist_enabled(int nx) {
+  return env_int("PW_MARCH_PERSIST", 0) != 0 && (nx == 128 || nx == 256 || nx == 384 || nx == 512);
+}
+
+size_t march_persist_sync_ints(int ny, int batch) { return 1 + (size_t)batch * (size_t)(ny / 16 + 1); }
+
+void launch_rk3_march_persist(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp,
+                              int batch, int nsteps, long long d, int* sync) {
+  switch (fp.nx) {
+    case 128: return launch_march_persist_cfg<MC<128, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 256: return launch_march_persist_cfg<MC<256, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 384: return launch_march_persist_cfg<MC<384, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 512: return launch_march_persist_cfg<MC<512, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    default: throw Error{PW_ERR_VALUE, "persistent march needs nx in {128, 256, 384, 512}"};
+  }
+}
 
 bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in,
                      const void* out) {

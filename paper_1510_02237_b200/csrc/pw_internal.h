@@ -150,6 +150,12 @@ bool march_supported(int nx, int ny, long long ld_in, long long ld_out, const vo
                      const void* out);
 void launch_rk3_march(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch);
 bool march_peer_capable(int nx);  // launch_rk3_march handles fp.npeer > 0 for this nx
+// persistent march over all steps of one propagation (PW_MARCH_PERSIST=1): one launch,
+// work items (step, state, segment) with per-segment step counters in sync
+bool march_persist_enabled(int nx);
+size_t march_persist_sync_ints(int ny, int batch);
+void launch_rk3_march_persist(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp,
+                              int batch, int nsteps, long long d, int* sync);
 
 // linalg.cu
 void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,

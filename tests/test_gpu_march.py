@@ -128,3 +128,27 @@ def test_march_strided_batch_and_blowup(dev):
     r = prop.batch(bad)
     assert not np.isfinite(r[0]).all()
     assert rel(r[1], want[1]) <= 1e-12
+
+
+@pytest.mark.parametrize("nx,ny,batch,nsteps,nseg", [
+    (256, 256, 64, 10, 0),   # c2 shape, persistent heuristic (5 segments)
+    (256, 256, 64, 7, 4),    # odd step count, the plain kernel's segments
+    (512, 96, 6, 4, 3),
+    (128, 64, 5, 3, 1),      # one segment: each item waits on itself only
+    (384, 48, 3, 2, 2),
+])
+def test_persistent_march_matches_per_step_launches(dev, monkeypatch, nx, ny, batch, nsteps, nseg):
+    """PW_MARCH_PERSIST=1: all steps in one launch with per-segment step counters.  Each
+    row is computed by the same arithmetic whatever CTA computes it, so the result is
+    bitwise equal to the per-step launches."""
+    from paper_1510_02237_b200.integrators import SlicePropagator
+
+    prop = SlicePropagator(fine_spec(nx, ny), nsteps=nsteps)
+    x = torch.as_tensor(random_states(nx, ny, batch, 31 + nx)).cuda()
+    want = prop.apply(x)
+    monkeypatch.setenv("PW_MARCH_PERSIST", "1")
+    if nseg:
+        monkeypatch.setenv("PW_MARCH_NSEG", str(nseg))
+    got = prop.apply(x)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
