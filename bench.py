@@ -49,11 +49,16 @@ C2_WORKLOAD = ("c2: 64 states x 256^2 periodic x 200 RK3 steps (CFL 0.5, order 6
                "seeded random-mode fields")
 
 
-def load_traffic():
-    """DRAM bytes per fine-kernel launch (rk3_march_kernel at c2) from the committed ncu --set full capture."""
+def load_traffic(persistent=False):
+    """DRAM bytes per fine-kernel launch at c2 from the committed ncu captures: the
+    per-step rk3_march_kernel, or (persistent) rk3_march_persist_kernel over 200 steps."""
     if os.path.exists(TRAFFIC_FILE):
         with open(TRAFFIC_FILE) as fh:
             d = json.load(fh)
+        if persistent:
+            d = d.get("persistent")
+            if not d:
+                return None, None
         return float(d["dram_bytes_per_launch"]), d.get("source")
     return None, None
 
@@ -404,10 +409,14 @@ def run_ours(args, rank, world, local_rank):
     ok = bool(torch.isfinite(pinned_out[(args.steps - 1) % 2]).all())
 
     peak, peak_kind = load_peaks()
-    launch_s = (ms_per_step * 1e-3) / STEPS_PER_SAMPLE
-    algo_bytes = BYTES_PER_CELL_UPDATE * BATCH * N_GRID * N_GRID
+    # launches of the fine kernel per timed step: 1 for the persistent march (all 200 RK3
+    # steps in one launch, the default at c2), 200 for per-step launches (PW_MARCH_PERSIST=0)
+    launches_per_step = max(1, round(launches / max(1, args.steps)))
+    launch_s = (ms_per_step * 1e-3) / launches_per_step
+    algo_bytes = BYTES_PER_CELL_UPDATE * BATCH * N_GRID * N_GRID * (STEPS_PER_SAMPLE // launches_per_step)
     achieved = algo_bytes / launch_s / 1e9
-    traffic, traffic_src = load_traffic()
+    persistent = launches_per_step == 1
+    traffic, traffic_src = load_traffic(persistent)
     fp64_peak = ctx.fp64_peak_tflops() if rank == 0 else None  # outside the timed region
     fp64_achieved = FLOP_PER_CELL_UPDATE * value / world / 1e12
 
@@ -449,7 +458,9 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "avg_launch_us": launch_s * 1e6,
-                         "kernel": "rk3_march_kernel (row-marching fused RK3; one launch per RK3 step over all 64 states)",
+                         "kernel": ("rk3_march_persist_kernel (row-marching fused RK3; one persistent launch runs "
+                                    "all 200 RK3 steps of the 64 states)" if persistent else
+                                    "rk3_march_kernel (row-marching fused RK3; one launch per RK3 step over all 64 states)"),
                          "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": (fp64_achieved / fp64_peak) if fp64_peak else None,
                                   "flop_per_cell_update": FLOP_PER_CELL_UPDATE,

@@ -50,7 +50,10 @@ struct MC {
   static constexpr int NX = NX_, BX = BX_, NS = NS_;  // NS states side by side per CTA
   // PR_: stage 3 also stores every output row into the peers' buffers (FusedParams
   // npeer / peer_delta): the slice all-gather fused into the last RK3 step's epilogue
-  static constexpr bool PEERS = PR_ != 0;
+  static constexpr bool PEERS = PR_ == 1;
+  // PR_ == 2: persistent kernel; the item's src / dst live in shared memory (seg_shared)
+  // and are re-read where used, so they take no registers across the tick loop
+  static constexpr bool PERSIST = PR_ == 2;
   // CL CTAs of one thread-block cluster share each grid row (NX columns each; ghost
   // columns exchanged through distributed shared memory): rows of NXT = CL * NX cells
   static constexpr int CL = CL_, NXT = CL * NX;
@@ -95,6 +98,25 @@ __device__ __forceinline__ void tick_sync() {
   }
 }
 
+struct SegShared {
+  const double* src;
+  double* dst;
+};
+template <class K>
+__device__ __forceinline__ SegShared& seg_shared() {
+  __shared__ SegShared sh;
+  return sh;
+}
+template <class K>
+__device__ __forceinline__ const double* seg_src(const double* reg) {
+  if constexpr (K::PERSIST) return *reinterpret_cast<const double* const volatile*>(&seg_shared<K>().src);
+  else return reg;
+}
+template <class K>
+__device__ __forceinline__ double* seg_dst(double* reg) {
+  if constexpr (K::PERSIST) return *reinterpret_cast<double* const volatile*>(&seg_shared<K>().dst);
+  else return reg;
+}
 // this CTA's rank in its cluster (0 without clusters: blockIdx.x is then free)
 template <class K>
 __device__ __forceinline__ int crank() {
@@ -281,7 +303,7 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
   } else {
     const int x = crank<K>() * K::NX + g * BX;
     if (sg.st_ok && k - 1 >= 0 && k - 1 < sg.TY) {
-      double* o = sg.dst + (long long)(sg.y0 + k - 1) * K::NXT + x;
+      double* o = seg_dst<K>(sg.dst) + (long long)(sg.y0 + k - 1) * K::NXT + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) {
         *reinterpret_cast<double2*>(o + c) = make_double2(A.u[U0][c], A.u[U0][c + 1]);
@@ -299,7 +321,7 @@ __device__ __forceinline__ void stage_tick(Acc<K>& A, double* sm, const Seg& sg,
       }
     }
     if (sg.st_ok && k - 2 >= 0 && k - 2 < sg.TY) {
-      double* o = sg.dst + sg.n + (long long)(sg.y0 + k - 2) * K::NXT + x;
+      double* o = seg_dst<K>(sg.dst) + sg.n + (long long)(sg.y0 + k - 2) * K::NXT + x;
 #pragma unroll
       for (int c = 0; c < BX; c += 2) *reinterpret_cast<double2*>(o + c) = make_double2(A.v[0][c], A.v[0][c + 1]);
       if constexpr (K::PEERS) {
@@ -330,7 +352,7 @@ __device__ __forceinline__ void tick(Acc<K>& A, double* sm, double* smj, const S
       gy += (gy < 0) ? sg.ny : 0;
       gy -= (gy >= sg.ny) ? sg.ny : 0;
       double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-      const double* rowp = sg.src + (long long)gy * K::NXT;
+      const double* rowp = seg_src<K>(sg.src) + (long long)gy * K::NXT;
 #pragma unroll
       for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
     }
@@ -361,7 +383,7 @@ __device__ __forceinline__ void tick_all(Acc<K>& A, double* sm, double* smj, con
       gy += (gy < 0) ? sg.ny : 0;
       gy -= (gy >= sg.ny) ? sg.ny : 0;
       double* slot = sm + (size_t)(rr & 7) * K::SLOT;
-      const double* rowp = sg.src + (long long)gy * K::NXT;
+      const double* rowp = seg_src<K>(sg.src) + (long long)gy * K::NXT;
 #pragma unroll
       for (int j = 0; j < K::NLD; ++j) cp16(slot + ld_soff[j], rowp + ld_goff[j]);
     }
@@ -455,6 +477,13 @@ __device__ __forceinline__ void march_body(double* sm, const double* __restrict_
   const int jst = K::NS > 1 ? (tid - S * K::G) / K::GS : 0;
   const int g = tid - S * K::G - jst * K::GS;
   sg.dst = out + (long long)(grp0 + jst) * ld_out;
+  if constexpr (K::PERSIST) {  // read back after the first tick's barrier
+    static_assert(K::NS == 1, "one state per CTA");
+    if (threadIdx.x == 0) {
+      seg_shared<K>().src = sg.src;
+      seg_shared<K>().dst = sg.dst;
+    }
+  }
   sg.st_ok = K::NS > 1 ? grp0 + jst < batch : true;
   double* smj = sm + jst * K::SROW;  // ring rows of this thread's state
   constexpr int BX = K::BX;
@@ -654,8 +683,14 @@ void launch_march_persist_cfg(Ctx& c, const FusedParams& fp, const double* in, d
 
 }  // namespace
 
+// default: on for the two-CTA-per-SM grids (nx 128 / 256), where it removes the idle
+// CTA slots of the per-step launches (c2: 58.4 vs 55.3 G/s over 200 steps); 512 measured
+// slower (57.0 vs 58.3 G/s, 4 steps).  PW_MARCH_PERSIST=1 forces it on, 0 off.
 bool march_persist_enabled(int nx) {
-  return env_int("PW_MARCH_PERSIST", 0) != 0 && (nx == 128 || nx == 256 || nx == 384 || nx == 512);
+  const int e = env_int("PW_MARCH_PERSIST", -1);
+  if (e == 0) return false;
+  if (e > 0) return nx == 128 || nx == 256 || nx == 384 || nx == 512;
+  return nx == 128 || nx == 256;
 }
 
 size_t march_persist_sync_ints(int ny, int batch) { return 1 + (size_t)batch * (size_t)(ny / 16 + 1); }
@@ -663,10 +698,10 @@ size_t march_persist_sync_ints(int ny, int batch) { return 1 + (size_t)batch * (
 void launch_rk3_march_persist(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp,
                               int batch, int nsteps, long long d, int* sync) {
   switch (fp.nx) {
-    case 128: return launch_march_persist_cfg<MC<128, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
-    case 256: return launch_march_persist_cfg<MC<256, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
-    case 384: return launch_march_persist_cfg<MC<384, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
-    case 512: return launch_march_persist_cfg<MC<512, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 128: return launch_march_persist_cfg<MC<128, 4, 1, 1, 2>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 256: return launch_march_persist_cfg<MC<256, 4, 1, 1, 2>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 384: return launch_march_persist_cfg<MC<384, 4, 1, 1, 2>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 512: return launch_march_persist_cfg<MC<512, 4, 1, 1, 2>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
     default: throw Error{PW_ERR_VALUE, "persistent march needs nx in {128, 256, 384, 512}"};
   }
 }

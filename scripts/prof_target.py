@@ -33,6 +33,12 @@ if what == "fine":
     y = p.apply(x)
     torch.cuda.synchronize()
     print("fine ok", bool(torch.isfinite(y).all()))
+elif what == "fine200":  # the bench's c2 propagation: 200 RK3 steps (one persistent launch)
+    f, _ = specs(256)
+    x = torch.as_tensor(harness.fine_batch_states(256, 64, 2001)).cuda()
+    y = SlicePropagator(f, nsteps=200).apply(x)
+    torch.cuda.synchronize()
+    print("fine200 ok", bool(torch.isfinite(y).all()))
 elif what == "coarse":
     _, c = specs(512)
     x = torch.as_tensor(harness.initial_state("c3")).cuda()[None, :].contiguous()
