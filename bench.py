@@ -49,6 +49,34 @@ C2_WORKLOAD = ("c2: 64 states x 256^2 periodic x 200 RK3 steps (CFL 0.5, order 6
                "seeded random-mode fields")
 
 
+def bench_config(world):
+    """The workload both arms report (identical dicts, so the driver can match them)."""
+    return {"workload": C2_WORKLOAD, "global_batch_states": BATCH * world, "grid": N_GRID,
+            "rk3_steps_per_state": STEPS_PER_SAMPLE, "seed": 2001,
+            "parallelism": "single GPU" if world == 1 else f"slice-sharded x{world} (independent states)"}
+
+
+# The reference's own c3 window (512^2, P=64, K=5, stable completion), timed once in the
+# survey container (8-core Xeon, numba, 8 workers): tests/golden/c3_reference.npz "seconds"
+# when that fixture carries it, else the DESIGN.md section 5 figure.
+C3_REFERENCE_WINDOW_S = 642.0
+
+
+def c3_reference_window():
+    path = os.path.join(ROOT, "tests", "golden", "c3_reference.npz")
+    try:
+        import numpy as np
+
+        with np.load(path) as z:
+            if "seconds" in z.files:
+                return {"window_s": float(z["seconds"]), "threads": int(z["threads"]) if "threads" in z.files
+                        else None, "source": "tests/golden/c3_reference.npz (reference kse_sweep, survey container)"}
+    except Exception:  # noqa: BLE001 - informational field only
+        pass
+    return {"window_s": C3_REFERENCE_WINDOW_S, "threads": 8,
+            "source": "DESIGN.md section 5 (reference kse_sweep, survey container, numba, 8 workers)"}
+
+
 def load_traffic(persistent=False):
     """DRAM bytes per fine-kernel launch at c2 from the committed ncu captures: the
     per-step rk3_march_kernel, or (persistent) rk3_march_persist_kernel over 200 steps."""
@@ -192,9 +220,10 @@ def run_reference(args, rank, world):
     line = {"metric": "fine RK-3 fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "impl": "reference", "dtype": "f64", "data": "synthetic",
-            "config": {"workload": C2_WORKLOAD, "global_batch_states": BATCH, "grid": N_GRID,
-                       "rk3_steps_per_state": STEPS_PER_SAMPLE,
-                       "implementation": "CPU port of the reference kernels (oracle/pw_oracle.c)"},
+            "config": bench_config(1),
+            "implementation": "CPU port of the reference kernels (oracle/pw_oracle.c, reference operation "
+                              "order, all host threads); the reference itself is Python and is not on the "
+                              "GPU box",
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "vs_baseline": None}
@@ -231,6 +260,8 @@ def parareal_window(name="c3", warm=True, group=None):
     if group is not None:
         torch.distributed.barrier(group)
     torch.cuda.synchronize()
+    fine.ctx.mem_stats(reset=True)
+    torch.cuda.reset_peak_memory_stats()
     t0 = time.perf_counter()
     ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm, return_device=True,
                                group=group)
@@ -257,15 +288,29 @@ def parareal_window(name="c3", warm=True, group=None):
                                       "frac": serial_bytes / tm.coarse / 1e9 / peak if tm.coarse else None,
                                       "note": "HBM bytes of the serial GEMV passes over the whole phase "
                                               "time (the latency-bound coarse G included)"}}
-    return {"workload": f"{name}: {wl.n}^2, P={wl.n_p}, K={wl.n_it} KSE-Parareal window",
+    extra = {"reference_window": c3_reference_window()} if name == "c3" else {}
+    return {**extra, "workload": f"{name}: {wl.n}^2, P={wl.n_p}, K={wl.n_it} KSE-Parareal window",
             "window_s": wall, "iteration_s": wall / wl.n_it,
             "phases_s": {"coarse_and_correction": tm.coarse, "fine": tm.fine, "qr": tm.qr},
             "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res],
             "fine_cell_updates_per_s": wl.n_p * wl.n_it * fine.nsteps * d / 3 / tm.fine if tm.fine else None,
-            "peak_device_gib": torch.cuda.max_memory_allocated() / 2**30,
+            "memory_gib": _memory_gib(fine.ctx),
             "roofline": roof, "warm": warm, "n_gpus": n_ranks,
             "parallelism": "fine sweep slice-sharded over ranks, serial correction replicated"
                            if n_ranks > 1 else "single GPU"}
+
+
+def _memory_gib(ctx):
+    """Peak device memory of the window: the library's stream-ordered pool (every basis and
+    sweep buffer) plus torch's caching allocator (inputs, outputs), and cudaMemGetInfo's
+    in-use bytes after the window (every allocator of the process)."""
+    import torch
+
+    m = ctx.mem_stats()
+    return {"library_pool_used_high": m["pool_used_high"] / 2**30,
+            "library_pool_reserved_high": m["pool_reserved_high"] / 2**30,
+            "torch_allocated_high": torch.cuda.max_memory_allocated() / 2**30,
+            "device_in_use_after": m["device_used_now"] / 2**30}
 
 
 def parareal_c3(dev_index):
@@ -408,6 +453,25 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = world * cells_per_step * args.steps / (e2e_ms * 1e-3)
     ok = bool(torch.isfinite(pinned_out[(args.steps - 1) % 2]).all())
 
+    # ---------------- the drop-in host call a reference user makes: SlicePropagator.batch on a
+    # numpy batch (pageable memory, synchronous copies, returns numpy), wall clock per call
+    q_np = q_host.numpy()
+    prop.batch(q_np)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res_np = prop.batch(q_np)
+    dropin_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([dropin_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dropin_s = float(t.item())
+    dropin = {"value": world * cells_per_step * args.steps / dropin_s, "unit": "cell-updates/s",
+              "h2d_bytes_per_step": int(q_np.nbytes), "d2h_bytes_per_step": int(res_np.nbytes),
+              "finite": bool(np.isfinite(res_np).all()),
+              "call": "SlicePropagator.batch(numpy) -- pageable host arrays, synchronous, wall clock "
+                      "(integrators.py; the reference's propagate over a batch)"}
+
     peak, peak_kind = load_peaks()
     # launches of the fine kernel per timed step: 1 for the persistent march (all 200 RK3
     # steps in one launch, the default at c2), 200 for per-step launches (PW_MARCH_PERSIST=0)
@@ -447,11 +511,9 @@ def run_ours(args, rank, world, local_rank):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": C2_WORKLOAD,
-                       "global_batch_states": BATCH * world, "grid": N_GRID,
-                       "rk3_steps_per_state": STEPS_PER_SAMPLE, "parallelism": f"slice-sharded x{world}",
-                       "l2": "256 MiB flush between timed steps; the 200 chained RK3 launches inside a "
-                             "step keep their natural L2 reuse"},
+            "config": bench_config(world),
+            "l2": "256 MiB flush between timed steps; the 200 chained RK3 steps inside a step keep "
+                  "their natural L2 reuse",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
@@ -469,6 +531,7 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_bytes_per_step": int(q_host.numel() * 8), "finite": ok,
                     "copies": "pinned host buffers; H2D/D2H on a second stream, double-buffered "
                               "against the propagation"},
+            "e2e_dropin": dropin,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

@@ -228,6 +228,14 @@ int pw_serial_step(pw_ctx* ctx, const double* g, const double* D, int rd, const 
  * half of the roofline; no reference counterpart. */
 int pw_probe_fp64_peak(pw_ctx* ctx, int iters, double* tflops);
 
+/* Device memory high-water marks of the context's device (bench reporting; no
+ * reference counterpart): the stream-ordered pool every library buffer comes from
+ * (used and reserved bytes since the last reset) and cudaMemGetInfo's in-use bytes
+ * now (all allocators of the process, torch's caching allocator included).
+ * reset != 0 restarts the pool's high-water marks after reading them. */
+int pw_mem_stats(pw_ctx* ctx, int reset, long long* pool_used_high, long long* pool_reserved_high,
+                 long long* device_used_now);
+
 #ifdef __cplusplus
 }
 #endif

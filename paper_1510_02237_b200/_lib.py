@@ -98,6 +98,8 @@ SIGNATURES = [
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
     ("pw_probe_fp64_peak", ctypes.c_int, [c_vp, ctypes.c_int, c_dp]),
+    ("pw_mem_stats", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),
+                                    ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
     ("pw_serial_step", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int,
                                       ctypes.c_longlong, ctypes.c_longlong, c_vp, c_vp]),
 ]
@@ -199,6 +201,14 @@ class Context:
         out = ctypes.c_double()
         check(self.lib.pw_probe_fp64_peak(self.handle, int(iters), ctypes.byref(out)))
         return float(out.value)
+
+
+    def mem_stats(self, reset: bool = False) -> dict:
+        """Library pool high-water marks and the device's in-use bytes (cudaMemGetInfo)."""
+        used, reserved, now = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
+        check(self.lib.pw_mem_stats(self.handle, int(bool(reset)), ctypes.byref(used), ctypes.byref(reserved),
+                                    ctypes.byref(now)))
+        return {"pool_used_high": used.value, "pool_reserved_high": reserved.value, "device_used_now": now.value}
 
 
 def ptr(t: torch.Tensor):

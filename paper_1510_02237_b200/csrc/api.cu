@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <memory>
 #include <mutex>
 
@@ -20,6 +21,23 @@
 
 using pw::Ctx;
 using pw::Error;
+
+namespace pw {
+int kernel_setup(int device, const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({device, kern});
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  per_sm = std::max(per_sm, 1);
+  cache[{device, kern}] = per_sm;
+  return per_sm;
+}
+}  // namespace pw
 
 struct pw_ctx {
   Ctx c;
@@ -216,7 +234,9 @@ bool prop_apply_impl(pw_prop* P, const double* in, double* out, int batch, long 
       pw::FusedParams fp = P->fp;
       fp.ld_in = ld_src;
       fp.ld_out = ld_dst;
-      if (s == nsteps - 1 && npeer > 0 && !P->vadv && pw::march_peer_capable(fp.nx) &&
+      bool peers_aligned = true;  // the epilogue's 16-byte peer stores need 16-byte buffers
+      for (int i = 0; i < npeer; ++i) peers_aligned &= ((uintptr_t)peers[i] & 15) == 0;
+      if (s == nsteps - 1 && npeer > 0 && peers_aligned && !P->vadv && pw::march_peer_capable(fp.nx) &&
           pw::march_supported(fp.nx, fp.ny, ld_src, ld_dst, src, dst)) {
         fp.npeer = npeer;
         for (int i = 0; i < npeer; ++i)
@@ -911,6 +931,29 @@ int pw_probe_fp64_peak(pw_ctx* ctx, int iters, double* tflops) {
   return guarded([&] {
     PW_CHECK(ctx && tflops && iters > 0, PW_ERR_VALUE, "bad argument");
     *tflops = pw::probe_fp64_tflops(ctx->c, iters);
+  });
+}
+
+int pw_mem_stats(pw_ctx* ctx, int reset, long long* pool_used_high, long long* pool_reserved_high,
+                 long long* device_used_now) {
+  return guarded([&] {
+    PW_CHECK(ctx, PW_ERR_VALUE, "ctx is NULL");
+    PW_CUDA(cudaSetDevice(ctx->c.device));
+    cudaMemPool_t pool;
+    PW_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
+    uint64_t used = 0, reserved = 0;
+    PW_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &used));
+    PW_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &reserved));
+    size_t free_b = 0, total_b = 0;
+    PW_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (pool_used_high) *pool_used_high = (long long)used;
+    if (pool_reserved_high) *pool_reserved_high = (long long)reserved;
+    if (device_used_now) *device_used_now = (long long)(total_b - free_b);
+    if (reset) {
+      uint64_t zero = 0;
+      PW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero));
+      PW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &zero));
+    }
   });
 }
 

@@ -659,14 +659,8 @@ void launch_rk3_exact(Ctx& c, const ExactParams& p, double* states, int batch, l
 template <int T>
 static void launch_tiled(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                          int nsteps, double h, int nsub, double* work) {
-  static int per_sm = -1;
   constexpr size_t smem = tiled_smem<T>();
-  if (per_sm < 0) {
-    PW_CUDA(cudaFuncSetAttribute(fefb_tiled_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fefb_tiled_coop<T>, 256, smem));
-    if (per_sm < 1) per_sm = 1;
-  }
+  const int per_sm = kernel_setup(c, fefb_tiled_coop<T>, 256, smem);
   const long long items = (long long)(p.nx / T) * (p.ny / T) * batch;
   const int cap_sm = c.coop_blocks_per_sm > 0 ? std::min(per_sm, c.coop_blocks_per_sm) : per_sm;
   int blocks = (int)std::max<long long>(1, std::min<long long>(items, (long long)c.num_sms * cap_sm));
@@ -683,13 +677,8 @@ template <int TMX, int TMY, int K, int NT, int MINB, bool FIXX, bool FIXY, int O
 static void launch_tb(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                       int nsteps, double h, int nsub, double* work, bool fill_sms = false) {
   auto kern = fefb_tb_coop<TMX, TMY, K, NT, MINB, FIXX, FIXY, ORD>;
-  static int per_sm = -1;
   constexpr size_t smem = tb_smem<TMX, TMY, K>();
-  if (per_sm < 0) {
-    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    if (per_sm < 1) per_sm = 1;
-  }
+  const int per_sm = kernel_setup(c, kern, NT, smem);
   int tiles_x = (p.nx + TMX - 1) / TMX, tiles_y = (p.ny + TMY - 1) / TMY;
   if (fill_sms) {  // as many tile rows as keep every SM busy with one tile (batch 1)
     const int want = (c.num_sms * per_sm) / std::max(1, tiles_x * batch);
@@ -749,11 +738,7 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
 // per-cell cooperative FE-FB: nsteps x (A phase unless adv_given, nsub substeps of tau)
 void launch_fefb_coop(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                       int nsteps, double tau, int nsub, double* work, int adv_given) {
-  static int max_per_sm = -1;
-  if (max_per_sm < 0) {
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, fefb_coop, kCoopThreads, 0));
-    if (max_per_sm < 1) max_per_sm = 1;
-  }
+  const int max_per_sm = kernel_setup(c, fefb_coop, kCoopThreads, 0);
   const long long total = (long long)p.nx * p.ny * batch;
   long long want = (total + kCoopThreads - 1) / kCoopThreads;
   long long cap = (long long)c.num_sms * max_per_sm;

@@ -423,11 +423,7 @@ __global__ void __launch_bounds__(K::NT, K::MINB_SMEM < 1 ? 1 : K::MINB_SMEM) rk
 template <class K>
 void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
   auto kern = rk3_fused_kernel<K>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
-    attr_set = true;
-  }
+  kernel_setup(c, kern, K::NT, K::SMEM);
   dim3 grid(fp.nx / K::TX, fp.ny / K::TY, batch);
   kern<<<grid, K::NT, K::SMEM, c.stream>>>(in, out, fp);
   c.launches += 1;

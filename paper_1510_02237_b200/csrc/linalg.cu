@@ -854,12 +854,7 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
     }
     const size_t smem = tma_nst * kTmaStageBytes + 2 * tma_nst * sizeof(uint64_t) +
                         sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 2);
-    static bool attr = false;
-    if (!attr) {
-      PW_CUDA(cudaFuncSetAttribute(combine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-      attr = true;
-    }
+    kernel_setup(c.device, reinterpret_cast<const void*>(combine_tma_kernel), kTmaThreads, 227 * 1024);
     if (!c.tma_done) {
       PW_CUDA(cudaMalloc(&c.tma_done, sizeof(unsigned int)));
       PW_CUDA(cudaMemsetAsync(c.tma_done, 0, sizeof(unsigned int), st));

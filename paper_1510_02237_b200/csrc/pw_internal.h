@@ -119,6 +119,16 @@ struct Ctx {
   void* fine_hook_user = nullptr;
 };
 
+// One-time per-(device, kernel) launch setup: raises the dynamic shared-memory limit to
+// `smem` (when above the 48 KB default) and returns the resident CTAs per SM for
+// `threads` x `smem`.  The attribute is a per-device property, so a process that drives
+// several GPUs sets it once on each (cached under a mutex; api.cu).
+int kernel_setup(int device, const void* kern, int threads, size_t smem);
+template <class F>
+inline int kernel_setup(const Ctx& c, F* kern, int threads, size_t smem) {
+  return kernel_setup(c.device, reinterpret_cast<const void*>(kern), threads, smem);
+}
+
 // ---------------------------------------------------------------- kernels (launchers)
 // exact.cu  (compiled with -fmad=false: reference operation order, bitwise)
 void launch_rk3_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,

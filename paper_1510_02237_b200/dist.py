@@ -21,7 +21,8 @@ tensors (the gloo tests check it against the unsharded QR).
 step's kernel stores every output row into all ranks' gather buffers (peer
 memory mapped by CUDA IPC, ``PeerGather``), so the exchange overlaps the step's
 compute and no NCCL call sits on the data path.  ``kse_sweep(..., group=)`` uses
-it under the NCCL backend (PW_FUSED_GATHER=0 selects the NCCL all-gather).
+it under the NCCL backend when PW_FUSED_GATHER=1 (opt-in until an 8-GPU run has
+measured it; the default is the NCCL all-gather).
 """
 from __future__ import annotations
 

@@ -145,6 +145,7 @@ def test_persistent_march_matches_per_step_launches(dev, monkeypatch, nx, ny, ba
 
     prop = SlicePropagator(fine_spec(nx, ny), nsteps=nsteps)
     x = torch.as_tensor(random_states(nx, ny, batch, 31 + nx)).cuda()
+    monkeypatch.setenv("PW_MARCH_PERSIST", "0")  # the per-step launches (the default at 128/256 is persistent)
     want = prop.apply(x)
     monkeypatch.setenv("PW_MARCH_PERSIST", "1")
     if nseg:
