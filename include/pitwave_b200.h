@@ -216,6 +216,15 @@ int pw_copy(pw_ctx* ctx, void* dst, const void* src, long long nbytes);
 int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long dim,
                 double* out_host);
 
+/* Window diagnostics of one device state q (dim doubles) in one pass -- the per-window
+ * record of run_windowed (parareal.py:253-263, 316-318): out_host[0] = max|q| (max_norm,
+ * diagnostics.py:34-36; NaN propagates), out_host[1] = cell_area * sum q^2 (total_energy,
+ * diagnostics.py:20-23), out_host[2] = number of non-finite entries (State.all_finite,
+ * mesh.py:140-141), out_host[3 + k] = q[probes[k]] for nprobe <= 4 flat indices (ProbeSeries,
+ * diagnostics.py:39-66).  out_host holds 3 + nprobe doubles. */
+int pw_window_diag(pw_ctx* ctx, const double* q, long long dim, double cell_area, const long long* probes,
+                   int nprobe, double* out_host);
+
 /* The sweep's fused serial-step pass on caller buffers (device pointers; test and
  * diagnostic entry):  y = [g +] c + D alpha  (rd columns of D) and
  * alpha_next = Q^T y (rq columns of Q); D and Q are column-major with leading

@@ -1255,6 +1255,26 @@ int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long 
   });
 }
 
+int pw_window_diag(pw_ctx* ctx, const double* q, long long dim, double cell_area, const long long* probes,
+                   int nprobe, double* out_host) {
+  return guarded([&] {
+    PW_CHECK(ctx && q && out_host && dim >= 1, PW_ERR_VALUE, "bad pw_window_diag arguments");
+    PW_CHECK(nprobe >= 0 && nprobe <= 4 && (nprobe == 0 || probes), PW_ERR_VALUE, "0..4 probe indices");
+    for (int k = 0; k < nprobe; ++k)
+      PW_CHECK(probes[k] >= 0 && probes[k] < dim, PW_ERR_VALUE, "probe index outside the state");
+    Ctx& c = ctx->c;
+    DBuf scr;
+    const size_t ns = pw::window_diag_scratch_doubles(c);
+    double* s = scr.ensure(c, ns + 8 + 4);
+    long long* pr = reinterpret_cast<long long*>(s + ns + 8);
+    if (nprobe > 0)
+      PW_CUDA(cudaMemcpyAsync(pr, probes, sizeof(long long) * nprobe, cudaMemcpyHostToDevice, c.stream));
+    pw::launch_window_diag(c, q, dim, cell_area, pr, nprobe, s, s + ns);
+    PW_CUDA(cudaMemcpyAsync(out_host, s + ns, sizeof(double) * (3 + nprobe), cudaMemcpyDeviceToHost, c.stream));
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
 // ------------------------------------------------------------ the sweep
 namespace {
 // Run a scope's launches (our kernels, cuBLAS, cuSOLVER) on another stream.

@@ -739,6 +739,80 @@ void launch_residual(Ctx& c, const double* a, long long lda, const double* b, lo
   PW_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------- K7 window diagnostics
+// One pass over a window endpoint: max|q| (NaN-propagating like numpy's max), sum q^2 and
+// the non-finite count (reference diagnostics.py:20-36 max_norm / total_energy, and the
+// all_finite check of parareal.py:316-318).  Per-block partials, then one finishing block.
+__device__ __forceinline__ double nanmax2(double a, double b) {
+  return (a != a || a > b) ? a : b;  // a NaN on either side wins
+}
+
+constexpr int kDiagThreads = 256;
+__global__ void window_diag_partial_kernel(const double* __restrict__ q, long long n,
+                                           double* __restrict__ part) {
+  __shared__ double smax[kDiagThreads / 32], ssum[kDiagThreads / 32], sbad[kDiagThreads / 32];
+  double mx = 0.0, s = 0.0, bad = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i < n; i += stride) {
+    const double x = __ldcs(q + i);
+    mx = nanmax2(fabs(x), mx);
+    s = fma(x, x, s);
+    bad += isfinite(x) ? 0.0 : 1.0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = nanmax2(__shfl_xor_sync(0xffffffffu, mx, o), mx);
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    smax[w] = mx;
+    ssum[w] = s;
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kDiagThreads / 32; ++k) {
+      mx = nanmax2(smax[k], smax[0]);
+      smax[0] = mx;
+      ssum[0] += ssum[k];
+      sbad[0] += sbad[k];
+    }
+    part[3 * blockIdx.x + 0] = smax[0];
+    part[3 * blockIdx.x + 1] = ssum[0];
+    part[3 * blockIdx.x + 2] = sbad[0];
+  }
+}
+
+__global__ void window_diag_finish_kernel(const double* __restrict__ part, int nblk, double cell_area,
+                                          const long long* __restrict__ probes, int nprobe,
+                                          const double* __restrict__ q, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double mx = 0.0, s = 0.0, bad = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    mx = nanmax2(part[3 * b], mx);
+    s += part[3 * b + 1];
+    bad += part[3 * b + 2];
+  }
+  out[0] = mx;
+  out[1] = s * cell_area;
+  out[2] = bad;
+  for (int k = 0; k < nprobe; ++k) out[3 + k] = q[probes[k]];
+}
+
+size_t window_diag_scratch_doubles(const Ctx& c) { return 3 * (size_t)std::max(c.num_sms, 1) * 2 + 8; }
+
+void launch_window_diag(Ctx& c, const double* q, long long n, double cell_area, const long long* probes_dev,
+                        int nprobe, double* scratch, double* out_dev) {
+  const int nblk = (int)std::max<long long>(1, std::min<long long>((long long)std::max(c.num_sms, 1) * 2,
+                                                                   (n + kDiagThreads - 1) / kDiagThreads));
+  window_diag_partial_kernel<<<nblk, kDiagThreads, 0, c.stream>>>(q, n, scratch);
+  window_diag_finish_kernel<<<1, 32, 0, c.stream>>>(scratch, nblk, cell_area, probes_dev, nprobe, q, out_dev);
+  c.launches += 2;
+  PW_LAUNCH_CHECK();
+}
+
 int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv_dev,
                      double* tau_dev, double* diag_dev, int* rank_host) {
   PW_CHECK(m >= 1 && m <= 2048, PW_ERR_VALUE, "pivoted QR supports 1..2048 snapshot columns");

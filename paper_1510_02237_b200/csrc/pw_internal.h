@@ -179,6 +179,11 @@ void launch_make_unit_lower(Ctx& c, double* A, long long ld, int off, int k);
 void launch_larft_cols(Ctx& c, double* T, int ldt, const double* G, const double* tau, int col0, int p);
 void launch_set_diag_block(Ctx& c, double* A, long long ld, int k, double v);
 size_t residual_scratch_doubles(int ncols, long long nrows);
+// K7: out[0] = max|q| (NaN wins), out[1] = cell_area * sum q^2, out[2] = #non-finite,
+// out[3 + k] = q[probes[k]]
+size_t window_diag_scratch_doubles(const Ctx& c);
+void launch_window_diag(Ctx& c, const double* q, long long n, double cell_area, const long long* probes_dev,
+                        int nprobe, double* scratch, double* out_dev);
 void launch_residual(Ctx& c, const double* a, long long lda, const double* b, long long ldb,
                      int ncols, long long nrows, double* scratch, double* out_dev);
 // fp64 pipe peak probe (probe.cu): best-of-3 DFMA throughput in TFLOP/s
