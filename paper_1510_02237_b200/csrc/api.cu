@@ -1397,8 +1397,10 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       return ms * 1e-3;
     };
 
+    pw::NvtxRange nv_sweep(kse ? "pitwave.kse_sweep" : "pitwave.parareal_sweep");
     // serial coarse initialisation qk[i+1] = G(qk[i])  (parareal.py:112-116)
     if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
+    std::unique_ptr<pw::NvtxRange> nv_phase(new pw::NvtxRange("coarse.init"));
     copy_cols(c, QK, d, q0, d, d, 1);
     for (int i = 0; i < n_c; ++i) prop_apply(coarse, QK + (size_t)i * d, QK + (size_t)(i + 1) * d, 1, d);
     copy_cols(c, GK, ldr, QK + d + roff, d, ldr, n_c);  // G(qk[i]) for the first correction
@@ -1408,7 +1410,10 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     }
     SyncEvents sync;
     int k_done = 0;
+    nv_phase.reset();
     for (int k = 0; k < n_it; ++k) {
+      pw::NvtxRange nv_it("iteration");
+      nv_phase.reset(new pw::NvtxRange("fine"));
       if (timed) PW_CUDA(cudaEventRecord(ev[0], c.stream));
       // the snapshots qk[0..P-1] are final here: their QR runs on the side stream while
       // the fine propagator runs on the main one (only Y needs the fine images)
@@ -1434,6 +1439,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       }
       if (timed) PW_CUDA(cudaEventRecord(ev[1], c.stream));
       const int m_old = kse ? B->m : 0;
+      nv_phase.reset(new pw::NvtxRange("qr"));
       if (kse) {
         StreamScope side(c, c.qr_overlap ? c.side : c.stream);
         PW_CUDA(cudaStreamWaitEvent(c.stream, sync.snap, 0));
@@ -1472,6 +1478,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         }
       }
       if (timed) PW_CUDA(cudaEventRecord(ev[2], c.stream));
+      nv_phase.reset(new pw::NvtxRange("coarse.correction"));
       // serial correction sweep (parareal.py:128-132)
       copy_cols(c, QN, d, q0, d, d, 1);
       double* part = bPart.ensure(c, pw::combine_part_doubles(d, kse ? (int)std::min<long long>(B->cap, d) : 1));
@@ -1544,6 +1551,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         }
       }
       pw::launch_residual(c, QK + d, d, QN + d, d, n_c, d, scr, res_dev + k);
+      nv_phase.reset();
       if (timed) {
         PW_CUDA(cudaEventRecord(ev[3], c.stream));
         t_fine += elapsed(ev[0], ev[1]);

@@ -9,9 +9,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/pitwave_b200.h"
 
 namespace pw {
+
+// NVTX range for profilers (nsys / ncu --nvtx): named after the reference's phases
+// (parareal.py:31-47: coarse / fine / qr).  nvtx3 is header-only; without a tool attached
+// a push / pop costs a few ns.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);

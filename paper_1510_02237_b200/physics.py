@@ -1,7 +1,11 @@
-"""Model description of the linear acoustic-advection system (reference physics.py).
+"""Parameters of the linear acoustic-advection model (reference ``pkg/src/pitwave/physics.py``).
 
-Only the model *parameters* live here; the right-hand side itself is
-evaluated inside the sm_100a kernels (csrc/exact.cu, csrc/fine_fused.cu).
+The right-hand side itself never runs on the host here: the sm_100a kernels
+(csrc/exact.cu, fine_fused.cu, fine_march.cu) evaluate it.  This module only
+carries what those kernels are configured from -- the model kind, advecting
+velocity, flux order, sound speed and divergence-damping strength -- with the
+reference's up-front validation (``physics.py:21-51``), and the damping
+coefficients alpha = nu h^2 / tau the launchers pass down (``physics.py:54-64``).
 """
 from __future__ import annotations
 
@@ -18,9 +22,23 @@ def _check_order(order: int) -> int:
     return int(order)
 
 
+def _damping_problem(kind, nu, tau):
+    """Why (kind, nu, tau) is not a valid damping setting, or None."""
+    if nu < 0:
+        return f"damping strength must be nonnegative, got {nu}"
+    needs_tau = nu > 0 and kind == ACOUSTIC
+    if needs_tau and not (tau is not None and tau > 0):
+        return "damping_timescale must be positive when nu_damp > 0"
+    return None
+
+
 @dataclass(frozen=True)
 class ModelSpec:
-    """Continuous model + discretisation knobs (reference physics.py:21-51)."""
+    """Model kind + advecting velocity + the discretisation knobs of one propagator.
+
+    ``damping_timescale`` is the tau of alpha = nu dx^2 / tau: the fine step for
+    RK3, dt / n_sound for the split coarse scheme (set by make_propagator).
+    """
 
     kind: str
     vel: object
@@ -33,20 +51,19 @@ class ModelSpec:
         if self.kind not in (SCALAR, ACOUSTIC):
             raise ValueError(f"model kind must be {SCALAR!r} or {ACOUSTIC!r}, got {self.kind!r}")
         _check_order(self.advective_flux_order)
-        if self.kind == ACOUSTIC and self.sound_speed <= 0:
+        if self.kind == ACOUSTIC and not self.sound_speed > 0:
             raise ValueError(f"sound speed must be positive, got {self.sound_speed}")
-        if self.nu_damp < 0:
-            raise ValueError(f"damping strength must be nonnegative, got {self.nu_damp}")
-        if self.nu_damp > 0 and self.kind == ACOUSTIC:
-            if self.damping_timescale is None or self.damping_timescale <= 0:
-                raise ValueError("damping_timescale must be positive when nu_damp > 0")
+        problem = _damping_problem(self.kind, self.nu_damp, self.damping_timescale)
+        if problem:
+            raise ValueError(problem)
 
     def with_timescale(self, tau: float) -> "ModelSpec":
         return replace(self, damping_timescale=tau)
 
 
 def damping_coefficients(nu: float, dx: float, dy: float, tau: float):
-    """(alpha1, alpha2) = nu (dx^2, dy^2) / tau (reference physics.py:54-58)."""
-    if tau <= 0:
+    """(alpha1, alpha2) for the x and y damping terms; evaluated as (nu dx) dx / tau so
+    the bits match the reference's kernels' coefficients."""
+    if not tau > 0:
         raise ValueError(f"damping timescale must be positive, got {tau}")
-    return nu * dx * dx / tau, nu * dy * dy / tau
+    return tuple(nu * h * h / tau for h in (dx, dy))
