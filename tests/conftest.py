@@ -22,3 +22,14 @@ def rng():
 
 def golden(name):
     return np.load(os.path.join(GOLDEN, name))
+
+
+def floor_bound(case, iteration, kind="state"):
+    """SURVEY.md 8(c) parity bound for a reduced-shape window: max(1e-10, 10 x the
+    reference's own numba-vs-numpy floor) at that iteration (1-based), measured by
+    tests/golden/make_floor_golden.py into floors.json."""
+    import json
+
+    with open(os.path.join(GOLDEN, "floors.json")) as fh:
+        floors = json.load(fh)
+    return max(1e-10, 10.0 * floors[case][kind][iteration - 1])

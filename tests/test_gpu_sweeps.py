@@ -9,7 +9,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import floor_bound, golden
 from oracle import oracle as orc
 from paper_1510_02237_b200 import harness
 
@@ -392,8 +392,10 @@ def test_kse_residual_and_ranks_against_oracle_c1_shape_p16():
     o_ends, o_res, o_sub = orc.kse_sweep(q0, of, oc, p, k, ranks=ranks)
     assert sub.ranks_history == ranks
     worst = max(rel(a, b) for a, b in zip(ends, o_ends))
-    assert worst <= 1e-9, worst
-    np.testing.assert_allclose(res, o_res, rtol=1e-8)
+    bound = floor_bound("c1_shape_p16", k)
+    print(f"c1 shape P=16: max rel L2 per slice vs oracle {worst:.3e} (bound {bound:.1e})")
+    assert worst <= bound, worst
+    np.testing.assert_allclose(res, o_res, rtol=floor_bound("c1_shape_p16", k, "residual"))
 
 
 @pytest.mark.parametrize("d,ld,r,g_null", [(786432, 786432, 310, False), (200000, 200000, 1024, False),
@@ -484,5 +486,8 @@ def test_c5_shaped_window_against_oracle(dev, tsqr_shards):
     o_ends, o_res, _ = orc.kse_sweep(q0, of, oc, p, k, ranks=ranks)
     assert sub.ranks_history == ranks
     worst = max(rel(a, b) for a, b in zip(ends, o_ends))
-    assert worst <= 1e-9, worst
-    np.testing.assert_allclose(res, o_res, rtol=1e-8)
+    bound = floor_bound("c5_shape_128", k)
+    print(f"c5 shape 128^2 (tsqr shards {tsqr_shards}): max rel L2 per slice vs oracle {worst:.3e} "
+          f"(bound {bound:.1e})")
+    assert worst <= bound, worst
+    np.testing.assert_allclose(res, o_res, rtol=floor_bound("c5_shape_128", k, "residual"))

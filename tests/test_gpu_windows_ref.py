@@ -2,11 +2,14 @@
 (tests/golden/make_window_golden.py: residuals, ranks, per-slice norms and 512
 fixed-seed sampled entries per slice of qn[1:] after every iteration).
 
-Tolerance: SURVEY.md 8(c) -- per iteration, relative L2 per slice <=
-max(1e-10, 10 x the reference's own numba-vs-numpy noise floor measured by the
-survey for that iteration (Appendix A, c3 stable-G row)); the sampled entries stand
-in for the 6 GB states.  c4 has no survey floor: 1e-10 on iteration 1 is used and
-the measured deviation is printed."""
+Tolerance: SURVEY.md 8(c) -- per iteration, the deviation statistic (max over slices
+of the relative norm difference and the relative L2 difference of the sampled
+entries) must be <= max(1e-10, 10 x the reference's OWN floor), where the floor is
+the same statistic between the reference's numba run (<config>_reference.npz) and
+its numpy-backend run of the same window (<config>_reference_numpy.npz, same
+script with PITWAVE_KERNELS=numpy).  Iterations without a numpy-backend fixture
+fall back to the survey's c3 floor (Appendix A) or, for c4, to 1e-5, and say so.
+"""
 import os
 
 import numpy as np
@@ -18,8 +21,36 @@ from paper_1510_02237_b200 import harness
 
 pytestmark = pytest.mark.gpu
 
-# reference numba-vs-numpy per-slice max deviation, c3 stable G
-C3_FLOOR = [2.8e-9, 1.1e-8, 9.0e-9, 3.6e-8, 2.1e-7]
+# fallbacks when no numpy-backend fixture exists: the survey's c3 stable-G floor
+# (Appendix A; another seed, indicative) and the survey's expected c4 level
+FALLBACK_FLOOR = {"c3": [2.8e-9, 1.1e-8, 9.0e-9, 3.6e-8, 2.1e-7], "c4": [1e-6] * 4}
+
+
+def _stat(a_norms, a_samp, b_norms, b_samp):
+    d_norm = np.max(np.abs(a_norms - b_norms) / b_norms)
+    d_samp = np.max(np.linalg.norm(a_samp - b_samp, axis=1) / np.linalg.norm(b_samp, axis=1))
+    return float(max(d_norm, d_samp))
+
+
+def measured_floor(name):
+    """Per-iteration reference floor (numba vs numpy fixture), or the fallback."""
+    ref = np.load(os.path.join(GOLDEN, f"{name}_reference.npz"))
+    path = os.path.join(GOLDEN, f"{name}_reference_numpy.npz")
+    out = list(FALLBACK_FLOOR[name])
+    src = ["fallback"] * len(out)
+    if os.path.exists(path):
+        alt = np.load(path)
+        assert np.array_equal(alt["idx"], ref["idx"])
+        for k in range(min(len(alt["res"]), len(ref["res"]))):
+            out[k] = _stat(alt["norms"][k], alt["samples"][k], ref["norms"][k], ref["samples"][k])
+            src[k] = "measured"
+    print(f"{name} reference floor per iteration: " +
+          ", ".join(f"{f:.2e} ({s})" for f, s in zip(out, src)))
+    return out
+
+
+def bounds(name):
+    return [max(1e-10, 10.0 * f) for f in measured_floor(name)]
 
 
 def props(name):
@@ -54,9 +85,7 @@ def check_window(name, tol_per_iteration):
         norms = torch.linalg.norm(st, dim=1).cpu().numpy()
         samp = st[:, idx].cpu().numpy()
         want_n, want_s = g["norms"][k - 1], g["samples"][k - 1]
-        d_norm = np.max(np.abs(norms - want_n) / want_n)
-        d_samp = np.max(np.linalg.norm(samp - want_s, axis=1) / np.linalg.norm(want_s, axis=1))
-        worst.append(max(d_norm, d_samp))
+        worst.append(_stat(norms, samp, want_n, want_s))
         d_res = abs(res[-1] - g["res"][k - 1]) / abs(g["res"][k - 1])
         print(f"{name} iteration {k}: rank {sub.rank} (ref {g['ranks'][k - 1]}), state deviation "
               f"{worst[-1]:.3e}, residual deviation {d_res:.3e}", flush=True)
@@ -69,7 +98,7 @@ def check_window(name, tol_per_iteration):
 
 
 def test_c3_window_matches_reference_run():
-    check_window("c3", [max(1e-10, 10 * f) for f in C3_FLOOR])
+    check_window("c3", bounds("c3"))
 
 
 def test_c3_window_tsqr_two_row_shards_matches_reference_run():
@@ -82,18 +111,15 @@ def test_c3_window_tsqr_two_row_shards_matches_reference_run():
     ctx.set_row_shards(2)
     ctx.set_tsqr(True)
     try:
-        check_window("c3", [max(1e-10, 10 * f) for f in C3_FLOOR])
+        check_window("c3", bounds("c3"))
     finally:
         ctx.set_tsqr(False)
         ctx.set_row_shards(1)
 
 
-def test_c4_first_iteration_matches_reference_run():
-    """c4 iteration 1: ranks equal (142) but the rank gap is tight -- kept min |R_jj|/|R_11|
-    1.36e-10 against dropped max 9.45e-11, so cond(R11) ~ 7e9 and eps * cond ~ 1.6e-6.
-    Two QR algorithms (the reference's dgeqp3 on S, this repo's Householder of S + pivoted
-    QR of R1) then legitimately differ at that level: measured 1.3e-6 max / 6.2e-7 median,
-    identical in strict mode (so not the stencils), while the same-algorithm perturbation
-    floor (fast vs strict kernels, scripts/floor_check.py) is 3.2e-8.
-    expects c4/c5 floors of 1e-6 to 1e-5; the bound used is 1e-5."""
-    check_window("c4", [1e-5] * 4)
+def test_c4_window_matches_reference_run():
+    """c4 (1024^2, P=256) against the reference's run, every iteration the fixture holds.
+    The rank gap is tight here (kept min |R_jj|/|R_11| 1.36e-10 against dropped max
+    9.45e-11 at iteration 1, cond(R11) ~ 7e9), so two QR algorithms legitimately differ at
+    eps * cond ~ 1e-6; the bound is 10 x the reference's own numba-vs-numpy floor."""
+    check_window("c4", bounds("c4"))
