@@ -216,6 +216,22 @@ int pw_copy(pw_ctx* ctx, void* dst, const void* src, long long nbytes);
 int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long dim,
                 double* out_host);
 
+/* The library's fp64 tensor-core GEMM (DMMA, csrc/dgemm.cu) on caller device buffers:
+ * C (m x n) = alpha op(A) B + beta C, column-major, op(A) = A (trans_a = 0) or A^T.
+ * Every dense product of the subspace (Subspace.update / project / fine_on_projection,
+ * subspace.py:66-98, and the sweep's batched K(qk)) runs on it; exported for tests and
+ * benchmarks.  beta == 0 does not read C. */
+int pw_dgemm(pw_ctx* ctx, int trans_a, long long m, long long n, long long k, double alpha, const double* a,
+             long long lda, const double* b, long long ldb, double beta, double* c, long long ldc);
+
+/* The library's tall-skinny Householder QR (csrc/tsqr.cu: TSQR + Householder
+ * reconstruction, 32-column sub-panels) on a caller device buffer, in LAPACK dgeqrf's
+ * output format: R on and above the diagonal of a (rows x cols, ld lda), the unit-lower
+ * reflectors below it, tau[min(rows, cols)].  The subspace update factors every appended
+ * snapshot block with it (reference subspace.py:66-68: scipy qr, LAPACK); exported for
+ * tests and benchmarks. */
+int pw_geqrf(pw_ctx* ctx, long long rows, int cols, double* a, long long lda, double* tau);
+
 /* Window diagnostics of one device state q (dim doubles) in one pass -- the per-window
  * record of run_windowed (parareal.py:253-263, 316-318): out_host[0] = max|q| (max_norm,
  * diagnostics.py:34-36; NaN propagates), out_host[1] = cell_area * sum q^2 (total_energy,

@@ -97,6 +97,10 @@ SIGNATURES = [
     ("pw_ctx_set_tsqr", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),
+    ("pw_dgemm", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
+                                ctypes.c_double, c_vp, ctypes.c_longlong, c_vp, ctypes.c_longlong, ctypes.c_double,
+                                c_vp, ctypes.c_longlong]),
+    ("pw_geqrf", ctypes.c_int, [c_vp, ctypes.c_longlong, ctypes.c_int, c_vp, ctypes.c_longlong, c_vp]),
     ("pw_window_diag", ctypes.c_int, [c_vp, c_vp, ctypes.c_longlong, ctypes.c_double, c_vp, ctypes.c_int, c_dp]),
     ("pw_probe_fp64_peak", ctypes.c_int, [c_vp, ctypes.c_int, c_dp]),
     ("pw_mem_stats", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),

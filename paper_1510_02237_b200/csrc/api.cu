@@ -140,6 +140,11 @@ void copy_cols(Ctx& c, double* dst, long long ldd, const double* src, long long 
 }
 
 // C(m x n) = alpha * op(A) * op(B) + beta * C, column-major
+bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e == '1';
+}
+
 void gemm(Ctx& c, bool ta, bool tb, long long m, long long n, long long k, double alpha,
           const double* A, long long lda, const double* B, long long ldb, double beta, double* C,
           long long ldc) {
@@ -150,8 +155,13 @@ void gemm(Ctx& c, bool ta, bool tb, long long m, long long n, long long k, doubl
       PW_CUDA(cudaMemset2DAsync(C, ldc * sizeof(double), 0, m * sizeof(double), n, c.stream));
     return;
   }
-  PW_BLAS(cublasDgemm_64(blas(c), ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N,
-                         m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc));
+  PW_CHECK(!tb, PW_ERR_STATE, "gemm: op(B) = B^T is not used by the library");
+  if (getenv_flag("PW_CUBLAS")) {  // A/B comparison against the vendor GEMM (tests, profiling)
+    PW_BLAS(cublasDgemm_64(blas(c), ta ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_OP_N, m, n, k, &alpha, A, lda, B,
+                           ldb, &beta, C, ldc));
+    return;
+  }
+  pw::dgemm(c, ta, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 }  // namespace
@@ -402,6 +412,10 @@ static std::mutex g_geqrf_mu;
 
 static void xgeqrf(pw_basis* B, long long rows, long long cols, double* A, long long lda, double* tau) {
   Ctx& c = B->ctx->c;
+  if (!getenv_flag("PW_CUSOLVER")) {  // default: the library's TSQR panel (tsqr.cu)
+    pw::tsqr_geqrf(c, rows, (int)cols, A, lda, tau);
+    return;
+  }
   int* info = B->info.ensure(c, 1);
   auto call = [&] {
     PW_SOLVER(cusolverDnXgeqrf(solver(c), solver_params(c), rows, cols, CUDA_R_64F, A, lda, CUDA_R_64F, tau,
@@ -1252,6 +1266,26 @@ int pw_residual(pw_ctx* ctx, const double* a, const double* b, int n, long long 
     pw::launch_residual(c, a, dim, b, dim, n, dim, s + 1, s);
     PW_CUDA(cudaMemcpyAsync(out_host, s, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     PW_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pw_dgemm(pw_ctx* ctx, int trans_a, long long m, long long n, long long k, double alpha, const double* a,
+             long long lda, const double* b, long long ldb, double beta, double* c, long long ldc) {
+  return guarded([&] {
+    PW_CHECK(ctx && (m <= 0 || n <= 0 || (c && (k <= 0 || (a && b)))), PW_ERR_VALUE, "NULL argument");
+    PW_CHECK(m >= 0 && n >= 0 && k >= 0, PW_ERR_VALUE, "negative dimension");
+    PW_CHECK(ldc >= std::max<long long>(1, m) && ldb >= std::max<long long>(1, k) &&
+                 lda >= std::max<long long>(1, trans_a ? k : m),
+             PW_ERR_VALUE, "leading dimension too small");
+    gemm(ctx->c, trans_a != 0, false, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+  });
+}
+
+int pw_geqrf(pw_ctx* ctx, long long rows, int cols, double* a, long long lda, double* tau) {
+  return guarded([&] {
+    PW_CHECK(ctx && a && tau, PW_ERR_VALUE, "NULL argument");
+    PW_CHECK(rows >= 0 && cols >= 0 && lda >= std::max<long long>(1, rows), PW_ERR_VALUE, "bad geqrf shape");
+    pw::tsqr_geqrf(ctx->c, rows, cols, a, lda, tau);
   });
 }
 

@@ -191,6 +191,16 @@ void launch_make_unit_lower(Ctx& c, double* A, long long ld, int off, int k);
 void launch_larft_cols(Ctx& c, double* T, int ldt, const double* G, const double* tau, int col0, int p);
 void launch_set_diag_block(Ctx& c, double* A, long long ld, int k, double v);
 size_t residual_scratch_doubles(int ncols, long long nrows);
+// fp64 DMMA GEMM (dgemm.cu): C = alpha op(A) B + beta C, column-major, 64-bit sizes;
+// acol gathers op(A)'s columns (op N), b_upper skips the zero lower part of an upper-
+// triangular B
+void dgemm(Ctx& c, bool ta, long long m, long long n, long long k, double alpha, const double* A, long long lda,
+           const double* B, long long ldb, double beta, double* C, long long ldc, const int* acol = nullptr,
+           bool b_upper = false);
+
+// tall-skinny Householder QR (tsqr.cu): LAPACK geqrf's output format for rows x p
+void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double* tau);
+
 // K7: out[0] = max|q| (NaN wins), out[1] = cell_area * sum q^2, out[2] = #non-finite,
 // out[3 + k] = q[probes[k]]
 size_t window_diag_scratch_doubles(const Ctx& c);
