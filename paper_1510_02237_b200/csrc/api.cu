@@ -29,8 +29,9 @@ int kernel_setup(int device, const void* kern, int threads, size_t smem) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find({device, kern});
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024)
-    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // always explicit: with static shared memory as well, the default dynamic limit is
+  // 48 KB minus the static part
+  if (smem > 0) PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   per_sm = std::max(per_sm, 1);

@@ -28,14 +28,24 @@
 namespace pw {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, NST = 3, NTH = 256;
+constexpr int BK = 16, NST = 3, NTH = 256;
 constexpr int PADK = BK + 4;  // rows of [m][k] / [n][k] tiles
-constexpr int PADM = BM + 4;  // rows of the [k][m] tile
-constexpr int A_STAGE_N = BK * PADM;  // op(A) = A: [k][m]
-constexpr int A_STAGE_T = BM * PADK;  // op(A) = A^T: [m][k]
-constexpr int B_STAGE = BN * PADK;    // [n][k]
-constexpr int A_STAGE = A_STAGE_N > A_STAGE_T ? A_STAGE_N : A_STAGE_T;
-constexpr size_t SMEM = sizeof(double) * (size_t)NST * (A_STAGE + B_STAGE);
+
+// CTA tile (32 WM) x (32 WN) with 8 warps of 32 x 32: WM = 4 (128 x 64, the default) or
+// WM = 1 (32 x 256, for the 32-row outputs of the TSQR trailing reductions V^T A)
+template <int WM_>
+struct Cfg {
+  static constexpr int WM = WM_, WN = 8 / WM_;
+  static constexpr int BM = 32 * WM, BN = 32 * WN;
+  static constexpr int PADM = BM + 4;  // rows of the [k][m] tile
+  static constexpr int A_STAGE_N = BK * PADM;  // op(A) = A: [k][m]
+  static constexpr int A_STAGE_T = BM * PADK;  // op(A) = A^T: [m][k]
+  static constexpr int B_STAGE = BN * PADK;    // [n][k]
+  static constexpr int A_STAGE = A_STAGE_N > A_STAGE_T ? A_STAGE_N : A_STAGE_T;
+  static constexpr size_t SMEM_PIPE = sizeof(double) * (size_t)NST * (A_STAGE + B_STAGE);
+  static constexpr size_t SMEM_EPI = sizeof(double) * (size_t)BN * (BM + 1);  // staged C tile
+  static constexpr size_t SMEM = SMEM_PIPE > SMEM_EPI ? SMEM_PIPE : SMEM_EPI;
+};
 
 __host__ __device__ __forceinline__ long long lmin(long long a, long long b) { return a < b ? a : b; }
 
@@ -75,9 +85,10 @@ struct GemmArgs {
 
 // Stage k tile kt (global k in [kt*BK, kt*BK+BK)) of op(A) and B into ring slot `st`.
 // VEC: 16-byte copies (pointers 16-byte aligned, leading dimensions even); else 8-byte.
-template <bool TA, bool VEC>
+template <class K, bool TA, bool VEC>
 __device__ __forceinline__ void load_tile(const GemmArgs& g, double* As, double* Bs, long long m0, long long n0,
                                           long long kt) {
+  constexpr int BM = K::BM, BN = K::BN, PADM = K::PADM;
   const int tid = threadIdx.x;
   const long long k0 = kt * BK;
   constexpr int W = VEC ? 2 : 1;  // doubles per copy
@@ -139,15 +150,16 @@ __device__ __forceinline__ void load_tile(const GemmArgs& g, double* As, double*
   }
 }
 
-template <bool TA, bool VEC>
+template <class K, bool TA, bool VEC>
 __global__ void __launch_bounds__(NTH, 2) dgemm_kernel(GemmArgs g) {
+  constexpr int BM = K::BM, BN = K::BN, PADM = K::PADM, A_STAGE = K::A_STAGE, B_STAGE = K::B_STAGE;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + NST * A_STAGE;
   const long long m0 = (long long)(g.nfast ? blockIdx.y : blockIdx.x) * BM;
   const long long n0 = (long long)(g.nfast ? blockIdx.x : blockIdx.y) * BN;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int wm = (warp % K::WM) * 32, wn = (warp / K::WM) * 32;
   // k tiles of this split; an upper-triangular B ends at the tile's last column
   long long kend = g.k;
   if (g.b_upper) kend = lmin(kend, n0 + BN);
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(NTH, 2) dgemm_kernel(GemmArgs g) {
 
 #pragma unroll
   for (int s = 0; s < NST - 1; ++s) {
-    if (s < nkt) load_tile<TA, VEC>(g, As + s * A_STAGE, Bs + s * B_STAGE, m0, n0, kt0 + s);
+    if (s < nkt) load_tile<K, TA, VEC>(g, As + s * A_STAGE, Bs + s * B_STAGE, m0, n0, kt0 + s);
     cp_commit();
   }
   const int ar = lane >> 2, ak = lane & 3;  // fragment row / k of this lane
@@ -173,7 +185,7 @@ __global__ void __launch_bounds__(NTH, 2) dgemm_kernel(GemmArgs g) {
     __syncthreads();  // tile t landed for all; slot (t-1) % NST is free again
     {
       const int tn = t + NST - 1;
-      if (tn < nkt) load_tile<TA, VEC>(g, As + (tn % NST) * A_STAGE, Bs + (tn % NST) * B_STAGE, m0, n0, kt0 + tn);
+      if (tn < nkt) load_tile<K, TA, VEC>(g, As + (tn % NST) * A_STAGE, Bs + (tn % NST) * B_STAGE, m0, n0, kt0 + tn);
       cp_commit();
     }
     const double* a_s = As + (t % NST) * A_STAGE;
@@ -196,34 +208,32 @@ __global__ void __launch_bounds__(NTH, 2) dgemm_kernel(GemmArgs g) {
   }
   cp_wait<0>();
 
-  // epilogue: lane holds C[row][col], C[row][col + 1] of each 8 x 8 fragment
-  const long long cr = m0 + wm + ar;
-  const long long cc = n0 + wn + 2 * ak;
-  if (g.part) {
-    double* P = g.part + (long long)blockIdx.z * g.m * g.n;
+  __syncthreads();  // the pipeline buffers become the C tile
+  // epilogue: lane holds C[row][col], C[row][col + 1] of each 8 x 8 fragment; stage the
+  // tile in shared memory ([col][row], ld BM + 1) and write it column by column with
+  // consecutive threads on consecutive rows (coalesced read-modify-write of C)
+  double* Cs = smem;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const long long r = cr + i * 8, c = cc + j * 8 + h;
-          if (r < g.m && c < g.n) P[r + c * g.m] = acc[i][j][h];
-        }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const long long r = cr + i * 8, c = cc + j * 8 + h;
-          if (r < g.m && c < g.n) {
-            double* p = g.C + r + c * g.ldc;
-            const double v = g.alpha * acc[i][j][h];
-            *p = (g.beta == 0.0) ? v : fma(g.beta, *p, v);
-          }
-        }
+      for (int h = 0; h < 2; ++h) Cs[(wn + j * 8 + 2 * ak + h) * (BM + 1) + wm + i * 8 + ar] = acc[i][j][h];
+  __syncthreads();
+  const long long mrem = lmin(BM, g.m - m0), nrem = lmin(BN, g.n - n0);
+  double* P = g.part ? g.part + (long long)blockIdx.z * g.m * g.n : nullptr;
+  for (int e = threadIdx.x; e < BM * BN; e += NTH) {
+    const int cl = e / BM, rl = e - cl * BM;
+    if (rl < mrem && cl < nrem) {
+      const double v = Cs[cl * (BM + 1) + rl];
+      const long long r = m0 + rl, cc = n0 + cl;
+      if (P) {
+        P[r + cc * g.m] = v;
+      } else {
+        double* p = g.C + r + cc * g.ldc;
+        *p = (g.beta == 0.0) ? g.alpha * v : fma(g.beta, *p, g.alpha * v);
+      }
+    }
   }
 }
 
@@ -242,13 +252,24 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int splits
   }
 }
 
-template <bool TA, bool VEC>
+template <class K, bool TA, bool VEC>
 void launch_cfg(Ctx& c, const GemmArgs& g, dim3 grid) {
-  auto kern = dgemm_kernel<TA, VEC>;
-  kernel_setup(c, kern, NTH, SMEM);
-  kern<<<grid, NTH, SMEM, c.stream>>>(g);
+  auto kern = dgemm_kernel<K, TA, VEC>;
+  kernel_setup(c, kern, NTH, K::SMEM);
+  kern<<<grid, NTH, K::SMEM, c.stream>>>(g);
   c.launches += 1;
   PW_LAUNCH_CHECK();
+}
+
+template <class K>
+void launch_any(Ctx& c, const GemmArgs& g, dim3 grid, bool ta, bool vec) {
+  if (ta) {
+    if (vec) launch_cfg<K, true, true>(c, g, grid);
+    else launch_cfg<K, true, false>(c, g, grid);
+  } else {
+    if (vec) launch_cfg<K, false, true>(c, g, grid);
+    else launch_cfg<K, false, false>(c, g, grid);
+  }
 }
 
 }  // namespace
@@ -276,7 +297,10 @@ void dgemm(Ctx& c, bool ta, long long m, long long n, long long k, double alpha,
   g.beta = beta;
   g.acol = acol;
   g.b_upper = b_upper ? 1 : 0;
-  const long long tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
+  // 32 x 256 tiles for short outputs (m <= 32: the TSQR's V^T A), else 128 x 64
+  const bool narrow = m <= 32 && n > 64;
+  const long long BMc = narrow ? Cfg<1>::BM : Cfg<4>::BM, BNc = narrow ? Cfg<1>::BN : Cfg<4>::BN;
+  const long long tm = (m + BMc - 1) / BMc, tn = (n + BNc - 1) / BNc;
   const long long nkt = (k + BK - 1) / BK;
   // split the k range when the output tiles cannot fill the GPU (two CTAs per SM), keeping
   // at least 16 k tiles per split; the partials cost splits x m x n doubles
@@ -294,23 +318,15 @@ void dgemm(Ctx& c, bool ta, long long m, long long n, long long k, double alpha,
     PW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * (size_t)(splits * m * n), c.stream));
     g.part = part;
   }
-  const bool vec = ((((uintptr_t)A | (uintptr_t)B) & 15) == 0) && !(lda & 1) && !(ldb & 1) && !acol;
-  const bool vec_a_cols = acol && ((((uintptr_t)A | (uintptr_t)B) & 15) == 0) && !(lda & 1) && !(ldb & 1);
+  const bool vec = ((((uintptr_t)A | (uintptr_t)B) & 15) == 0) && !(lda & 1) && !(ldb & 1);
   // tall products (many m tiles, several n tiles): n fastest, so the CTAs in flight work on
   // few row blocks of A and read each from HBM once; B (k x n <= 8 MB) stays in L2
   g.nfast = (tn > 1 && tm >= 4 * tn && tm < 65536) ? 1 : 0;
   PW_CHECK(splits < 65536 && (g.nfast ? (tn < (1LL << 31) && tm < 65536) : (tm < (1LL << 31) && tn < 65536)),
            PW_ERR_VALUE, "dgemm: grid too large");
   dim3 grid(g.nfast ? (unsigned)tn : (unsigned)tm, g.nfast ? (unsigned)tm : (unsigned)tn, (unsigned)splits);
-  // gathered columns keep 16-byte copies along m (the gather is per column)
-  const bool v = vec || vec_a_cols;
-  if (ta) {
-    if (v) launch_cfg<true, true>(c, g, grid);
-    else launch_cfg<true, false>(c, g, grid);
-  } else {
-    if (v) launch_cfg<false, true>(c, g, grid);
-    else launch_cfg<false, false>(c, g, grid);
-  }
+  if (narrow) launch_any<Cfg<1>>(c, g, grid, ta, vec);
+  else launch_any<Cfg<4>>(c, g, grid, ta, vec);
   if (part) {
     const long long total = m * n;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 4LL * slots);

@@ -42,192 +42,306 @@ struct TsqrArgs {
   int nin;              // node levels: R factors at the level below
   const double* rin;    // node levels: those R factors (b x b each, ld b)
   double* vnode;        // node levels: reflectors [node][TB * TL] (column-major, ld TL)
-  double* tau;          // [node][TB]
+  double* tau;          // [node][TB]  (unused by the kernels: T carries tau on its diagonal)
+  double* tnode;        // [node][TB * TB] compact-WY T of every block (b x b, ld b)
   double* rout;         // [node][b * b] R factors of this level
   const double* cin;    // expand: the parent level's output blocks [node][TB * TL], or null (root: C = I)
   double* xout;         // expand, node levels: this level's output blocks [node][TB * TL]
 };
 
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+constexpr int LD = TL + 1;  // shared row stride of a TL x TB block (odd: lane = column is conflict free)
 
-// Householder QR (LAPACK dlarfg convention) of X (TL x b, column-major ld TL) in shared
-// memory: R in the upper triangle, v_j (implicit unit) below the diagonal, tau[j].
-__device__ void block_house_qr(double* X, double* tau, int b) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ double s_tau;
-  for (int j = 0; j < b; ++j) {
-    double* xj = X + j * TL;
-    if (warp == 0) {
-      double ss = 0.0;
+// Thread layout of every block kernel here: lane = column c (0..31), warp = row chunk q
+// (rows 32q .. 32q+31 of the 128-row block).  A column's dot product is four per-warp
+// partials summed through shared memory -- no shuffle reductions on the critical path.
+
+// Householder QR (LAPACK dlarfg convention) of X (TL x b, column-major, ld LD) in shared
+// memory.  Thread (c, q) keeps its 32 entries of column c in registers for the whole
+// factorisation; per column j the owner threads (j, q) publish column j through a
+// shared buffer (read back as broadcasts), so the shared-memory traffic per step is one
+// column instead of the whole block.  Column j stays unscaled while later columns are
+// updated (v_r = x_r * scale[j]); one barrier pair per column: partial dots x_j . x_c
+// for every c >= j (which include ||x_j||), then every thread derives beta, tau, scale
+// and its column's w itself.  The j loop is unrolled so register indices stay static.
+__device__ void block_house_qr(double* X, double* tau, double* scale, double (*part)[TB][4], double (*xb)[TL],
+                               double* xcj_s, int b) {
+  const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
+  double x[32];
 #pragma unroll
-      for (int k = 0; k < TL / 32; ++k) {
-        const int r = lane + 32 * k;
-        const double v = (r > j) ? xj[r] : 0.0;
-        ss = fma(v, v, ss);
-      }
-      ss = warp_sum_d(ss);
-      const double alpha = xj[j];
-      double t = 0.0, beta = alpha, scale = 0.0;
-      if (ss > 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-        t = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      __syncwarp();
-      if (ss > 0.0) {
+  for (int rr = 0; rr < 32; ++rr) x[rr] = X[c * LD + q * 32 + rr];
+  if (c == 0) {
 #pragma unroll
-        for (int k = 0; k < TL / 32; ++k) {
-          const int r = lane + 32 * k;
-          if (r > j) xj[r] *= scale;
-        }
-      }
-      if (lane == 0) {
-        xj[j] = beta;
+    for (int rr = 0; rr < 32; ++rr) xb[0][q * 32 + rr] = x[rr];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < TB; ++j) {
+    if (j >= b) break;
+    double (*pd)[4] = part[j & 1];
+    const double* xjs = xb[j & 1];
+    double xj[32];
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) xj[rr] = xjs[q * 32 + rr];
+    const double alpha = xjs[j];
+    double acc = 0.0;
+    if (c >= j && c < b) {
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr)
+        if (q > 0 || rr > j) a4[rr & 3] = fma(xj[rr], x[rr], a4[rr & 3]);
+      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    }
+    pd[c][q] = acc;
+    if (q == 0) xcj_s[c] = x[j];
+    __syncthreads();
+    const double dj = (pd[j][0] + pd[j][1]) + (pd[j][2] + pd[j][3]);
+    double t = 0.0, beta = alpha, sc = 0.0;
+    if (dj > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, dj)), alpha);
+      t = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    if (c > j && c < b && t != 0.0) {
+      const double dc = (pd[c][0] + pd[c][1]) + (pd[c][2] + pd[c][3]);
+      const double xcj = xcj_s[c];
+      const double w = t * fma(sc, dc, xcj);
+      const double ws = w * sc;
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr)
+        if (q > 0 || rr > j) x[rr] = fma(-ws, xj[rr], x[rr]);
+      if (q == 0) x[j] = xcj - w;  // row j (< 32) lives in chunk 0
+    }
+    if (c == j) {
+      if (q == 0) {
+        x[j] = beta;
         tau[j] = t;
-        s_tau = t;
+        scale[j] = sc;
       }
     }
-    __syncthreads();
-    const double t = s_tau;
-    if (t != 0.0) {
-      for (int c = j + 1 + warp; c < b; c += TTH / 32) {
-        double* xc = X + c * TL;
-        double acc = 0.0;
+    if (c == j + 1 && j + 1 < b) {  // publish the next column (updated above)
 #pragma unroll
-        for (int k = 0; k < TL / 32; ++k) {
-          const int r = lane + 32 * k;
-          if (r > j) acc = fma(xj[r], xc[r], acc);
-        }
-        acc = warp_sum_d(acc);
-        const double w = t * (xc[j] + acc);
-#pragma unroll
-        for (int k = 0; k < TL / 32; ++k) {
-          const int r = lane + 32 * k;
-          if (r > j) xc[r] = fma(-w, xj[r], xc[r]);
-        }
-        if (lane == 0) xc[j] -= w;
-      }
+      for (int rr = 0; rr < 32; ++rr) xb[(j + 1) & 1][q * 32 + rr] = x[rr];
     }
     __syncthreads();
   }
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) X[c * LD + q * 32 + rr] = x[rr];
+  __syncthreads();
 }
 
-// X <- Q X with Q = H_0 H_1 ... H_{b-1} (reflectors V, tau); X is TL x b, each warp owns
-// whole columns of X, so no barrier is needed between reflectors.
-__device__ void block_apply_q(const double* V, const double* tau, double* X, int b) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < b; c += TTH / 32) {
-    double* xc = X + c * TL;
-    double x[TL / 32];
+// After block_house_qr: R (upper b x b) out, X turned into the explicit unit-lower V in
+// place, and the compact-WY T (Q = I - V T V^T, larft) of the block into Tout (b x b).
+__device__ void block_finish(double* X, const double* tau, const double* scale, double* Rout, double* Tout,
+                             double (*G)[TB + 1], int b) {
+  const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < b * b; e += TTH) {
+    const int cc = e / b, r = e - cc * b;
+    Rout[e] = (r <= cc) ? X[cc * LD + r] : 0.0;
+  }
+  __syncthreads();
+  if (c < b) {
+    const double sc = scale[c];
+    for (int rr = 0; rr < 32; ++rr) {
+      const int r = q * 32 + rr;
+      double* p = X + c * LD + r;
+      *p = (r > c) ? *p * sc : (r == c ? 1.0 : 0.0);
+    }
+  }
+  __syncthreads();
+  // G = V^T V on the fp64 tensor cores: warp q computes rows 8q .. 8q+7 of G (four 8 x 8
+  // fragments), k over the TL block rows in steps of 4 (m8n8k4: A = V^T rows, B = V cols)
+  {
+    const int ar = c >> 2, ak = c & 3;
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+    for (int k0 = 0; k0 < TL; k0 += 4) {
+      const double av = X[(q * 8 + ar) * LD + k0 + ak];
 #pragma unroll
-    for (int k = 0; k < TL / 32; ++k) x[k] = xc[lane + 32 * k];
-    for (int j = b - 1; j >= 0; --j) {
-      const double t = tau[j];
-      if (t == 0.0) continue;
-      const double* vj = V + j * TL;
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < TL / 32; ++k) {
-        const int r = lane + 32 * k;
-        if (r > j) acc = fma(vj[r], x[k], acc);
-      }
-      acc = warp_sum_d(acc);
-      // x_j sits in lane j % 32, slot j / 32
-      const double xj = __shfl_sync(0xffffffffu, x[0], j & 31);  // j < 32: slot 0
-      const double w = t * (xj + acc);
-#pragma unroll
-      for (int k = 0; k < TL / 32; ++k) {
-        const int r = lane + 32 * k;
-        if (r > j) x[k] = fma(-w, vj[r], x[k]);
-        else if (r == j) x[k] -= w;
+      for (int f = 0; f < 4; ++f) {
+        const double bv = X[(f * 8 + ar) * LD + k0 + ak];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[f][0]), "+d"(acc[f][1])
+                     : "d"(av), "d"(bv));
       }
     }
 #pragma unroll
-    for (int k = 0; k < TL / 32; ++k) xc[lane + 32 * k] = x[k];
+    for (int f = 0; f < 4; ++f) {
+      G[q * 8 + ar][f * 8 + 2 * ak] = acc[f][0];
+      G[q * 8 + ar][f * 8 + 2 * ak + 1] = acc[f][1];
+    }
+  }
+  __syncthreads();
+  // T by the UT transform: T = S^-1, S = strict_upper(G) + diag(1 / tau) (T^-1 + T^-T =
+  // V^T V for I - V T V^T = H_0 ... H_{b-1}).  Warp 0, lane = column c of T, back
+  // substitution bottom-up with the column in registers (no serial chain across lanes).
+  // A reflector with tau = 0 (H = I: a zero column in this block) has a zero row and column
+  // in T: its S row / column are masked out of the solve.
+  if (q == 0) {
+    double tcol[TB];
+    const bool live_c = c < b && tau[c] != 0.0;
+#pragma unroll
+    for (int r = TB - 1; r >= 0; --r) {
+      double v = 0.0;
+      if (live_c && r <= c && r < b && tau[r] != 0.0) {
+        if (r == c) {
+          v = tau[c];
+        } else {
+          double a2[2] = {0.0, 0.0};
+#pragma unroll
+          for (int k = r + 1; k < TB; ++k)
+            if (k <= c) a2[k & 1] = fma(G[r][k], tcol[k], a2[k & 1]);
+          v = -tau[r] * (a2[0] + a2[1]);
+        }
+      }
+      tcol[r] = v;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < TB; ++r)
+      if (r < c) G[c][r] = tcol[r];  // T's strict upper part, transposed into G's strict lower part
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < b * b; e += TTH) {
+    const int cc = e / b, r = e - cc * b;
+    Tout[e] = (r < cc) ? G[cc][r] : (r == cc ? tau[r] : 0.0);
   }
 }
 
 // Level 0 (LEAF): block i = panel rows [i TL, i TL + TL); level >= 1: block i = the stacked
-// R factors 4i .. 4i+3 of the level below.  Writes this block's R, tau and reflectors.
+// R factors 4i .. 4i+3 of the level below.  Writes this block's R, T and explicit V.
 template <bool LEAF>
 __global__ void __launch_bounds__(TTH) tsqr_qr_kernel(TsqrArgs a) {
-  __shared__ __align__(16) double X[TB * TL];
-  __shared__ double tau[TB];
+  extern __shared__ __align__(16) double X[];  // TB x LD
+  __shared__ double tau[TB], scale[TB];
+  __shared__ double part[2][TB][4];
+  __shared__ double G[TB][TB + 1];
+  __shared__ double xb[2][TL];
+  __shared__ double xcj_s[TB];
   const int b = a.b;
   const long long i = blockIdx.x;
   const long long r0 = i * TL;
-  for (int e = threadIdx.x; e < TB * TL; e += TTH) {
-    const int c = e / TL, r = e - c * TL;
-    double v = 0.0;
-    if (c < b) {
-      if (LEAF) {
-        if (r0 + r < a.rows) v = a.panel[r0 + r + (long long)c * a.lda];
-      } else {
-        const long long child = 4 * i + r / b;
-        if (r < 4 * b && child < a.nin) v = a.rin[child * b * b + (r % b) + (long long)c * b];
+  static_assert(TTH == TL, "one block row per thread in the load / store phases");
+  {
+    // thread = row: all 32 loads in flight before the first shared store (coalesced per column)
+    const int r = threadIdx.x;
+    double v[TB];
+    const double* src = nullptr;
+    long long ld = 0;
+    if (LEAF) {
+      if (r0 + r < a.rows) {
+        src = a.panel + r0 + r;
+        ld = a.lda;
+      }
+    } else {
+      const long long child = 4 * i + r / b;
+      if (r < 4 * b && child < a.nin) {
+        src = a.rin + child * b * b + (r % b);
+        ld = b;
       }
     }
-    X[e] = v;
+#pragma unroll
+    for (int c = 0; c < TB; ++c) v[c] = (src && c < b) ? src[c * ld] : 0.0;
+#pragma unroll
+    for (int c = 0; c < TB; ++c) X[c * LD + r] = v[c];
   }
   __syncthreads();
-  block_house_qr(X, tau, b);
-  // R (b x b, zero below the diagonal), tau, reflectors
-  for (int e = threadIdx.x; e < b * b; e += TTH) {
-    const int c = e / b, r = e - c * b;
-    a.rout[i * b * b + e] = (r <= c) ? X[c * TL + r] : 0.0;
-  }
-  if (threadIdx.x < TB) a.tau[i * TB + threadIdx.x] = threadIdx.x < b ? tau[threadIdx.x] : 0.0;
-  for (int e = threadIdx.x; e < b * TL; e += TTH) {
-    const int c = e / TL, r = e - c * TL;
-    if (LEAF) {
-      if (r0 + r < a.rows) a.panel[r0 + r + (long long)c * a.lda] = X[e];
-    } else {
-      a.vnode[i * (TB * TL) + e] = X[e];
+  block_house_qr(X, tau, scale, part, xb, xcj_s, b);
+  block_finish(X, tau, scale, a.rout + i * b * b, a.tnode + i * TB * TB, G, b);
+  __syncthreads();
+  {
+    const int r = threadIdx.x;
+    double* dst = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.vnode + i * (TB * TL) + r;
+    const long long ld = LEAF ? a.lda : TL;
+    if (dst) {
+#pragma unroll
+      for (int c = 0; c < TB; ++c)
+        if (c < b) dst[c * ld] = X[c * LD + r];
     }
   }
 }
 
-// Top-down explicit Q: block i's output = Q_i [C_i; 0], C_i = rows (i % 4) b.. of the parent's
-// output block (or I at the root).  Leaves write their rows of the sub-panel's Q in place.
+// Top-down explicit Q: block i's output = Q_i [C_i; 0] = [C_i; 0] - V (T (V_top^T C_i)),
+// C_i = rows (i % 4) b .. of the parent's output block (I at the root): two b x b products
+// and one TL x b x b product per block, no reductions over rows.  Leaves write their rows
+// of the sub-panel's Q in place.
 template <bool LEAF>
 __global__ void __launch_bounds__(TTH) tsqr_expand_kernel(TsqrArgs a) {
-  extern __shared__ __align__(16) double sm[];
-  double* V = sm;
-  double* X = sm + TB * TL;
-  __shared__ double tau[TB];
+  extern __shared__ __align__(16) double V[];  // TB x LD, then reused for the output
+  __shared__ double C[TB][TB + 1], Y[TB][TB + 1], T[TB][TB + 1];
   const int b = a.b;
   const long long i = blockIdx.x;
   const long long r0 = i * TL;
-  for (int e = threadIdx.x; e < TB * TL; e += TTH) {
-    const int c = e / TL, r = e - c * TL;
-    double v = 0.0, x = 0.0;
-    if (c < b) {
-      if (LEAF) {
-        if (r0 + r < a.rows) v = a.panel[r0 + r + (long long)c * a.lda];
-      } else {
-        v = a.vnode[i * (TB * TL) + e];
-      }
-      if (r < b) {
-        x = a.cin ? a.cin[(i / 4) * (TB * TL) + (long long)c * TL + (i % 4) * b + r] : (r == c ? 1.0 : 0.0);
-      }
-    }
-    V[e] = v;
-    X[e] = x;
+  const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
+  {
+    const int r = threadIdx.x;
+    const double* src = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.vnode + i * (TB * TL) + r;
+    const long long ld = LEAF ? a.lda : TL;
+    double v[TB];
+#pragma unroll
+    for (int cc = 0; cc < TB; ++cc) v[cc] = (src && cc < b) ? src[cc * ld] : 0.0;
+#pragma unroll
+    for (int cc = 0; cc < TB; ++cc) V[cc * LD + r] = v[cc];
   }
-  if (threadIdx.x < TB) tau[threadIdx.x] = threadIdx.x < b ? a.tau[i * TB + threadIdx.x] : 0.0;
+  for (int e = threadIdx.x; e < TB * TB; e += TTH) {
+    const int cc = e / TB, r = e - cc * TB;
+    double x = 0.0, t = 0.0;
+    if (cc < b && r < b) {
+      x = a.cin ? a.cin[(i / 4) * (TB * TL) + (long long)cc * TL + (i % 4) * b + r] : (r == cc ? 1.0 : 0.0);
+      t = a.tnode[i * TB * TB + r + cc * b];
+    }
+    C[r][cc] = x;  // C[row][col]
+    T[r][cc] = t;
+  }
   __syncthreads();
-  block_apply_q(V, tau, X, b);
+  // Y = V_top^T C  (thread (c, q): rows 8q .. 8q+7 of Y, column c)
+  double y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int row = q * 8 + k;
+    double acc = 0.0;
+    for (int kk = 0; kk < b; ++kk) acc = fma(V[row * LD + kk], C[kk][c], acc);
+    y[k] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) Y[q * 8 + k][c] = y[k];
   __syncthreads();
-  for (int e = threadIdx.x; e < b * TL; e += TTH) {
-    const int c = e / TL, r = e - c * TL;
-    if (LEAF) {
-      if (r0 + r < a.rows) a.panel[r0 + r + (long long)c * a.lda] = X[e];
-    } else {
-      a.xout[i * (TB * TL) + e] = X[e];
+  // Y2 = T Y   (same ownership; T upper triangular)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int row = q * 8 + k;
+    double acc = 0.0;
+    for (int kk = row; kk < b; ++kk) acc = fma(T[row][kk], Y[kk][c], acc);
+    y[k] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) Y[q * 8 + k][c] = y[k];
+  __syncthreads();
+  // X = [C; 0] - V Y2: thread (c, q) computes rows 32q .. 32q+31 of column c
+  double x[32];
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    const int r = q * 32 + rr;
+    x[rr] = (r < TB) ? C[r][c] : 0.0;
+  }
+  for (int kk = 0; kk < b; ++kk) {
+    const double ykk = Y[kk][c];
+    const double* vk = V + kk * LD + q * 32;
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) x[rr] = fma(-vk[rr], ykk, x[rr]);
+  }
+  __syncthreads();  // everyone done reading V: reuse it for the output
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) V[c * LD + q * 32 + rr] = x[rr];
+  __syncthreads();
+  {
+    const int r = threadIdx.x;
+    double* dst = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.xout + i * (TB * TL) + r;
+    const long long ld = LEAF ? a.lda : TL;
+    if (dst) {
+#pragma unroll
+      for (int cc = 0; cc < TB; ++cc)
+        if (cc < b) dst[cc * ld] = V[cc * LD + r];
     }
   }
 }
@@ -316,7 +430,7 @@ __global__ void __launch_bounds__(128) recon_solve_kernel(double* panel, long lo
   }
 }
 
-size_t expand_smem() { return sizeof(double) * 2 * TB * TL; }
+size_t block_smem() { return sizeof(double) * TB * LD; }
 
 }  // namespace
 
@@ -335,7 +449,7 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
   // small blocks (U, Vtop, T), and the trailing GEMM temporaries (W, X: TB x p each)
   long long total_nodes = n0 + nodes_above;
   const size_t n_r = (size_t)total_nodes * TB * TB;
-  const size_t n_tau = (size_t)total_nodes * TB;
+  const size_t n_tau = (size_t)total_nodes * TB * TB;  // T of every block
   const size_t n_v = (size_t)nodes_above * TB * TL;
   const size_t n_small = 3 * TB * TB;
   const size_t n_w = 2 * (size_t)TB * p;
@@ -355,8 +469,10 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
     off[l] = off[l - 1] + nl[l - 1];
     voff[l] = (l == 1) ? 0 : voff[l - 1] + nl[l - 1];
   }
-  kernel_setup(c, tsqr_expand_kernel<true>, TTH, expand_smem());
-  kernel_setup(c, tsqr_expand_kernel<false>, TTH, expand_smem());
+  kernel_setup(c, tsqr_qr_kernel<true>, TTH, block_smem());
+  kernel_setup(c, tsqr_qr_kernel<false>, TTH, block_smem());
+  kernel_setup(c, tsqr_expand_kernel<true>, TTH, block_smem());
+  kernel_setup(c, tsqr_expand_kernel<false>, TTH, block_smem());
   for (long long j0 = 0; j0 < kmax; j0 += TB) {
     const int b = (int)std::min<long long>(TB, kmax - j0);
     const long long mrows = rows - j0;
@@ -372,15 +488,15 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
     a.b = b;
     // 1. TSQR up the tree
     for (int l = 0; l < L; ++l) {
-      a.tau = Tb + off[l] * TB;
+      a.tnode = Tb + off[l] * TB * TB;
       a.rout = Rb + off[l] * TB * TB;
       if (l == 0) {
-        tsqr_qr_kernel<true><<<(unsigned)ml[0], TTH, 0, c.stream>>>(a);
+        tsqr_qr_kernel<true><<<(unsigned)ml[0], TTH, block_smem(), c.stream>>>(a);
       } else {
         a.rin = Rb + off[l - 1] * TB * TB;
         a.nin = (int)ml[l - 1];
         a.vnode = Vb + voff[l] * TB * TL;
-        tsqr_qr_kernel<false><<<(unsigned)ml[l], TTH, 0, c.stream>>>(a);
+        tsqr_qr_kernel<false><<<(unsigned)ml[l], TTH, block_smem(), c.stream>>>(a);
       }
       c.launches += 1;
       PW_LAUNCH_CHECK();
@@ -388,14 +504,14 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
     const double* Rroot = Rb + off[L - 1] * TB * TB;
     // 2. explicit Q down the tree
     for (int l = L - 1; l >= 0; --l) {
-      a.tau = Tb + off[l] * TB;
+      a.tnode = Tb + off[l] * TB * TB;
       a.cin = (l == L - 1) ? nullptr : Xb + voff[l + 1] * TB * TL;
       if (l == 0) {
-        tsqr_expand_kernel<true><<<(unsigned)ml[0], TTH, expand_smem(), c.stream>>>(a);
+        tsqr_expand_kernel<true><<<(unsigned)ml[0], TTH, block_smem(), c.stream>>>(a);
       } else {
         a.vnode = Vb + voff[l] * TB * TL;
         a.xout = Xb + voff[l] * TB * TL;
-        tsqr_expand_kernel<false><<<(unsigned)ml[l], TTH, expand_smem(), c.stream>>>(a);
+        tsqr_expand_kernel<false><<<(unsigned)ml[l], TTH, block_smem(), c.stream>>>(a);
       }
       c.launches += 1;
       PW_LAUNCH_CHECK();
