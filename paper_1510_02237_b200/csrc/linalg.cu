@@ -873,6 +873,24 @@ void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv,
   PW_LAUNCH_CHECK();
 }
 
+// Xc (r x r, ld r) = rows piv[0..r) of X (m x r, ld m): the compact upper-triangular R11^-1
+__global__ void gather_rows_kernel(const double* __restrict__ X, int m, const int* __restrict__ piv, int r,
+                                   double* __restrict__ Xc) {
+  const long long total = (long long)r * r;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / r), k = (int)(e - (long long)j * r);
+    Xc[e] = X[piv[k] + (long long)j * m];
+  }
+}
+
+void launch_gather_rows(Ctx& c, const double* X, int m, const int* piv, int r, double* Xc) {
+  if (r <= 0) return;
+  const long long total = (long long)r * r;
+  gather_rows_kernel<<<(int)std::min<long long>((total + 255) / 256, 1024), 256, 0, c.stream>>>(X, m, piv, r, Xc);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
 static int cg_variant() {
   static int v = -1;
   if (v < 0) {

@@ -198,6 +198,9 @@ void dgemm(Ctx& c, bool ta, long long m, long long n, long long k, double alpha,
            const double* B, long long ldb, double beta, double* C, long long ldc, const int* acol = nullptr,
            bool b_upper = false);
 
+// Xc (r x r) = rows piv[0..r) of X (m x r): R11^-1 back from its scattered form
+void launch_gather_rows(Ctx& c, const double* X, int m, const int* piv, int r, double* Xc);
+
 // tall-skinny Householder QR (tsqr.cu): LAPACK geqrf's output format for rows x p
 void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double* tau);
 
