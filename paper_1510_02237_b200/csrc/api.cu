@@ -226,6 +226,17 @@ bool prop_apply_impl(pw_prop* P, const double* in, double* out, int batch, long 
       ld_src = d;
     }
     double* tmp = P->t2.ensure(c, (size_t)d * batch);
+    if (npeer == 0 && !P->vadv && pw::mtma_enabled() &&
+        pw::mtma_supported(P->fp.nx, P->fp.ny, ld_src, ld, src, out, tmp)) {
+      // K1: TMA-fed persistent row march over all nsteps (march_tma.cu)
+      int* sync = reinterpret_cast<int*>(
+          P->sync.ensure(c, (pw::march_persist_sync_ints(P->fp.ny, batch) + 1) / 2));
+      pw::FusedParams fp = P->fp;
+      fp.ld_in = ld_src;
+      fp.ld_out = ld;
+      pw::launch_rk3_mtma(c, fp, src, out, tmp, batch, nsteps, d, sync);
+      return false;
+    }
     if (npeer == 0 && nsteps >= 2 && !P->vadv && pw::march_persist_enabled(P->fp.nx) &&
         pw::march_supported(P->fp.nx, P->fp.ny, ld_src, ld, src, out) &&
         pw::march_supported(P->fp.nx, P->fp.ny, d, d, tmp, tmp)) {

@@ -1,0 +1,455 @@
+// K1: TMA-fed, row-marching, persistent RK3 propagation for constant x-advection (V = 0),
+// sm_100a, fp64.  The production fine kernel for rows of 128 / 256 / 384 / 512 cells.
+//
+// Operator: the folded constant-velocity WS-RK3 step of fine_fused.cu (integrators.py:126-146
+// rk3_step with acoustic_rhs, numba_backend.py:119-128): stage S computes
+// s_out = q + beta_S L(s_in) as 7-point x stencils plus narrow y differences (radius 1 for u
+// and p, radius 2 for the v damping).  Results equal the reference up to rounding (tests:
+// <= 1e-12 relative against the oracle).
+//
+// Data movement, designed from the previous kernel's ncu profile (fine_march.cu: issue-bound,
+// ~110 of ~290 instructions per thread and tick were cp.async address generation, spill
+// reloads and the v register rotation):
+//
+// * A CTA owns whole grid rows of one state and a y-segment of TY rows.  Three warp groups,
+//   one per RK stage, march down the segment one row per tick: in tick t stage 1 consumes
+//   q row t-6, stage 2 s1 row t-9, stage 3 s2 row t-12, all reading rows finished in an
+//   earlier tick, so one CTA barrier per tick.
+// * q rows arrive by ONE 5-D TMA copy per row (u, v, p together: box {4, NX/4, 1, 3, 1} of
+//   the view {4, NX/4, ny, 3, batch}) issued by one thread two ticks ahead into an 8-slot
+//   ring, completion on a per-slot mbarrier.  The copy lands with the 32-byte swizzle, which
+//   is exactly the chunk XOR the window loads need (16-byte chunk c at c ^ ((c >> 3) & 1)):
+//   the 32-byte per-thread stride of the window loads is bank-conflict free.
+// * No ghost columns: the periodic x wrap lives in each thread's window offset table (the
+//   first thread's left chunks point at the row's end, the last thread's right chunks at
+//   its start), so ring rows are exactly NX doubles and nothing is copied twice.
+// * y coupling in registers: a thread consuming row k adds its x-stencil terms to row k and
+//   its y-difference terms to rows k-1 and k+1; u and p keep rows k-1..k+1 in 3 fixed slots
+//   (row mod 3, the tick loop is unrolled 3x).  v's radius-2 damping keeps only 3 rows plus
+//   h = dv2 v(k-1), added when row k+1 is born: no register rotation at all.
+// * Persistent: one launch runs every RK3 step of the propagation.  CTAs take work items
+//   (step, state, segment) in order from an atomic counter; an item waits on the step
+//   counters of its three neighbouring segments (the y halo it reads and the buffer it
+//   overwrites), so items never deadlock and there is no wave quantisation between steps.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "pw_internal.h"
+
+namespace pw {
+namespace {
+
+template <int NX_>
+struct TK {
+  static constexpr int NX = NX_, BX = 4;
+  static constexpr int GS = NX / BX;   // threads per stage group
+  static constexpr int NT = 3 * GS;
+  static constexpr int CH = NX / 2;    // 16-byte chunks per field row
+  static constexpr int SLOT = 3 * NX;  // doubles per ring slot: u, v, p rows
+  static constexpr int NQ = 8, N1 = 3, N2 = 3;
+  static constexpr size_t RING = sizeof(double) * SLOT * (NQ + N1 + N2);
+  static constexpr size_t SMEM = RING + 1024 + 8 * NQ;  // + alignment slack + mbarriers
+  static constexpr uint32_t ROW_BYTES = SLOT * sizeof(double);
+  static constexpr int MB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
+  static constexpr int MB_REGS = 65536 / (NT * 168);
+  static constexpr int MINB = (MB_SMEM < MB_REGS ? MB_SMEM : MB_REGS) < 1 ? 1 : (MB_SMEM < MB_REGS ? MB_SMEM : MB_REGS);
+  static_assert(GS % 32 == 0, "stage groups must be whole warps");
+  static_assert((SLOT * 8) % 1024 == 0, "ring slots keep the 1024-byte TMA alignment");
+};
+
+__device__ __forceinline__ int swz(int c) { return c ^ ((c >> 3) & 1); }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// one q row (u, v, p of state b, grid row gy) into a ring slot
+__device__ __forceinline__ void tma_row(const CUtensorMap* map, double* slot, uint64_t* bar, int gy, int b,
+                                        uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(slot)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(0), "r"(gy), "r"(0), "r"(b), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void ld_chunks(double (&w)[2 * N], const double* row, const int* off) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double2 t = *reinterpret_cast<const double2*>(row + off[j]);
+    w[2 * j] = t.x;
+    w[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void st4(double* row, const int* off, const double (&v)[4]) {
+  *reinterpret_cast<double2*>(row + off[0]) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(row + off[1]) = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void stg4(double* p, const double (&v)[4]) {
+  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+}
+
+// One stage thread's registers: u, p rows k-1..k+1 and v rows k-2..k (slot = row mod 3),
+// h = dv2 v(k-1) for the birth of v row k+1.
+struct Acc {
+  double u[3][4], p[3][4], v[3][4], h[4];
+};
+
+// Where the completed rows go: the next stage's ring (S < 2) or the state in HBM (S = 2).
+struct Sink {
+  double* ring;     // S < 2: the output ring's slot 0
+  double* g;        // S = 2: this thread's columns of the segment's first row (u field)
+  long long n;      // nx * ny (field stride)
+  int TY;
+};
+
+// Consume input row k (ring slot `in`; q row k+1 at `qb` for the births when S > 0), store
+// the completed rows: u, p of row k-1 and v of row k-2.  PH = k mod 3 (compile time).
+template <int NX, int S, int PH>
+__device__ __forceinline__ void row_step(Acc& A, const double* in, const double* qb, const int* woff,
+                                         const StageCoef& C, const Sink& o, int k) {
+  constexpr int U0 = (PH + 2) % 3, U1 = PH, U2 = (PH + 1) % 3;  // u, p: rows k-1, k, k+1
+  constexpr int V0 = (PH + 1) % 3, V1 = (PH + 2) % 3, V2 = PH;  // v: rows k-2 (-> k+1), k-1, k
+  double w[12];
+  // ---- v row k: x stencil of row k; completes v(k-2); births v(k+1); u_y-mixed / p_y terms
+  ld_chunks<6>(w, in + NX, woff);
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)  // cxv equals cxp off the centre
+      A.v[V2][c] = fma(m == 3 ? C.cxv[3] : C.cxp[m], w[c + 1 + m], A.v[V2][c]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) A.v[V0][c] = fma(C.dv2, w[c + 4], A.v[V0][c]);
+  if constexpr (S < 2) {
+    st4(o.ring + ((PH + 1) % 3) * (3 * NX) + NX, woff + 2, A.v[V0]);
+  } else {
+    if (k - 2 >= 0 && k - 2 < o.TY) stg4(o.g + o.n + (long long)(k - 2) * NX, A.v[V0]);
+  }
+  {
+    double b[4];
+    if constexpr (S > 0) ld_chunks<2>(b, qb + NX, woff + 2);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      A.v[V0][c] = (S > 0) ? b[c] + A.h[c] : A.h[c];  // v(k+1) = q + dv2 v(k-1)
+      A.h[c] = C.dv2 * w[c + 4];
+    }
+  }
+  {
+    double bu[4], bp[4];
+    if constexpr (S > 0) {
+      ld_chunks<2>(bu, qb, woff + 2);
+      ld_chunks<2>(bp, qb + 2 * NX, woff + 2);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double t1 = C.cuv * (w[c + 5] - w[c + 3]);
+      A.u[U0][c] += t1;
+      A.u[U2][c] = (S > 0) ? bu[c] - t1 : -t1;
+      A.p[U0][c] = fma(C.pv, w[c + 4], A.p[U0][c]);
+      A.p[U2][c] = (S > 0) ? fma(-C.pv, w[c + 4], bp[c]) : -C.pv * w[c + 4];
+    }
+  }
+  if constexpr (S < 2) {
+    double* r = o.ring + ((PH + 2) % 3) * (3 * NX);
+    st4(r, woff + 2, A.u[U0]);
+    st4(r + 2 * NX, woff + 2, A.p[U0]);
+  } else {
+    if (k - 1 >= 0 && k - 1 < o.TY) {
+      double* g = o.g + (long long)(k - 1) * NX;
+      stg4(g, A.u[U0]);
+      stg4(g + 2 * o.n, A.p[U0]);
+    }
+  }
+  // ---- u row k: x stencil; u_x for p(k) and the mixed damping of v(k-1), v(k+1)
+  double t2[4];
+  ld_chunks<6>(w, in, woff);
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)  // cxu equals cxp at the odd offsets -3, -1, 1, 3
+      A.u[U1][c] = fma((m & 1) ? C.cxu[m] : C.cxp[m], w[c + 1 + m], A.u[U1][c]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double bx = w[c + 5] - w[c + 3];
+    A.p[U1][c] = fma(C.pu, bx, A.p[U1][c]);
+    t2[c] = C.cvu * bx;
+  }
+  // ---- p row k: x stencil; p_x for u(k), p_y for v(k-1), v(k+1)
+  ld_chunks<6>(w, in + 2 * NX, woff);
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) A.p[U1][c] = fma(C.cxp[m], w[c + 1 + m], A.p[U1][c]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    A.u[U1][c] = fma(C.pu, w[c + 5] - w[c + 3], A.u[U1][c]);  // pgx == pu
+    t2[c] = fma(C.pv, w[c + 4], t2[c]);                        // pgy == pv
+    A.v[V1][c] += t2[c];
+    A.v[V0][c] -= t2[c];
+  }
+}
+
+struct Item {
+  int y0, TY, b;
+  uint32_t seq;  // q rows this CTA issued before the item (ring slot / mbarrier phase base)
+  const CUtensorMap* map;
+};
+
+// q ring slot and mbarrier parity of segment row r (r >= -6)
+__device__ __forceinline__ uint32_t qslot(uint32_t seq, int r) { return (seq + (uint32_t)(r + 6)) & 7u; }
+__device__ __forceinline__ uint32_t qpar(uint32_t seq, int r) { return ((seq + (uint32_t)(r + 6)) >> 3) & 1u; }
+
+template <class K>
+__device__ __forceinline__ void issue(double* ring, uint64_t* full, const Item& it, int ny, int r) {
+  int gy = it.y0 + r;
+  gy += (gy < 0) ? ny : 0;
+  gy -= (gy >= ny) ? ny : 0;
+  const uint32_t s = qslot(it.seq, r);
+  tma_row(it.map, ring + (size_t)s * K::SLOT, full + s, gy, it.b, K::ROW_BYTES);
+}
+
+// One tick: the CTA barrier, the q row two ticks ahead, then stage S's row k = t - lag.
+template <class K, int I>
+__device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const Item& it, const FusedParams& P,
+                                     int S, int t, const int* woff, const Sink& o, bool producer) {
+  constexpr int NX = K::NX;
+  bar_sync();
+  if (producer && t - 4 <= it.TY + 5) issue<K>(ring, full, it, P.ny, t - 4);
+  double* q = ring;
+  double* r1 = ring + K::NQ * K::SLOT;
+  double* r2 = r1 + K::N1 * K::SLOT;
+  // k = t - lag with lag in {6, 9, 12}: k mod 3 = t mod 3 = I
+  if (S == 0) {
+    const int k = t - 6;
+    if (k > it.TY + 5) return;
+    const uint32_t s = qslot(it.seq, k);
+    mbar_wait(full + s, qpar(it.seq, k));
+    row_step<NX, 0, I>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k);
+  } else if (S == 1) {
+    const int k = t - 9;
+    if (k < -4 || k > it.TY + 3) return;
+    const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
+    row_step<NX, 1, I>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k);
+  } else {
+    const int k = t - 12;
+    if (k < -2 || k > it.TY + 1) return;
+    const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
+    row_step<NX, 2, I>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k);
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
+    const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_out,
+    const __grid_constant__ CUtensorMap map_tmp, double* out, double* tmp, long long ld_out, long long ld_tmp,
+    const __grid_constant__ FusedParams P, int nseg, int batch, int nsteps, int* sync) {
+  constexpr int NX = K::NX;
+  extern __shared__ unsigned char smraw[];
+  // 1024-byte aligned ring (offset arithmetic on smraw keeps the shared address space visible)
+  double* ring = reinterpret_cast<double*>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)K::SLOT * (K::NQ + K::N1 + K::N2));
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < K::NQ; ++s) mbar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // warp-uniform stage index (through a shuffle, so the compiler knows it)
+  const int S = __shfl_sync(0xffffffffu, tid / K::GS, 0);
+  const int g = tid - S * K::GS;
+  // window chunk offsets: cols [4g - 4, 4g + 8) as 6 chunks, wrapped periodically
+  int woff[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    int c = 2 * g - 2 + j;
+    c += (c < 0) ? K::CH : 0;
+    c -= (c >= K::CH) ? K::CH : 0;
+    woff[j] = 2 * swz(c);
+  }
+  const bool producer = (tid == 0);
+  const int ny = P.ny;
+  const long long n = (long long)NX * ny;
+  const int per_step = nseg * batch;
+  const long long total = (long long)per_step * nsteps;
+  int* done = sync + 1;
+  uint32_t seq = 0;
+  double* ring_out = S == 0 ? ring + K::NQ * K::SLOT : ring + (K::NQ + K::N1) * K::SLOT;
+  for (;;) {
+    __syncthreads();  // s_item of the previous item is no longer read; rings are free
+    if (tid == 0) s_item = atomicAdd(sync, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) break;
+    const int s = item / per_step;
+    const int rem = item - s * per_step;
+    const int b = rem / nseg, j = rem - b * nseg;
+    if (s > 0 && tid < 3) {  // the three neighbouring segments finished step s-1
+      int jj = j + tid - 1;
+      jj += (jj < 0) ? nseg : 0;
+      jj -= (jj >= nseg) ? nseg : 0;
+      const int* f = done + b * nseg + jj;
+      long long spins = 0;
+      while (ld_acquire(f) < s) {
+        __nanosleep(64);
+        if (++spins > (1LL << 26)) __trap();  // a broken dependency fails, never hangs
+      }
+    }
+    __syncthreads();
+    // the neighbours' generic-proxy stores (seen through the acquire) before this CTA's TMA reads
+    if (producer) asm volatile("fence.proxy.async.global;" ::: "memory");
+    // ping-pong so that the last step lands in out
+    const bool to_out = ((nsteps - 1 - s) % 2) == 0;
+    Item it;
+    it.y0 = (int)((long long)j * ny / nseg);
+    it.TY = (int)((long long)(j + 1) * ny / nseg) - it.y0;
+    it.b = b;
+    it.seq = seq;
+    it.map = s == 0 ? &map_in : (to_out ? &map_tmp : &map_out);
+    Sink o;
+    o.ring = ring_out;
+    o.n = n;
+    o.TY = it.TY;
+    o.g = (to_out ? out + (long long)b * ld_out : tmp + (long long)b * ld_tmp) + (long long)it.y0 * NX + 4 * g;
+    if (producer) {  // prologue: q rows -6 and -5 (stage 1's ticks 0 and 1)
+      issue<K>(ring, full, it, ny, -6);
+      issue<K>(ring, full, it, ny, -5);
+    }
+    Acc A;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) A.u[r][c] = A.p[r][c] = A.v[r][c] = 0.0;
+      A.h[c] = 0.0;
+    }
+    // tick count rounded up to the unroll (equal barrier counts for every warp)
+    const int nt = (it.TY + 14 + 2) / 3 * 3;
+    for (int t = 0; t < nt; t += 3) {
+      tick<K, 0>(A, ring, full, it, P, S, t, woff, o, producer);
+      tick<K, 1>(A, ring, full, it, P, S, t + 1, woff, o, producer);
+      tick<K, 2>(A, ring, full, it, P, S, t + 2, woff, o, producer);
+    }
+    seq += (uint32_t)(it.TY + 12);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // stores before later TMA reads
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(done + b * nseg + j, s + 1);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  PW_CHECK(fn != nullptr, PW_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+  return fn;
+}
+
+// view {4, nx/4, ny, 3, batch} of a batch of states (ld doubles apart); box = one grid row
+// of the three fields, 32-byte swizzle
+CUtensorMap row_map(const double* base, int nx, int ny, long long ld, int batch) {
+  CUtensorMap m;
+  const cuuint64_t dims[5] = {4, (cuuint64_t)nx / 4, (cuuint64_t)ny, 3, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {32, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8, (cuuint64_t)ld * 8};
+  const cuuint32_t box[5] = {4, (cuuint32_t)nx / 4, 1, 3, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  PW_CHECK(r == CUDA_SUCCESS, PW_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+int env_int2(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+
+template <class K>
+void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp, int batch, int nsteps,
+                long long d, int* sync) {
+  auto kern = rk3_mtma_kernel<K>;
+  const int per_sm = kernel_setup(c, kern, K::NT, K::SMEM);
+  const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
+  // segments per state: ticks per item (TY + 14) x max(1, items / CTA slots), clamped so
+  // every segment has >= 16 rows (the 6-row halo of the neighbour dependency, and the
+  // sync buffer's ny / 16 + 1 counters per state)
+  int nseg = env_int2("PW_MARCH_NSEG", 0);
+  if (nseg <= 0) {
+    double best = 1e300;
+    for (int s = 1; s <= fp.ny / 16; ++s) {
+      const double items = (double)batch * s;
+      const double cost = ((double)fp.ny / s + 14.0) * std::max(1.0, items / (double)slots);
+      if (cost < best - 1e-9) {
+        best = cost;
+        nseg = s;
+      }
+    }
+  }
+  nseg = std::max(1, std::min(nseg, fp.ny / 16));
+  const CUtensorMap m_in = row_map(in, fp.nx, fp.ny, fp.ld_in, batch);
+  const CUtensorMap m_out = row_map(out, fp.nx, fp.ny, fp.ld_out, batch);
+  const CUtensorMap m_tmp = row_map(tmp, fp.nx, fp.ny, d, batch);
+  const long long items = (long long)batch * nseg * nsteps;
+  const int grid = (int)std::min<long long>(slots, items);
+  PW_CUDA(cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)batch * nseg), c.stream));
+  kern<<<grid, K::NT, K::SMEM, c.stream>>>(m_in, m_out, m_tmp, out, tmp, fp.ld_out, d, fp, nseg, batch, nsteps,
+                                           sync);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool mtma_enabled() { return env_int2("PW_MARCH_V2", 1) != 0; }
+
+bool mtma_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in, const void* out,
+                    const void* tmp) {
+  if (!(nx == 128 || nx == 256 || nx == 384 || nx == 512)) return false;
+  if (ny < 32) return false;
+  if ((ld_in & 1) || (ld_out & 1)) return false;
+  return (((uintptr_t)in | (uintptr_t)out | (uintptr_t)tmp) & 15) == 0;
+}
+
+void launch_rk3_mtma(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp, int batch,
+                     int nsteps, long long d, int* sync) {
+  switch (fp.nx) {
+    case 128: return launch_cfg<TK<128>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 256: return launch_cfg<TK<256>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 384: return launch_cfg<TK<384>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 512: return launch_cfg<TK<512>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    default: throw Error{PW_ERR_VALUE, "TMA row march needs nx in {128, 256, 384, 512}"};
+  }
+}
+
+}  // namespace pw

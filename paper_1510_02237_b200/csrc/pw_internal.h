@@ -179,6 +179,13 @@ size_t march_persist_sync_ints(int ny, int batch);
 void launch_rk3_march_persist(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp,
                               int batch, int nsteps, long long d, int* sync);
 
+// march_tma.cu: the TMA-fed persistent row march (K1; default, PW_MARCH_V2=0 turns it off)
+bool mtma_enabled();
+bool mtma_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in, const void* out,
+                    const void* tmp);
+void launch_rk3_mtma(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp, int batch,
+                     int nsteps, long long d, int* sync);
+
 // linalg.cu
 void launch_axpby_cols(Ctx& c, double* y, const double* a, const double* b, double alpha,
                        double beta, size_t n);

@@ -2,8 +2,9 @@
 
 64 states x 256^2 x 200 RK3 steps (CFL 0.5, order 6, nu 0.005, cs 1, U 0.1),
 seeded random-mode inputs (seed 2001, the bench's rank-0 batch), through the
-default device path (the persistent row-marching kernel) and through the
-per-step launches (PW_MARCH_PERSIST=0), each state compared with the C
+default device path (K1, the TMA-fed persistent row march, march_tma.cu) and
+through the previous-generation kernels (PW_MARCH_V2=0: the cp.async persistent march
+and its per-step launches, PW_MARCH_PERSIST=0), each state compared with the C
 oracle (reference operation order, oracle/pw_oracle.c; integrators.py:126-146,
 numba_backend.py:119-128).
 
@@ -56,13 +57,15 @@ def _check(got, want):
     return err.max()
 
 
-@pytest.mark.parametrize("persist", ["", "0"])
-def test_bench_workload_every_state_matches_oracle(c2, monkeypatch, persist):
+@pytest.mark.parametrize("env", [{}, {"PW_MARCH_V2": "0"}, {"PW_MARCH_V2": "0", "PW_MARCH_PERSIST": "0"}],
+                         ids=["tma-persistent", "cpasync-persistent", "cpasync-per-step"])
+def test_bench_workload_every_state_matches_oracle(c2, monkeypatch, env):
+    """The default K1 (march_tma.cu) and both previous-generation paths, every state."""
     from paper_1510_02237_b200.integrators import SlicePropagator
 
     q0, want = c2
-    if persist:
-        monkeypatch.setenv("PW_MARCH_PERSIST", persist)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     prop = SlicePropagator(_spec(), nsteps=STEPS)
     x = torch.as_tensor(q0).cuda()
     got = prop.apply(x).cpu().numpy()

@@ -1,6 +1,7 @@
-"""Row-marching fused RK3 kernel (csrc/fine_march.cu) vs the oracle (B200 only).
+"""Row-marching fused RK3 kernels (K1: csrc/march_tma.cu; previous generation
+csrc/fine_march.cu) vs the oracle (B200 only).
 
-The marching kernel serves V = 0 on grids with nx in {128, 256, 384, 512}.
+The marching kernels serve V = 0 on grids with nx in {128, 256, 384, 512}.
 Tolerance: <= 1e-12 relative L2 per state, as for the tile kernel (its
 arithmetic differs from the reference only by rounding).  Cases cover every
 flux order, non-square grids, ny not a multiple of the segment count
@@ -138,11 +139,12 @@ def test_march_strided_batch_and_blowup(dev):
     (384, 48, 3, 2, 2),
 ])
 def test_persistent_march_matches_per_step_launches(dev, monkeypatch, nx, ny, batch, nsteps, nseg):
-    """PW_MARCH_PERSIST=1: all steps in one launch with per-segment step counters.  Each
-    row is computed by the same arithmetic whatever CTA computes it, so the result is
-    bitwise equal to the per-step launches."""
+    """Previous-generation kernels (PW_MARCH_V2=0): the cp.async persistent march
+    (PW_MARCH_PERSIST=1) against its per-step launches.  Each row is computed by the same
+    arithmetic whatever CTA computes it, so the result is bitwise equal."""
     from paper_1510_02237_b200.integrators import SlicePropagator
 
+    monkeypatch.setenv("PW_MARCH_V2", "0")
     prop = SlicePropagator(fine_spec(nx, ny), nsteps=nsteps)
     x = torch.as_tensor(random_states(nx, ny, batch, 31 + nx)).cuda()
     monkeypatch.setenv("PW_MARCH_PERSIST", "0")  # the per-step launches (the default at 128/256 is persistent)
@@ -153,3 +155,37 @@ def test_persistent_march_matches_per_step_launches(dev, monkeypatch, nx, ny, ba
     got = prop.apply(x)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("nx,ny,batch,nsteps,nseg", [
+    (256, 256, 64, 10, 0),   # c2 shape, default segments
+    (256, 256, 64, 7, 4),
+    (512, 96, 6, 4, 3),
+    (128, 64, 5, 3, 1),      # one segment: each item waits on itself only
+    (384, 48, 3, 2, 2),
+    (256, 100, 4, 5, 6),     # ragged segments (16-row minimum)
+])
+def test_tma_march_all_steps_vs_one_step_launches(dev, monkeypatch, nx, ny, batch, nsteps, nseg):
+    """K1 (march_tma.cu) runs all steps of a propagation in one persistent launch.  Against
+    nsteps launches of one step each: the same rows from the same arithmetic, so the
+    result is bitwise equal -- and against the previous-generation per-step kernel
+    (PW_MARCH_V2=0, different operation order) to rounding."""
+    from paper_1510_02237_b200.integrators import SlicePropagator
+
+    spec = fine_spec(nx, ny)
+    x = torch.as_tensor(random_states(nx, ny, batch, 77 + nx + ny)).cuda()
+    if nseg:
+        monkeypatch.setenv("PW_MARCH_NSEG", str(nseg))
+    got = SlicePropagator(spec, nsteps=nsteps).apply(x)
+    one = SlicePropagator(spec, nsteps=1)
+    want = x
+    for _ in range(nsteps):
+        want = one.apply(want)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    monkeypatch.setenv("PW_MARCH_V2", "0")
+    monkeypatch.setenv("PW_MARCH_PERSIST", "0")
+    monkeypatch.delenv("PW_MARCH_NSEG", raising=False)
+    old = SlicePropagator(spec, nsteps=nsteps).apply(x)
+    err = ((got - old).norm(dim=1) / old.norm(dim=1)).max().item()
+    assert err <= 1e-13, err
