@@ -612,6 +612,266 @@ __global__ void __launch_bounds__(NT, MINB) fefb_tb_coop(double* st, int batch, 
   }
 }
 
+// ---------------------------------------------------------------- neighbour-flag G
+// One FE-FB propagation (split_fe_fb_step x nsteps, integrators.py:103-106 with
+// fb_substeps, numba_backend.py:131-146) of ONE state as a persistent cooperative launch
+// without grid barriers.  The state is cut into 32 x TY tiles; per step a tile runs phase A
+// (its cells' frozen advective tendencies) and ceil(nsub / K) substep blocks, each block K
+// substeps on its tile plus a 3K-cell halo in shared memory (temporal blocking).  Before a
+// phase a tile waits only until its 8 neighbour tiles have finished the previous phase
+// (per-tile phase counters, release / acquire): that orders both the halo it reads (RAW)
+// and the buffer it overwrites, which those neighbours read in the previous phase (WAR).
+// A CTA walks its tiles phase by phase, so every wait points at a lower phase: no deadlock.
+//
+// Same expressions as fb_cell (bitwise equal to the reference; -fmad=false), restructured:
+// the divergence D = dx(u) + dy(v) that both damping terms difference is computed once per
+// cell and substep (the reference's own damping_tendencies form), each thread owns one
+// column of cells of the region (compile-time strip), its cells' tendencies stay in
+// registers for the whole block, and staging loads bypass L1 (ld.global.cg).
+template <int TMY, int K, int NT>
+struct NfCfg {
+  // x halo rounded up to even (HX): staged rows start 16-byte aligned (cp.async of pairs)
+  static constexpr int TX = 32, H = 3 * K, HX = (H + 1) / 2 * 2, RX = TX + 2 * HX, RYM = TMY + 2 * H;
+  static constexpr int NSTR = NT / RX;                // column strips of the region
+  static constexpr int S = (RYM + NSTR - 1) / NSTR;   // cells per thread (one column)
+  // plane: NSTR * S rows (>= RYM) plus a padding row above and below (branch-free passes)
+  static constexpr int PL = RX * (NSTR * S + 2);
+  static constexpr size_t SMEM = sizeof(double) * 6 * PL;
+  static_assert(NSTR >= 1, "the region must be at most NT columns wide");
+};
+
+__device__ __forceinline__ int nf_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void nf_st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// wait until the 8 neighbours of tile (ix, iy) have completed phase `ph`
+__device__ __forceinline__ void nf_wait(const int* flags, int ix, int iy, int tiles_x, int tiles_y, int ph) {
+  if (ph > 0 && threadIdx.x < 9 && threadIdx.x != 4) {
+    int jx = ix + (int)threadIdx.x % 3 - 1, jy = iy + (int)threadIdx.x / 3 - 1;
+    jx += jx < 0 ? tiles_x : 0;
+    jx -= jx >= tiles_x ? tiles_x : 0;
+    jy += jy < 0 ? tiles_y : 0;
+    jy -= jy >= tiles_y ? tiles_y : 0;
+    const int* f = flags + jy * tiles_x + jx;
+    long long spins = 0;
+    while (nf_ld_acquire(f) < ph) {
+      __nanosleep(32);
+      if (++spins > (1LL << 26)) __trap();  // a broken dependency fails, never hangs
+    }
+  }
+  __syncthreads();
+}
+// the CTA barrier orders every thread's stores before thread 0's fence (cumulative) and
+// release, as cooperative groups' grid barrier does
+__device__ __forceinline__ void nf_signal(int* flags, int tile, int ph) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    nf_st_release(flags + tile, ph);
+  }
+}
+
+template <int TMY, int K, int NT, int ORD>
+__global__ void __launch_bounds__(NT, 1) fefb_nf_kernel(double* st, ExactParams p, int nsteps, double tau,
+                                                       int nsub, double* work, int tiles_x, int tiles_y,
+                                                       int* flags) {
+  using C = NfCfg<TMY, K, NT>;
+  constexpr int TX = C::TX, H = C::H, HX = C::HX, RX = C::RX, PL = C::PL, S = C::S;
+  extern __shared__ double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const long long n = (long long)nx * ny;
+  const double sx = 0.5 / p.dx, sy = 0.5 / p.dy, cs = p.cs, a1 = p.a1, a2 = p.a2;
+  const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
+  double* au = work;
+  double* av = work + n;
+  double* ap = work + 2 * n;
+  double* ws = work + 3 * n;  // ping-pong state (u, v, p planes)
+  const int tiles = tiles_x * tiles_y;
+  const int tid = threadIdx.x;
+  const int cx = tid % RX, strip = tid / RX;  // this thread's column and strip of the region
+  const bool comp = strip < C::NSTR;
+  const int y0s = strip * S;
+  const int nblk = (nsub + K - 1) / K;
+  int ph = 0;
+  for (int step = 0; step < nsteps; ++step) {
+    // ---- phase A: frozen advective tendency of the tile's cells (physics.py:67-74)
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int iy = t / tiles_x, ix = t - iy * tiles_x;
+      const int ty0 = (int)((long long)iy * ny / tiles_y), ty1 = (int)((long long)(iy + 1) * ny / tiles_y);
+      nf_wait(flags, ix, iy, tiles_x, tiles_y, ph);
+      for (int c = tid; c < TX * (ty1 - ty0); c += NT) {
+        const int j = ty0 + c / TX, i = ix * TX + c % TX;
+        const long long cell = (long long)j * nx + i;
+        au[cell] = adv_at<ORD>(p, st, j, i);
+        av[cell] = adv_at<ORD>(p, st + n, j, i);
+        ap[cell] = adv_at<ORD>(p, st + 2 * n, j, i);
+      }
+      nf_signal(flags, t, ph + 1);
+    }
+    ++ph;
+    // ---- substep blocks
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int ks = min(K, nsub - blk * K);
+      const double* src = (blk % 2 == 0) ? st : ws;
+      double* dst = (blk % 2 == 0) ? ws : st;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int tx0 = ix * TX;
+        const int ty0 = (int)((long long)iy * ny / tiles_y);
+        const int TY = (int)((long long)(iy + 1) * ny / tiles_y) - ty0;
+        const int RY = TY + 2 * H;
+        nf_wait(flags, ix, iy, tiles_x, tiles_y, ph);
+        double* su = sm + RX;  // row 0 of the region (one padding row above)
+        double* sv = su + PL;
+        double* sp = sv + PL;
+        double* sd = sp + PL;
+        double* sun = sd + PL;
+        double* svn = sun + PL;
+        // stage (u, v, p) of the region [tx0 - HX, tx0 + TX + HX) x [ty0 - H, ty0 + TY + H):
+        // 16-byte cp.async.cg (L2 only) of column pairs, all in flight before one wait
+        for (int c = tid; c < (RX / 2) * RY; c += NT) {
+          const int y = c / (RX / 2), x = 2 * (c - y * (RX / 2));
+          int gx = tx0 - HX + x, gy = ty0 - H + y;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          gy += gy < 0 ? ny : 0;
+          gy -= gy >= ny ? ny : 0;
+          const long long cell = (long long)gy * nx + gx;
+          const int o = y * RX + x;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(su + f * PL + o);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + f * n + cell) : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // this thread's cells' tendencies (registers for the whole block)
+        double tu[S], tv[S], tp[S];
+        if (comp) {
+          int gx = tx0 - HX + cx;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          int gy = ty0 - H + y0s;
+          gy += gy < 0 ? ny : 0;
+          gy -= gy >= ny ? ny : 0;
+          const double* qa = au + (long long)gy * nx + gx;
+#pragma unroll
+          for (int r = 0; r < S; ++r) {
+            tu[r] = __ldcg(qa);
+            tv[r] = __ldcg(qa + n);
+            tp[r] = __ldcg(qa + 2 * n);
+            // next row, wrapping at the bottom edge (rows past the region: any valid row)
+            qa += (++gy < ny) ? nx : -(long long)(ny - 1) * nx;
+            if (gy >= ny) gy = 0;
+          }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        // Each pass computes all S cells of the thread's column branch-free (independent
+        // rows: full ILP), then stores the rows inside the pass's margin.  Rows outside it
+        // carry garbage that no valid cell ever reads (the margins shrink by the stencil
+        // radius); planes have a padding row above and below, so no access leaves them.
+        for (int ss = 0; ss < ks; ++ss) {
+          const int M = H - 3 * ss;  // (u, v, p) valid on margin M of the tile
+          // D = dx(u) + dy(v) on margin M - 1 (damping_tendencies' div, numba_backend.py:108-111)
+          if (damp && comp && cx >= HX - (M - 1) && cx < HX + TX + (M - 1) &&
+              y0s + S > H - (M - 1) && y0s < H + TY + (M - 1)) {
+            double dd[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = (y0s + r) * RX + cx;
+              dd[r] = (su[o + 1] - su[o - 1]) * sx + (sv[o + RX] - sv[o - RX]) * sy;
+            }
+            const int lo = H - (M - 1) - y0s, hi = H + TY + (M - 1) - y0s;
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+              if (r >= lo && r < hi) sd[(y0s + r) * RX + cx] = dd[r];
+          }
+          __syncthreads();
+          // u', v' on margin M - 2 (fb_substeps, numba_backend.py:137-143)
+          if (comp && cx >= HX - (M - 2) && cx < HX + TX + (M - 2) &&
+              y0s + S > H - (M - 2) && y0s < H + TY + (M - 2)) {
+            double nu_[S], nv_[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = (y0s + r) * RX + cx;
+              double du = tu[r] - cs * ((sp[o + 1] - sp[o - 1]) * sx);
+              double dv = tv[r] - cs * ((sp[o + RX] - sp[o - RX]) * sy);
+              if (damp) {
+                du = du + a1 * ((sd[o + 1] - sd[o - 1]) * sx);
+                dv = dv + a2 * ((sd[o + RX] - sd[o - RX]) * sy);
+              }
+              nu_[r] = su[o] + tau * du;
+              nv_[r] = sv[o] + tau * dv;
+            }
+            const int lo = H - (M - 2) - y0s, hi = H + TY + (M - 2) - y0s;
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+              if (r >= lo && r < hi) {
+                sun[(y0s + r) * RX + cx] = nu_[r];
+                svn[(y0s + r) * RX + cx] = nv_[r];
+              }
+          }
+          __syncthreads();
+          // p' on margin M - 3 from the new velocities (numba_backend.py:144-145)
+          if (comp && cx >= HX - (M - 3) && cx < HX + TX + (M - 3) &&
+              y0s + S > H - (M - 3) && y0s < H + TY + (M - 3)) {
+            double np_[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = (y0s + r) * RX + cx;
+              const double divn = (sun[o + 1] - sun[o - 1]) * sx + (svn[o + RX] - svn[o - RX]) * sy;
+              np_[r] = sp[o] + tau * (tp[r] - cs * divn);
+            }
+            const int lo = H - (M - 3) - y0s, hi = H + TY + (M - 3) - y0s;
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+              if (r >= lo && r < hi) sp[(y0s + r) * RX + cx] = np_[r];
+          }
+          __syncthreads();
+          double* tt = su;
+          su = sun;
+          sun = tt;
+          tt = sv;
+          sv = svn;
+          svn = tt;
+        }
+        // the tile's new (u, v, p)
+        for (int c = tid; c < TX * TY; c += NT) {
+          const int ly = c / TX, lx = c - ly * TX;
+          const int o = (ly + H) * RX + lx + HX;
+          const long long cell = (long long)(ty0 + ly) * nx + tx0 + lx;
+          dst[cell] = su[o];
+          dst[n + cell] = sv[o];
+          dst[2 * n + cell] = sp[o];
+        }
+        nf_signal(flags, t, ph + 1);
+      }
+      ++ph;
+    }
+    if (nblk % 2 == 1) {  // the last block wrote ws: copy the tiles back (WAR on st: a phase)
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int ty0 = (int)((long long)iy * ny / tiles_y), ty1 = (int)((long long)(iy + 1) * ny / tiles_y);
+        nf_wait(flags, ix, iy, tiles_x, tiles_y, ph);
+        for (int c = tid; c < TX * (ty1 - ty0); c += NT) {
+          const long long cell = (long long)(ty0 + c / TX) * nx + ix * TX + c % TX;
+          st[cell] = ws[cell];
+          st[n + cell] = ws[n + cell];
+          st[2 * n + cell] = ws[2 * n + cell];
+        }
+        nf_signal(flags, t, ph + 1);
+      }
+      ++ph;
+    }
+  }
+}
+
 template <int TMX, int TMY, int K>
 constexpr size_t tb_smem() {
   return sizeof(double) * 5 * (TMX + 6 * K) * (TMY + 6 * K);
@@ -632,7 +892,8 @@ size_t rk3_exact_work_doubles(const ExactParams& p, int batch) {
 }
 
 size_t fefb_exact_work_doubles(const ExactParams& p, int batch) {
-  return (size_t)6 * p.nx * p.ny * (size_t)batch;
+  // + the neighbour-flag kernel's per-tile phase counters (<= nx/32 x ny/8 ints)
+  return (size_t)6 * p.nx * p.ny * (size_t)batch + (size_t)p.nx * p.ny / 512 + 64;
 }
 
 void launch_rk3_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
@@ -703,10 +964,57 @@ static int coarse_variant() {
   return v;
 }
 
+// Neighbour-flag G for one state (serial sweep): tiles of 32 x <= TMY rows, as many tile
+// rows as fill the resident CTA slots (near-equal heights); the flags follow the 6 n work
+// doubles (fefb_exact_work_doubles reserves them).  Returns false when the grid does not fit.
+template <int TMY, int K, int NT, int ORD>
+static bool launch_nf(Ctx& c, const ExactParams& p, double* states, int nsteps, double h, int nsub, double* work) {
+  using C = NfCfg<TMY, K, NT>;
+  auto kern = fefb_nf_kernel<TMY, K, NT, ORD>;
+  const int per_sm = kernel_setup(c, kern, NT, C::SMEM);
+  const int tiles_x = p.nx / 32;
+  const int slots = c.num_sms * per_sm;
+  int tiles_y = (p.ny + TMY - 1) / TMY;                        // smallest count with TY <= TMY
+  const int fill = std::max(1, slots / std::max(1, tiles_x));  // one tile per CTA when it fits
+  if (tiles_x * tiles_y < slots) tiles_y = std::max(tiles_y, std::min(p.ny / (3 * K), fill));
+  if (p.ny / tiles_y < 3 * K || tiles_x * 32 != p.nx) return false;  // halo must stay in the 8 neighbours
+  if (((uintptr_t)states | (uintptr_t)work) & 15) return false;      // 16-byte staging copies
+  const int tiles = tiles_x * tiles_y;
+  const int grid = std::min(tiles, slots);
+  int* flags = reinterpret_cast<int*>(work + 6 * (size_t)p.nx * p.ny);
+  PW_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)tiles, c.stream));
+  double tau = h / nsub;
+  ExactParams pp = p;
+  int tx = tiles_x, ty = tiles_y;
+  void* args[] = {&states, &pp, &nsteps, &tau, &nsub, &work, &tx, &ty, &flags};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, C::SMEM, c.stream));
+  c.launches += 1;
+  return true;
+}
+
+static int nf_variant() {
+  const char* e = getenv("PW_COARSE_NF");  // 0: the grid-barrier kernels; 2 / 3 / 4: substeps per phase
+  return (e && *e) ? atoi(e) : 3;
+}
+
 void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,
                        int nsteps, double h, int nsub, double* work) {
   if (nsteps <= 0 || batch <= 0) return;
   PW_CHECK((long long)p.nx * p.ny < (1LL << 31), PW_ERR_VALUE, "grid too large");
+  if (!c.strict && batch == 1 && ld >= 3LL * p.nx * p.ny && p.nx % 32 == 0 && p.ny >= 64 &&
+      (long long)p.nx * p.ny >= 16384 && nf_variant() > 0) {
+    const bool o1 = p.order == 1;
+    bool ok = false;
+    switch (nf_variant()) {
+      case 2: ok = o1 ? launch_nf<64, 2, 512, 1>(c, p, states, nsteps, h, nsub, work)
+                      : launch_nf<64, 2, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
+      case 4: ok = o1 ? launch_nf<56, 4, 512, 1>(c, p, states, nsteps, h, nsub, work)
+                      : launch_nf<56, 4, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
+      default: ok = o1 ? launch_nf<60, 3, 512, 1>(c, p, states, nsteps, h, nsub, work)
+                       : launch_nf<60, 3, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
+    }
+    if (ok) return;
+  }
   if (!c.strict && p.nx % 32 == 0 && p.ny % 32 == 0 && (long long)p.nx * p.ny >= 65536) {
     const bool o1 = p.order == 1;
     switch (coarse_variant()) {
