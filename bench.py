@@ -41,9 +41,10 @@ N_GRID = 256
 BATCH = 64
 STEPS_PER_SAMPLE = 200
 BYTES_PER_CELL_UPDATE = 48  # read (u,v,p) + write (u,v,p), fp64
-# fp64 flops of the folded constant-velocity RK3 form per cell-update (FMA = 2 flop, halo
-# recompute excluded): stage 1 = 65, stages 2 and 3 = 68 (+ the q base)
-FLOP_PER_CELL_UPDATE = 201
+# fp64 flops of the folded constant-velocity RK3 form per cell-update as K1 (march_tma.cu)
+# evaluates it (FMA = 2 flop, halo recompute excluded; K1): stage 1 = 63 (no q
+# base), stages 2 and 3 = 66
+FLOP_PER_CELL_UPDATE = 195
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "fine_traffic.json")
 C2_WORKLOAD = ("c2: 64 states x 256^2 periodic x 200 RK3 steps (CFL 0.5, order 6, nu 0.005, cs=1, U=0.1), "
                "seeded random-mode fields")
@@ -77,14 +78,21 @@ def c3_reference_window():
             "source": "DESIGN.md section 5 (reference kse_sweep, survey container, numba, 8 workers)"}
 
 
+def k1_generation():
+    """Which fine kernel the library runs at c2: K1 = the TMA-fed persistent march
+    (march_tma.cu, default), or the previous cp.async kernels (PW_MARCH_V2=0)."""
+    return "tma" if os.environ.get("PW_MARCH_V2", "1") != "0" else "cpasync"
+
+
 def load_traffic(persistent=False):
-    """DRAM bytes per fine-kernel launch at c2 from the committed ncu captures: the
-    per-step rk3_march_kernel, or (persistent) rk3_march_persist_kernel over 200 steps."""
+    """DRAM bytes per fine-kernel launch at c2 from the committed ncu captures: K1
+    (rk3_mtma_kernel, all 200 steps in one launch), or the previous generation's per-step
+    rk3_march_kernel / persistent rk3_march_persist_kernel."""
     if os.path.exists(TRAFFIC_FILE):
         with open(TRAFFIC_FILE) as fh:
             d = json.load(fh)
         if persistent:
-            d = d.get("persistent")
+            d = d.get("persistent_tma" if k1_generation() == "tma" else "persistent")
             if not d:
                 return None, None
         return float(d["dram_bytes_per_launch"]), d.get("source")
@@ -520,8 +528,10 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "avg_launch_us": launch_s * 1e6,
-                         "kernel": ("rk3_march_persist_kernel (row-marching fused RK3; one persistent launch runs "
-                                    "all 200 RK3 steps of the 64 states)" if persistent else
+                         "kernel": (("rk3_mtma_kernel (K1: TMA-fed persistent row march, march_tma.cu; one "
+                                     "launch runs all 200 RK3 steps of the 64 states)" if k1_generation() == "tma" else
+                                     "rk3_march_persist_kernel (previous generation: cp.async row march; one persistent "
+                                     "launch runs all 200 RK3 steps of the 64 states)") if persistent else
                                     "rk3_march_kernel (row-marching fused RK3; one launch per RK3 step over all 64 states)"),
                          "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": (fp64_achieved / fp64_peak) if fp64_peak else None,

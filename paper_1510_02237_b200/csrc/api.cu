@@ -226,16 +226,21 @@ bool prop_apply_impl(pw_prop* P, const double* in, double* out, int batch, long 
       ld_src = d;
     }
     double* tmp = P->t2.ensure(c, (size_t)d * batch);
-    if (npeer == 0 && !P->vadv && pw::mtma_enabled() &&
+    bool peers_ok = true;  // the epilogue's 16-byte peer stores need 16-byte buffers
+    for (int i = 0; i < npeer; ++i) peers_ok &= ((uintptr_t)peers[i] & 15) == 0;
+    if (peers_ok && !P->vadv && pw::mtma_enabled() &&
         pw::mtma_supported(P->fp.nx, P->fp.ny, ld_src, ld, src, out, tmp)) {
-      // K1: TMA-fed persistent row march over all nsteps (march_tma.cu)
+      // K1: TMA-fed persistent row march over all nsteps (march_tma.cu); with peers, the
+      // last step's rows also go straight into every peer's buffer (fused all-gather)
       int* sync = reinterpret_cast<int*>(
           P->sync.ensure(c, (pw::march_persist_sync_ints(P->fp.ny, batch) + 1) / 2));
       pw::FusedParams fp = P->fp;
       fp.ld_in = ld_src;
       fp.ld_out = ld;
+      fp.npeer = npeer;
+      for (int i = 0; i < npeer; ++i) fp.peer_delta[i] = (long long)((uintptr_t)peers[i] - (uintptr_t)out);
       pw::launch_rk3_mtma(c, fp, src, out, tmp, batch, nsteps, d, sync);
-      return false;
+      return npeer > 0;
     }
     if (npeer == 0 && nsteps >= 2 && !P->vadv && pw::march_persist_enabled(P->fp.nx) &&
         pw::march_supported(P->fp.nx, P->fp.ny, ld_src, ld, src, out) &&

@@ -125,7 +125,24 @@ struct Sink {
   double* g;        // S = 2: this thread's columns of the segment's first row (u field)
   long long n;      // nx * ny (field stride)
   int TY;
+  int npeer;        // last RK3 step of a fused all-gather: also store into npeer peer buffers
+  const long long* peer_delta;  // (bytes from out, FusedParams::peer_delta), else npeer = 0
 };
+
+// stage 3's 4 cells of one output row: HBM, and (PEERS: fused slice all-gather,
+// pw_prop_apply_to_peers) the same bytes into each peer's buffer over NVLink, from the
+// registers that hold them.  A separate instantiation: the peer loop in the plain kernel
+// cost 11 % (64.6 vs 72.4 G/s at c2).
+template <bool PEERS>
+__device__ __forceinline__ void st_out(const Sink& o, double* p, const double (&v)[4]) {
+  stg4(p, v);
+  if constexpr (PEERS)
+  for (int i = 0; i < o.npeer; ++i) {
+    double* q = reinterpret_cast<double*>(reinterpret_cast<char*>(p) + o.peer_delta[i]);
+    __stcg(reinterpret_cast<double2*>(q), make_double2(v[0], v[1]));
+    __stcg(reinterpret_cast<double2*>(q + 2), make_double2(v[2], v[3]));
+  }
+}
 
 __device__ __forceinline__ double2 lds2(const double* p) {
   double2 v;
@@ -163,7 +180,7 @@ __device__ __forceinline__ void xstencil(double (&acc)[4], double (&d1)[4], cons
 
 // Consume input row k (ring slot `in`; q row k+1 at `qb` for the births when S > 0), store
 // the completed rows: u, p of row k-1 and v of row k-2.  PH = k mod 3 (compile time).
-template <int NX, int S, int PH>
+template <int NX, int S, int PH, bool PEERS>
 __device__ __forceinline__ void row_step(Acc& A, const double* in, const double* qb, const int* woff,
                                          const StageCoef& C, const Sink& o, int k) {
   constexpr int U0 = (PH + 2) % 3, U1 = PH, U2 = (PH + 1) % 3;  // u, p: rows k-1, k, k+1
@@ -178,7 +195,7 @@ __device__ __forceinline__ void row_step(Acc& A, const double* in, const double*
   if constexpr (S < 2) {
     st4(o.ring + ((PH + 1) % 3) * (3 * NX) + NX, woff + 2, A.v[V0]);
   } else {
-    if (k - 2 >= 0 && k - 2 < o.TY) stg4(o.g + o.n + (long long)(k - 2) * NX, A.v[V0]);
+    if (k - 2 >= 0 && k - 2 < o.TY) st_out<PEERS>(o, o.g + o.n + (long long)(k - 2) * NX, A.v[V0]);
   }
   {
     double b[4];
@@ -211,8 +228,8 @@ __device__ __forceinline__ void row_step(Acc& A, const double* in, const double*
   } else {
     if (k - 1 >= 0 && k - 1 < o.TY) {
       double* g = o.g + (long long)(k - 1) * NX;
-      stg4(g, A.u[U0]);
-      stg4(g + 2 * o.n, A.p[U0]);
+      st_out<PEERS>(o, g, A.u[U0]);
+      st_out<PEERS>(o, g + 2 * o.n, A.p[U0]);
     }
   }
   // ---- u row k: x stencil (advection + the symmetric x damping at +-2 and the centre);
@@ -257,7 +274,7 @@ __device__ __forceinline__ void issue(double* ring, uint64_t* full, const Item& 
 }
 
 // One tick: the CTA barrier, the q row two ticks ahead, then stage S's row k = t - lag.
-template <class K, int I>
+template <class K, int I, bool PEERS>
 __device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const Item& it, const FusedParams& P,
                                      int S, int t, const int* woff, const Sink& o, bool producer) {
   constexpr int NX = K::NX;
@@ -272,21 +289,21 @@ __device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const
     if (k > it.TY + 5) return;
     const uint32_t s = qslot(it.seq, k);
     mbar_wait(full + s, qpar(it.seq, k));
-    row_step<NX, 0, I>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k);
+    row_step<NX, 0, I, PEERS>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k);
   } else if (S == 1) {
     const int k = t - 9;
     if (k < -4 || k > it.TY + 3) return;
     const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
-    row_step<NX, 1, I>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k);
+    row_step<NX, 1, I, PEERS>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k);
   } else {
     const int k = t - 12;
     if (k < -2 || k > it.TY + 1) return;
     const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
-    row_step<NX, 2, I>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k);
+    row_step<NX, 2, I, PEERS>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k);
   }
 }
 
-template <class K>
+template <class K, bool PEERS>
 __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
     const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_out,
     const __grid_constant__ CUtensorMap map_tmp, double* out, double* tmp, long long ld_out, long long ld_tmp,
@@ -357,6 +374,10 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
     o.ring = ring_out;
     o.n = n;
     o.TY = it.TY;
+    if constexpr (PEERS) {
+      o.npeer = (s == nsteps - 1) ? P.npeer : 0;  // peers get the final state only
+      o.peer_delta = P.peer_delta;
+    }
     o.g = (to_out ? out + (long long)b * ld_out : tmp + (long long)b * ld_tmp) + (long long)it.y0 * NX + 4 * g;
     if (producer) {  // prologue: q rows -6 and -5 (stage 1's ticks 0 and 1)
       issue<K>(ring, full, it, ny, -6);
@@ -372,9 +393,9 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
     // tick count rounded up to the unroll (equal barrier counts for every warp)
     const int nt = (it.TY + 14 + 2) / 3 * 3;
     for (int t = 0; t < nt; t += 3) {
-      tick<K, 0>(A, ring, full, it, P, S, t, woff, o, producer);
-      tick<K, 1>(A, ring, full, it, P, S, t + 1, woff, o, producer);
-      tick<K, 2>(A, ring, full, it, P, S, t + 2, woff, o, producer);
+      tick<K, 0, PEERS>(A, ring, full, it, P, S, t, woff, o, producer);
+      tick<K, 1, PEERS>(A, ring, full, it, P, S, t + 1, woff, o, producer);
+      tick<K, 2, PEERS>(A, ring, full, it, P, S, t + 2, woff, o, producer);
     }
     seq += (uint32_t)(it.TY + 12);
     asm volatile("fence.proxy.async.global;" ::: "memory");  // stores before later TMA reads
@@ -423,7 +444,7 @@ CUtensorMap row_map(const double* base, int nx, int ny, long long ld, int batch)
 template <class K>
 void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp, int batch, int nsteps,
                 long long d, int* sync) {
-  auto kern = rk3_mtma_kernel<K>;
+  auto kern = fp.npeer > 0 ? rk3_mtma_kernel<K, true> : rk3_mtma_kernel<K, false>;
   const int per_sm = kernel_setup(c, kern, K::NT, K::SMEM);
   const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
   // segments per state: ticks per item (TY + 14) x max(1, items / CTA slots), clamped so

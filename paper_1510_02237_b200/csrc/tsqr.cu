@@ -7,9 +7,12 @@
 // the diagonal, tau), so the compact-WY machinery around it (larft, Q1^T N, Q = Q1 Q2)
 // is unchanged.  The panel is factored in sub-panels of TB = 32 columns; each one:
 //
-//   1. TSQR (tsqr_qr_kernel): leaves of TL = 128 rows, one CTA each, Householder QR in
-//      shared memory (reflectors stored back in place, the leaf R to a buffer); then a
-//      4-ary tree over the stacked R factors (same kernel, one launch per level).
+//   1. TSQR (tsqr_qr_kernel): leaves of 128 rows (4 warps), one CTA each, Householder QR
+//      in shared memory (reflectors stored back in place, the leaf R to a buffer); then an
+//      8-ary tree over the stacked R factors (8-warp nodes, one launch per level).  Per
+//      column one CTA barrier: the column is broadcast inside each warp, only the per-warp
+//      partial dot products cross warps (the previous layout published each column through
+//      shared memory with two barriers: ~100 us per tree node, latency-bound).
 //      One read of the sub-panel.
 //   2. Explicit Q (tsqr_expand_kernel): top-down, Q_node [C; 0] for each node, C being
 //      the parent's output block; at the leaves that is the sub-panel's Q, written in
@@ -30,9 +33,18 @@
 namespace pw {
 namespace {
 
-constexpr int TB = 32;   // sub-panel width (columns)
-constexpr int TL = 128;  // rows per TSQR leaf / tree node (4 child R's of <= 32 rows)
-constexpr int TTH = 128; // threads per block (4 warps)
+constexpr int TB = 32;    // sub-panel width (columns)
+constexpr int NWL = 4;    // leaf blocks: 4 warps, 128 rows
+constexpr int NWN = 8;    // tree nodes: 8 warps, fan-in 8 (8 stacked child R's of <= 32 rows; 16 warps would spill)
+constexpr int TLN = 32 * NWN;
+
+template <int NW>
+struct Blk {
+  static constexpr int TL = 32 * NW;     // rows per block
+  static constexpr int LD = TL + 1;      // shared row stride (odd: lane = column is conflict free)
+  static constexpr int NT = 32 * NW;     // threads (one block row each in the load / store phases)
+  static constexpr size_t SMEM = sizeof(double) * TB * LD;
+};
 
 struct TsqrArgs {
   double* panel;        // sub-panel (rows x b, column-major, ld lda)
@@ -41,88 +53,133 @@ struct TsqrArgs {
   int b;
   int nin;              // node levels: R factors at the level below
   const double* rin;    // node levels: those R factors (b x b each, ld b)
-  double* vnode;        // node levels: reflectors [node][TB * TL] (column-major, ld TL)
-  double* tau;          // [node][TB]  (unused by the kernels: T carries tau on its diagonal)
+  double* vnode;        // node levels: reflectors [node][TB * TLN] (column-major, ld TLN)
   double* tnode;        // [node][TB * TB] compact-WY T of every block (b x b, ld b)
   double* rout;         // [node][b * b] R factors of this level
-  const double* cin;    // expand: the parent level's output blocks [node][TB * TL], or null (root: C = I)
-  double* xout;         // expand, node levels: this level's output blocks [node][TB * TL]
+  const double* cin;    // expand: the parent level's output blocks [node][TB * TLN], or null (root: C = I)
+  double* xout;         // expand, node levels: this level's output blocks [node][TB * TLN]
+  unsigned long long* prof;  // PW_TSQR_PROF=1: block 0's phase timestamps (globaltimer ns), else null
 };
 
-constexpr int LD = TL + 1;  // shared row stride of a TL x TB block (odd: lane = column is conflict free)
+__device__ __forceinline__ void prof_mark(unsigned long long* prof, int k) {
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    prof[k] = t;
+  }
+}
 
 // Thread layout of every block kernel here: lane = column c (0..31), warp = row chunk q
-// (rows 32q .. 32q+31 of the 128-row block).  A column's dot product is four per-warp
-// partials summed through shared memory -- no shuffle reductions on the critical path.
+// (rows 32q .. 32q+31 of the block).  A column's dot product is NW per-warp partials summed
+// through shared memory in a fixed pairwise order (deterministic).
+template <int NW>
+__device__ __forceinline__ double sum_parts(const double* p) {
+  double s[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) s[w] = p[w];
+#pragma unroll
+  for (int h = 1; h < NW; h *= 2)
+#pragma unroll
+    for (int w = 0; w + h < NW; w += 2 * h) s[w] = s[w] + s[w + h];
+  return s[0];
+}
 
 // Householder QR (LAPACK dlarfg convention) of X (TL x b, column-major, ld LD) in shared
 // memory.  Thread (c, q) keeps its 32 entries of column c in registers for the whole
-// factorisation; per column j the owner threads (j, q) publish column j through a
-// shared buffer (read back as broadcasts), so the shared-memory traffic per step is one
-// column instead of the whole block.  Column j stays unscaled while later columns are
-// updated (v_r = x_r * scale[j]); one barrier pair per column: partial dots x_j . x_c
-// for every c >= j (which include ||x_j||), then every thread derives beta, tau, scale
-// and its column's w itself.  The j loop is unrolled so register indices stay static.
-__device__ void block_house_qr(double* X, double* tau, double* scale, double (*part)[TB][4], double (*xb)[TL],
-                               double* xcj_s, int b) {
+// factorisation.  Per column j: lane j of each warp publishes its chunk of column j to a
+// per-warp buffer that the warp reads back as broadcasts, every thread forms its partial
+// x_j . x_c, ONE barrier,
+// then every thread derives beta, tau, scale and its column's w from the summed partials
+// and updates its chunk.  Partials and the row-j entries are double-buffered by j & 1, so
+// one barrier per column suffices.  Column j stays unscaled while later columns are
+// updated (v_r = x_r * scale[j]).  The j loop is unrolled so register indices stay static.
+template <int NW>
+__device__ void block_house_qr(double* X, double* tau, double* scale, double (*part)[TB][NW],
+                               double (*rowj)[TB], double (*xcol)[32], int b) {
+  constexpr int LD = Blk<NW>::LD;
   const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
   double x[32];
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) x[rr] = X[c * LD + q * 32 + rr];
-  if (c == 0) {
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) xb[0][q * 32 + rr] = x[rr];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < TB; ++j) {
-    if (j >= b) break;
-    double (*pd)[4] = part[j & 1];
-    const double* xjs = xb[j & 1];
+#pragma unroll 1
+  for (int j = 0; j < b; ++j) {
+    // column j's chunk: lane j stores it (16-byte stores), the warp reads it back as
+    // broadcasts -- 32 shared-memory instructions instead of 64 32-bit shuffles
     double xj[32];
+    double2* xc = reinterpret_cast<double2*>(xcol[q]);
+    if (c == j) {
 #pragma unroll
-    for (int rr = 0; rr < 32; ++rr) xj[rr] = xjs[q * 32 + rr];
-    const double alpha = xjs[j];
-    double acc = 0.0;
-    if (c >= j && c < b) {
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < 16; ++k) xc[k] = make_double2(x[2 * k], x[2 * k + 1]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double2 t2 = xc[k];
+      xj[2 * k] = t2.x;
+      xj[2 * k + 1] = t2.y;
+    }
+    // every lane computes (lanes of finished or absent columns produce values nobody reads):
+    // rows > j only -- in chunk 0 a compile-time mask (j, rr unrolled), the other chunks are
+    // all below row 31 (a warp-uniform branch, no per-element selects)
+    // 8 accumulator chains of 4 (latency: the column loop is a serial chain of these steps)
+    double a8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (q == 0) {
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr)
-        if (q > 0 || rr > j) a4[rr & 3] = fma(xj[rr], x[rr], a4[rr & 3]);
-      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        if (rr > j) a8[rr & 7] = fma(xj[rr], x[rr], a8[rr & 7]);
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) a8[rr & 7] = fma(xj[rr], x[rr], a8[rr & 7]);
     }
-    pd[c][q] = acc;
-    if (q == 0) xcj_s[c] = x[j];
+    part[j & 1][c][q] = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+    if (q == 0) {  // row j of every column (alpha = column j's): x[j], j not compile-time --
+      double s16[16], s8[8], s4[4], s2[2];  // a 5-level select tree on j's bits
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s16[k] = (j & 16) ? x[k + 16] : x[k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s8[k] = (j & 8) ? s16[k + 8] : s16[k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s4[k] = (j & 4) ? s8[k + 4] : s8[k];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) s2[k] = (j & 2) ? s4[k + 2] : s4[k];
+      rowj[j & 1][c] = (j & 1) ? s2[1] : s2[0];
+    }
     __syncthreads();
-    const double dj = (pd[j][0] + pd[j][1]) + (pd[j][2] + pd[j][3]);
+    const double dj = sum_parts<NW>(part[j & 1][j]);
+    const double alpha = rowj[j & 1][j];
     double t = 0.0, beta = alpha, sc = 0.0;
     if (dj > 0.0) {
       beta = -copysign(sqrt(fma(alpha, alpha, dj)), alpha);
-      t = (beta - alpha) / beta;
-      sc = 1.0 / (alpha - beta);
+      // one division: inv = 1 / (beta (alpha - beta)); t = (beta - alpha) / beta, sc = 1 / (alpha - beta)
+      const double amb = alpha - beta;
+      const double inv = 1.0 / (beta * amb);
+      t = -amb * amb * inv;
+      sc = beta * inv;
     }
-    if (c > j && c < b && t != 0.0) {
-      const double dc = (pd[c][0] + pd[c][1]) + (pd[c][2] + pd[c][3]);
-      const double xcj = xcj_s[c];
-      const double w = t * fma(sc, dc, xcj);
-      const double ws = w * sc;
+    // columns c > j take the reflector; the others update with ws = 0 (x + (-0) xj = x)
+    const bool upd = c > j && c < b && t != 0.0;
+    const double dc = sum_parts<NW>(part[j & 1][c]);
+    const double xcj = rowj[j & 1][c];
+    const double w = t * fma(sc, dc, xcj);
+    const double ws = upd ? w * sc : 0.0;
+    if (q == 0) {
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr)
-        if (q > 0 || rr > j) x[rr] = fma(-ws, xj[rr], x[rr]);
-      if (q == 0) x[j] = xcj - w;  // row j (< 32) lives in chunk 0
-    }
-    if (c == j) {
-      if (q == 0) {
-        x[j] = beta;
-        tau[j] = t;
-        scale[j] = sc;
-      }
-    }
-    if (c == j + 1 && j + 1 < b) {  // publish the next column (updated above)
+        if (rr > j) x[rr] = fma(-ws, xj[rr], x[rr]);
+      // row j (< 32) lives in chunk 0: the reflector's own row (beta) or the R entry
+      const double rj = (c == j) ? beta : xcj - w;
+      const bool setj = upd || c == j;
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr) xb[(j + 1) & 1][q * 32 + rr] = x[rr];
+      for (int rr = 0; rr < 32; ++rr)
+        if (rr == j && setj) x[rr] = rj;
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) x[rr] = fma(-ws, xj[rr], x[rr]);
     }
-    __syncthreads();
+    if (c == j && q == 0) {
+      tau[j] = t;
+      scale[j] = sc;
+    }
   }
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) X[c * LD + q * 32 + rr] = x[rr];
@@ -131,10 +188,12 @@ __device__ void block_house_qr(double* X, double* tau, double* scale, double (*p
 
 // After block_house_qr: R (upper b x b) out, X turned into the explicit unit-lower V in
 // place, and the compact-WY T (Q = I - V T V^T, larft) of the block into Tout (b x b).
+template <int NW>
 __device__ void block_finish(double* X, const double* tau, const double* scale, double* Rout, double* Tout,
-                             double (*G)[TB + 1], int b) {
+                             double (*G)[TB + 1], double (*Wm)[TB + 1], double (*Ym)[TB + 1], int b) {
+  constexpr int TL = Blk<NW>::TL, LD = Blk<NW>::LD, NT = Blk<NW>::NT;
   const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < b * b; e += TTH) {
+  for (int e = threadIdx.x; e < b * b; e += NT) {
     const int cc = e / b, r = e - cc * b;
     Rout[e] = (r <= cc) ? X[cc * LD + r] : 0.0;
   }
@@ -148,9 +207,9 @@ __device__ void block_finish(double* X, const double* tau, const double* scale, 
     }
   }
   __syncthreads();
-  // G = V^T V on the fp64 tensor cores: warp q computes rows 8q .. 8q+7 of G (four 8 x 8
+  // G = V^T V on the fp64 tensor cores: warp q < 4 computes rows 8q .. 8q+7 of G (four 8 x 8
   // fragments), k over the TL block rows in steps of 4 (m8n8k4: A = V^T rows, B = V cols)
-  {
+  if (q < 4) {
     const int ar = c >> 2, ak = c & 3;
     double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll 4
@@ -172,55 +231,68 @@ __device__ void block_finish(double* X, const double* tau, const double* scale, 
   }
   __syncthreads();
   // T by the UT transform: T = S^-1, S = strict_upper(G) + diag(1 / tau) (T^-1 + T^-T =
-  // V^T V for I - V T V^T = H_0 ... H_{b-1}).  Warp 0, lane = column c of T, back
-  // substitution bottom-up with the column in registers (no serial chain across lanes).
-  // A reflector with tau = 0 (H = I: a zero column in this block) has a zero row and column
-  // in T: its S row / column are masked out of the solve.
-  if (q == 0) {
-    double tcol[TB];
-    const bool live_c = c < b && tau[c] != 0.0;
-#pragma unroll
-    for (int r = TB - 1; r >= 0; --r) {
-      double v = 0.0;
-      if (live_c && r <= c && r < b && tau[r] != 0.0) {
-        if (r == c) {
-          v = tau[c];
-        } else {
-          double a2[2] = {0.0, 0.0};
-#pragma unroll
-          for (int k = r + 1; k < TB; ++k)
-            if (k <= c) a2[k & 1] = fma(G[r][k], tcol[k], a2[k & 1]);
-          v = -tau[r] * (a2[0] + a2[1]);
-        }
-      }
-      tcol[r] = v;
+  // V^T V for I - V T V^T = H_0 ... H_{b-1}).  A reflector with tau = 0 (H = I: a zero
+  // column in this block) or beyond b has a zero row and column in T: its S row and column
+  // are the identity's, inverted as such, and its diagonal zeroed afterwards.  The inverse
+  // is built by recursive doubling over the diagonal blocks, all threads at once:
+  //   [A B; 0 D]^-1 = [A^-1, -A^-1 (B D^-1); 0, D^-1]  for block sizes 1, 2, 4, 8, 16.
+  {
+    auto live = [&](int r) { return r < b && tau[r] != 0.0; };
+    for (int e = threadIdx.x; e < TB * TB; e += NT) {
+      const int r = e / TB, k = e - r * TB;
+      Wm[r][k] = (r == k) ? (live(r) ? tau[r] : 1.0) : 0.0;
     }
-    __syncwarp();
+    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < TB; ++r)
-      if (r < c) G[c][r] = tcol[r];  // T's strict upper part, transposed into G's strict lower part
+    for (int sz = 1; sz < TB; sz *= 2) {
+      // Y = B D^-1 for every pair of diagonal blocks (o = 2 sz p): B = S[o:o+sz, o+sz:o+2sz]
+      for (int e = threadIdx.x; e < (TB / 2) * sz; e += NT) {
+        const int pr = e / (sz * sz), rem = e - pr * sz * sz, r = rem / sz, cc = rem - r * sz;
+        const int o = 2 * sz * pr, row = o + r, col = o + sz + cc;
+        double acc = 0.0;
+        for (int k = 0; k <= cc; ++k) {
+          const int kk = o + sz + k;  // D^-1 upper triangular
+          const double bv = (live(row) && live(kk)) ? G[row][kk] : 0.0;
+          acc = fma(bv, Wm[kk][col], acc);
+        }
+        Ym[row][col] = acc;
+      }
+      __syncthreads();
+      // X = -A^-1 Y into the upper-right block
+      for (int e = threadIdx.x; e < (TB / 2) * sz; e += NT) {
+        const int pr = e / (sz * sz), rem = e - pr * sz * sz, r = rem / sz, cc = rem - r * sz;
+        const int o = 2 * sz * pr, row = o + r, col = o + sz + cc;
+        double acc = 0.0;
+        for (int k = r; k < sz; ++k) acc = fma(Wm[row][o + k], Ym[o + k][col], acc);  // A^-1 upper
+        Wm[row][col] = -acc;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < TB && !live(threadIdx.x)) Wm[threadIdx.x][threadIdx.x] = 0.0;
+    __syncthreads();
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < b * b; e += TTH) {
+  for (int e = threadIdx.x; e < b * b; e += NT) {
     const int cc = e / b, r = e - cc * b;
-    Tout[e] = (r < cc) ? G[cc][r] : (r == cc ? tau[r] : 0.0);
+    Tout[e] = (r <= cc) ? Wm[r][cc] : 0.0;
   }
 }
 
-// Level 0 (LEAF): block i = panel rows [i TL, i TL + TL); level >= 1: block i = the stacked
-// R factors 4i .. 4i+3 of the level below.  Writes this block's R, T and explicit V.
-template <bool LEAF>
-__global__ void __launch_bounds__(TTH) tsqr_qr_kernel(TsqrArgs a) {
+// LEAF (NW = NWL): block i = panel rows [i TL, i TL + TL); nodes (NW = NWN): block i = the
+// stacked R factors NW i .. NW i + NW - 1 of the level below.  Writes this block's R, T and
+// explicit V.
+template <bool LEAF, int NW>
+__global__ void __launch_bounds__(32 * NW) tsqr_qr_kernel(TsqrArgs a) {
+  constexpr int TL = Blk<NW>::TL, LD = Blk<NW>::LD;
   extern __shared__ __align__(16) double X[];  // TB x LD
   __shared__ double tau[TB], scale[TB];
-  __shared__ double part[2][TB][4];
-  __shared__ double G[TB][TB + 1];
-  __shared__ double xb[2][TL];
-  __shared__ double xcj_s[TB];
+  __shared__ double part[2][TB][NW];
+  __shared__ double rowj[2][TB];
+  __shared__ __align__(16) double xcol[NW][32];
+  __shared__ double G[TB][TB + 1], Wm[TB][TB + 1], Ym[TB][TB + 1];
   const int b = a.b;
   const long long i = blockIdx.x;
   const long long r0 = i * TL;
-  static_assert(TTH == TL, "one block row per thread in the load / store phases");
+  prof_mark(a.prof, 0);
   {
     // thread = row: all 32 loads in flight before the first shared store (coalesced per column)
     const int r = threadIdx.x;
@@ -233,8 +305,8 @@ __global__ void __launch_bounds__(TTH) tsqr_qr_kernel(TsqrArgs a) {
         ld = a.lda;
       }
     } else {
-      const long long child = 4 * i + r / b;
-      if (r < 4 * b && child < a.nin) {
+      const long long child = NW * i + r / b;
+      if (r < NW * b && child < a.nin) {
         src = a.rin + child * b * b + (r % b);
         ld = b;
       }
@@ -245,27 +317,33 @@ __global__ void __launch_bounds__(TTH) tsqr_qr_kernel(TsqrArgs a) {
     for (int c = 0; c < TB; ++c) X[c * LD + r] = v[c];
   }
   __syncthreads();
-  block_house_qr(X, tau, scale, part, xb, xcj_s, b);
-  block_finish(X, tau, scale, a.rout + i * b * b, a.tnode + i * TB * TB, G, b);
+  prof_mark(a.prof, 1);
+  block_house_qr<NW>(X, tau, scale, part, rowj, xcol, b);
+  prof_mark(a.prof, 2);
+  block_finish<NW>(X, tau, scale, a.rout + i * b * b, a.tnode + i * TB * TB, G, Wm, Ym, b);
   __syncthreads();
+  prof_mark(a.prof, 3);
   {
     const int r = threadIdx.x;
-    double* dst = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.vnode + i * (TB * TL) + r;
-    const long long ld = LEAF ? a.lda : TL;
+    double* dst = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.vnode + i * (TB * TLN) + r;
+    const long long ld = LEAF ? a.lda : TLN;
     if (dst) {
 #pragma unroll
       for (int c = 0; c < TB; ++c)
         if (c < b) dst[c * ld] = X[c * LD + r];
     }
   }
+  prof_mark(a.prof, 4);
 }
 
 // Top-down explicit Q: block i's output = Q_i [C_i; 0] = [C_i; 0] - V (T (V_top^T C_i)),
-// C_i = rows (i % 4) b .. of the parent's output block (I at the root): two b x b products
-// and one TL x b x b product per block, no reductions over rows.  Leaves write their rows
-// of the sub-panel's Q in place.
-template <bool LEAF>
-__global__ void __launch_bounds__(TTH) tsqr_expand_kernel(TsqrArgs a) {
+// C_i = rows (i % NWN) b .. of the parent's output block (I at the root): two b x b
+// products and one TL x b x b product per block, no reductions over rows.  Leaves write
+// their rows of the sub-panel's Q in place.
+template <bool LEAF, int NW>
+__global__ void __launch_bounds__(32 * NW) tsqr_expand_kernel(TsqrArgs a) {
+  constexpr int TL = Blk<NW>::TL, LD = Blk<NW>::LD, NT = Blk<NW>::NT;
+  constexpr int RPW = TB / NW;  // rows of the b x b products per warp
   extern __shared__ __align__(16) double V[];  // TB x LD, then reused for the output
   __shared__ double C[TB][TB + 1], Y[TB][TB + 1], T[TB][TB + 1];
   const int b = a.b;
@@ -274,48 +352,48 @@ __global__ void __launch_bounds__(TTH) tsqr_expand_kernel(TsqrArgs a) {
   const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
   {
     const int r = threadIdx.x;
-    const double* src = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.vnode + i * (TB * TL) + r;
-    const long long ld = LEAF ? a.lda : TL;
+    const double* src = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.vnode + i * (TB * TLN) + r;
+    const long long ld = LEAF ? a.lda : TLN;
     double v[TB];
 #pragma unroll
     for (int cc = 0; cc < TB; ++cc) v[cc] = (src && cc < b) ? src[cc * ld] : 0.0;
 #pragma unroll
     for (int cc = 0; cc < TB; ++cc) V[cc * LD + r] = v[cc];
   }
-  for (int e = threadIdx.x; e < TB * TB; e += TTH) {
+  for (int e = threadIdx.x; e < TB * TB; e += NT) {
     const int cc = e / TB, r = e - cc * TB;
     double x = 0.0, t = 0.0;
     if (cc < b && r < b) {
-      x = a.cin ? a.cin[(i / 4) * (TB * TL) + (long long)cc * TL + (i % 4) * b + r] : (r == cc ? 1.0 : 0.0);
+      x = a.cin ? a.cin[(i / NWN) * (TB * TLN) + (long long)cc * TLN + (i % NWN) * b + r] : (r == cc ? 1.0 : 0.0);
       t = a.tnode[i * TB * TB + r + cc * b];
     }
     C[r][cc] = x;  // C[row][col]
     T[r][cc] = t;
   }
   __syncthreads();
-  // Y = V_top^T C  (thread (c, q): rows 8q .. 8q+7 of Y, column c)
-  double y[8];
+  // Y = V_top^T C  (thread (c, q): rows RPW q .. RPW q + RPW - 1 of Y, column c)
+  double y[RPW];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int row = q * 8 + k;
+  for (int k = 0; k < RPW; ++k) {
+    const int row = q * RPW + k;
     double acc = 0.0;
     for (int kk = 0; kk < b; ++kk) acc = fma(V[row * LD + kk], C[kk][c], acc);
     y[k] = acc;
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) Y[q * 8 + k][c] = y[k];
+  for (int k = 0; k < RPW; ++k) Y[q * RPW + k][c] = y[k];
   __syncthreads();
   // Y2 = T Y   (same ownership; T upper triangular)
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int row = q * 8 + k;
+  for (int k = 0; k < RPW; ++k) {
+    const int row = q * RPW + k;
     double acc = 0.0;
     for (int kk = row; kk < b; ++kk) acc = fma(T[row][kk], Y[kk][c], acc);
     y[k] = acc;
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 8; ++k) Y[q * 8 + k][c] = y[k];
+  for (int k = 0; k < RPW; ++k) Y[q * RPW + k][c] = y[k];
   __syncthreads();
   // X = [C; 0] - V Y2: thread (c, q) computes rows 32q .. 32q+31 of column c
   double x[32];
@@ -336,8 +414,8 @@ __global__ void __launch_bounds__(TTH) tsqr_expand_kernel(TsqrArgs a) {
   __syncthreads();
   {
     const int r = threadIdx.x;
-    double* dst = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.xout + i * (TB * TL) + r;
-    const long long ld = LEAF ? a.lda : TL;
+    double* dst = LEAF ? ((r0 + r < a.rows) ? a.panel + r0 + r : nullptr) : a.xout + i * (TB * TLN) + r;
+    const long long ld = LEAF ? a.lda : TLN;
     if (dst) {
 #pragma unroll
       for (int cc = 0; cc < TB; ++cc)
@@ -430,7 +508,6 @@ __global__ void __launch_bounds__(128) recon_solve_kernel(double* panel, long lo
   }
 }
 
-size_t block_smem() { return sizeof(double) * TB * LD; }
 
 }  // namespace
 
@@ -438,19 +515,20 @@ size_t block_smem() { return sizeof(double) * TB * LD; }
 void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double* tau) {
   const long long kmax = std::min<long long>(rows, p);
   if (kmax <= 0) return;
-  // per sub-panel scratch: level sizes of the tree over the leaves
-  const long long n0 = (rows + TL - 1) / TL;
+  // per sub-panel scratch: level sizes of the tree over the leaves (leaves of 128 rows, nodes
+  // of fan-in NWN)
+  const long long n0 = (rows + Blk<NWL>::TL - 1) / Blk<NWL>::TL;
   std::vector<long long> nl{n0};
-  while (nl.back() > 1) nl.push_back((nl.back() + 3) / 4);
+  while (nl.back() > 1) nl.push_back((nl.back() + NWN - 1) / NWN);
   const int levels = (int)nl.size();
   long long nodes_above = 0;
   for (int l = 1; l < levels; ++l) nodes_above += nl[l];
-  // layout: R of every level, tau of every level, node reflectors and node outputs (levels >= 1),
+  // layout: R of every level, T of every level, node reflectors and node outputs (levels >= 1),
   // small blocks (U, Vtop, T), and the trailing GEMM temporaries (W, X: TB x p each)
   long long total_nodes = n0 + nodes_above;
   const size_t n_r = (size_t)total_nodes * TB * TB;
   const size_t n_tau = (size_t)total_nodes * TB * TB;  // T of every block
-  const size_t n_v = (size_t)nodes_above * TB * TL;
+  const size_t n_v = (size_t)nodes_above * TB * TLN;
   const size_t n_small = 3 * TB * TB;
   const size_t n_w = 2 * (size_t)TB * p;
   double* scr = nullptr;
@@ -469,19 +547,24 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
     off[l] = off[l - 1] + nl[l - 1];
     voff[l] = (l == 1) ? 0 : voff[l - 1] + nl[l - 1];
   }
-  kernel_setup(c, tsqr_qr_kernel<true>, TTH, block_smem());
-  kernel_setup(c, tsqr_qr_kernel<false>, TTH, block_smem());
-  kernel_setup(c, tsqr_expand_kernel<true>, TTH, block_smem());
-  kernel_setup(c, tsqr_expand_kernel<false>, TTH, block_smem());
+  kernel_setup(c, tsqr_qr_kernel<true, NWL>, Blk<NWL>::NT, Blk<NWL>::SMEM);
+  kernel_setup(c, tsqr_qr_kernel<false, NWN>, Blk<NWN>::NT, Blk<NWN>::SMEM);
+  kernel_setup(c, tsqr_expand_kernel<true, NWL>, Blk<NWL>::NT, Blk<NWL>::SMEM);
+  kernel_setup(c, tsqr_expand_kernel<false, NWN>, Blk<NWN>::NT, Blk<NWN>::SMEM);
+  // PW_TSQR_PROF=1: phase timestamps of block 0 of the last tree level's QR (debug)
+  unsigned long long* prof = nullptr;
+  const char* pe = getenv("PW_TSQR_PROF");
+  if (pe && *pe == '1') PW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prof), 8 * 8, c.stream));
   for (long long j0 = 0; j0 < kmax; j0 += TB) {
     const int b = (int)std::min<long long>(TB, kmax - j0);
     const long long mrows = rows - j0;
     double* P = A + j0 + j0 * lda;
     // the tree shape depends on mrows: recompute (fewer leaves for later sub-panels)
-    std::vector<long long> ml{(mrows + TL - 1) / TL};
-    while (ml.back() > 1) ml.push_back((ml.back() + 3) / 4);
+    std::vector<long long> ml{(mrows + Blk<NWL>::TL - 1) / Blk<NWL>::TL};
+    while (ml.back() > 1) ml.push_back((ml.back() + NWN - 1) / NWN);
     const int L = (int)ml.size();
     TsqrArgs a{};
+    a.prof = prof;
     a.panel = P;
     a.lda = lda;
     a.rows = mrows;
@@ -491,12 +574,12 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
       a.tnode = Tb + off[l] * TB * TB;
       a.rout = Rb + off[l] * TB * TB;
       if (l == 0) {
-        tsqr_qr_kernel<true><<<(unsigned)ml[0], TTH, block_smem(), c.stream>>>(a);
+        tsqr_qr_kernel<true, NWL><<<(unsigned)ml[0], Blk<NWL>::NT, Blk<NWL>::SMEM, c.stream>>>(a);
       } else {
         a.rin = Rb + off[l - 1] * TB * TB;
         a.nin = (int)ml[l - 1];
-        a.vnode = Vb + voff[l] * TB * TL;
-        tsqr_qr_kernel<false><<<(unsigned)ml[l], TTH, block_smem(), c.stream>>>(a);
+        a.vnode = Vb + voff[l] * TB * TLN;
+        tsqr_qr_kernel<false, NWN><<<(unsigned)ml[l], Blk<NWN>::NT, Blk<NWN>::SMEM, c.stream>>>(a);
       }
       c.launches += 1;
       PW_LAUNCH_CHECK();
@@ -505,13 +588,13 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
     // 2. explicit Q down the tree
     for (int l = L - 1; l >= 0; --l) {
       a.tnode = Tb + off[l] * TB * TB;
-      a.cin = (l == L - 1) ? nullptr : Xb + voff[l + 1] * TB * TL;
+      a.cin = (l == L - 1) ? nullptr : Xb + voff[l + 1] * TB * TLN;
       if (l == 0) {
-        tsqr_expand_kernel<true><<<(unsigned)ml[0], TTH, block_smem(), c.stream>>>(a);
+        tsqr_expand_kernel<true, NWL><<<(unsigned)ml[0], Blk<NWL>::NT, Blk<NWL>::SMEM, c.stream>>>(a);
       } else {
-        a.vnode = Vb + voff[l] * TB * TL;
-        a.xout = Xb + voff[l] * TB * TL;
-        tsqr_expand_kernel<false><<<(unsigned)ml[l], TTH, block_smem(), c.stream>>>(a);
+        a.vnode = Vb + voff[l] * TB * TLN;
+        a.xout = Xb + voff[l] * TB * TLN;
+        tsqr_expand_kernel<false, NWN><<<(unsigned)ml[l], Blk<NWN>::NT, Blk<NWN>::SMEM, c.stream>>>(a);
       }
       c.launches += 1;
       PW_LAUNCH_CHECK();
@@ -536,6 +619,14 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
     }
   }
   PW_CUDA(cudaFreeAsync(scr, c.stream));
+  if (prof) {
+    unsigned long long t[8];
+    PW_CUDA(cudaMemcpyAsync(t, prof, sizeof(t), cudaMemcpyDeviceToHost, c.stream));
+    PW_CUDA(cudaStreamSynchronize(c.stream));
+    fprintf(stderr, "[tsqr prof] load %.1f us  house %.1f us  finish %.1f us  store %.1f us\n", (t[1] - t[0]) * 1e-3,
+            (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3);
+    PW_CUDA(cudaFreeAsync(prof, c.stream));
+  }
 }
 
 }  // namespace pw
