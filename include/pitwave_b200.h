@@ -186,6 +186,19 @@ typedef int (*pw_allgather_hook)(void* user, double* data, long long block, long
 int pw_ctx_set_comm(pw_ctx* ctx, int rank, int world, pw_allreduce_hook allreduce,
                     pw_allgather_hook allgather, void* user);
 int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards);
+/* Native NCCL transport for the same collectives (replaces the hooks above; the serial
+ * step's allreduce and all-gather are then enqueued from the library on the context
+ * stream, no host round-trip per step -- reference serial loop parareal.py:128-132):
+ *   pw_nccl_unique_id(id)   rank 0: 128-byte ncclUniqueId to broadcast to the others
+ *   pw_ctx_set_nccl(ctx, id, rank, world)   every rank: ncclCommInitRank on the
+ *                           context's device; sets rank / world like pw_ctx_set_comm.
+ * NCCL is resolved at run time (libnccl.so.2 already in the process, e.g. torch's).
+ * pw_comm_allreduce / pw_comm_allgather expose the transport (hooks or NCCL) directly:
+ * allreduce = in-place sum of count doubles; allgather = as the hook above. */
+int pw_nccl_unique_id(unsigned char* id128);
+int pw_ctx_set_nccl(pw_ctx* ctx, const unsigned char* id128, int rank, int world);
+int pw_comm_allreduce(pw_ctx* ctx, double* data, long long count);
+int pw_comm_allgather(pw_ctx* ctx, double* data, long long block, long long total);
 /* Row-sharded subspace factorisation (distributed TSQR) for sharded sweeps
  * (world > 1 or row shards > 1): each shard Householder-factors its row block of the
  * snapshots, the m x m R factors are all-gathered (allgather hook, block m*m) and factored

@@ -94,6 +94,10 @@ SIGNATURES = [
     ("pw_ctx_set_comm", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ALLREDUCE_HOOK, ALLGATHER_HOOK,
                                        c_vp]),
     ("pw_ctx_set_row_shards", ctypes.c_int, [c_vp, ctypes.c_int]),
+    ("pw_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("pw_ctx_set_nccl", ctypes.c_int, [c_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+    ("pw_comm_allreduce", ctypes.c_int, [c_vp, c_vp, ctypes.c_longlong]),
+    ("pw_comm_allgather", ctypes.c_int, [c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong]),
     ("pw_ctx_set_tsqr", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("pw_copy", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_longlong]),
     ("pw_residual", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_longlong, c_dp]),

@@ -617,8 +617,7 @@ static void factor_tsqr(pw_basis* B) {
     // the fine sweep): hand the R factors over and take the gathered ones back with syncs of
     // the two streams (once per update)
     PW_CUDA(cudaStreamSynchronize(c.stream));
-    PW_CHECK(c.allgather_hook(c.comm_user, RG, (long long)m * m, (long long)nsh * m * m) == 0, PW_ERR_STATE,
-             "all-gather hook failed (TSQR R factors)");
+    pw::comm_allgather(c, RG, (long long)m * m, (long long)nsh * m * m);  // TSQR R factors
     if (c.outer) PW_CUDA(cudaStreamSynchronize(c.outer));
   }
   for (int g = 0; g < nsh; ++g)  // stack: RR[g m : (g+1) m, :] = R_g
@@ -909,6 +908,8 @@ int pw_ctx_destroy(pw_ctx* ctx) {
       cudaStreamSynchronize(ctx->c.side);
       cudaStreamDestroy(ctx->c.side);
     }
+    pw::nccl_destroy(ctx->c);
+    if (ctx->c.comm_scratch) cudaFree(ctx->c.comm_scratch);
     if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
     if (ctx->c.cublas) cublasDestroy(blas(ctx->c));
     if (ctx->c.cusolver_params) cusolverDnDestroyParams(static_cast<cusolverDnParams_t>(ctx->c.cusolver_params));
@@ -928,6 +929,35 @@ int pw_ctx_set_comm(pw_ctx* ctx, int rank, int world, pw_allreduce_hook allreduc
     ctx->c.allreduce_hook = allreduce;
     ctx->c.allgather_hook = allgather;
     ctx->c.comm_user = user;
+  });
+}
+
+int pw_nccl_unique_id(unsigned char* id128) {
+  return guarded([&] {
+    PW_CHECK(id128 != nullptr, PW_ERR_VALUE, "id buffer is NULL");
+    pw::nccl_unique_id(id128);
+  });
+}
+
+int pw_ctx_set_nccl(pw_ctx* ctx, const unsigned char* id128, int rank, int world) {
+  return guarded([&] {
+    PW_CHECK(ctx && id128, PW_ERR_VALUE, "bad argument");
+    PW_CHECK(world >= 1 && rank >= 0 && rank < world, PW_ERR_VALUE, "bad rank / world");
+    pw::nccl_init(ctx->c, id128, rank, world);
+  });
+}
+
+int pw_comm_allreduce(pw_ctx* ctx, double* data, long long count) {
+  return guarded([&] {
+    PW_CHECK(ctx && data && count >= 0, PW_ERR_VALUE, "bad argument");
+    if (ctx->c.comm_world > 1 || ctx->c.nccl) pw::comm_allreduce(ctx->c, data, count);
+  });
+}
+
+int pw_comm_allgather(pw_ctx* ctx, double* data, long long block, long long total) {
+  return guarded([&] {
+    PW_CHECK(ctx && data && block >= 1 && total >= 0, PW_ERR_VALUE, "bad argument");
+    if (ctx->c.comm_world > 1 || ctx->c.nccl) pw::comm_allgather(ctx->c, data, block, total);
   });
 }
 
@@ -1527,8 +1557,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             // correction reads no others)
             const long long lo = B->row_lo, nr = B->dim;
             gemm(c, true, false, r, n_c, nr, 1.0, B->Q.p, nr, QK + lo, d, 0.0, ab, r);
-            PW_CHECK(c.allreduce_hook(c.comm_user, ab, (long long)r * n_c) == 0, PW_ERR_STATE,
-                     "allreduce hook failed (TSQR projection)");
+            pw::comm_allreduce(c, ab, (long long)r * n_c);  // TSQR projection partials
             gemm(c, false, false, nr, n_c, r, -1.0, B->Y.p, nr, ab, r, 1.0, PRED, ldr);
           } else {
             gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
@@ -1560,7 +1589,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
           double* rr = a_part;
           const double rv = (double)r;
           PW_CUDA(cudaMemcpyAsync(rr, &rv, sizeof(double), cudaMemcpyHostToDevice, c.stream));
-          PW_CHECK(c.allreduce_hook(c.comm_user, rr, 1) == 0, PW_ERR_STATE, "allreduce hook failed");
+          pw::comm_allreduce(c, rr, 1);
           double tot = 0.0;
           PW_CUDA(cudaMemcpyAsync(&tot, rr, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
           PW_CUDA(cudaStreamSynchronize(c.stream));
@@ -1591,9 +1620,8 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
                                       cudaMemcpyDeviceToDevice, c.stream));
           }
           if (comm) {
-            PW_CHECK(c.allreduce_hook(c.comm_user, a_nxt, r) == 0, PW_ERR_STATE, "allreduce hook failed");
-            PW_CHECK(c.allgather_hook(c.comm_user, QN + (size_t)(i + 1) * d, blk, d) == 0, PW_ERR_STATE,
-                     "all-gather hook failed");
+            pw::comm_allreduce(c, a_nxt, r);
+            pw::comm_allgather(c, QN + (size_t)(i + 1) * d, blk, d);
           } else {
             pw::launch_axpby_cols(c, a_nxt, a_part, a_part + r, 1.0, 1.0, (size_t)r);
             for (int sh = 2; sh < nsh; ++sh)

@@ -125,6 +125,9 @@ struct Ctx {
   pw_allreduce_hook allreduce_hook = nullptr;
   pw_allgather_hook allgather_hook = nullptr;
   void* comm_user = nullptr;
+  void* nccl = nullptr;              // ncclComm_t owned by the library (pw_ctx_set_nccl), or null
+  double* comm_scratch = nullptr;    // world x block doubles for the padded NCCL all-gather
+  size_t comm_scratch_n = 0;
   pw_fine_hook fine_hook = nullptr;  // slice-sharded fine predictor (multi-GPU), see header
   pw_fine_rows_hook fine_rows_hook = nullptr;  // ... delivering this rank's rows (row-local sweeps)
   void* fine_rows_user = nullptr;
@@ -140,6 +143,15 @@ template <class F>
 inline int kernel_setup(const Ctx& c, F* kern, int threads, size_t smem) {
   return kernel_setup(c.device, reinterpret_cast<const void*>(kern), threads, smem);
 }
+
+// ---------------------------------------------------------------- collectives (comm.cu)
+// The row-sharded sweep's collectives on the context stream: NCCL when the context owns a
+// communicator (pw_ctx_set_nccl), else the pw_ctx_set_comm hooks.
+void nccl_unique_id(unsigned char* out128);
+void nccl_init(Ctx& c, const unsigned char* id128, int rank, int world);
+void nccl_destroy(Ctx& c);
+void comm_allreduce(Ctx& c, double* data, long long count);
+void comm_allgather(Ctx& c, double* data, long long block, long long total);
 
 // ---------------------------------------------------------------- kernels (launchers)
 // exact.cu  (compiled with -fmad=false: reference operation order, bitwise)

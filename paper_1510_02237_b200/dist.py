@@ -241,6 +241,41 @@ def device_vector(ptr: int, n: int, device) -> torch.Tensor:
     return torch.as_tensor(_DevVector(ptr, n), device=device)
 
 
+class NcclComm:
+    """The library's own NCCL communicator for the row-sharded sweep (pw_ctx_set_nccl).
+
+    Collective over `group`: rank 0 creates the 128-byte ncclUniqueId (pw_nccl_unique_id),
+    torch.distributed broadcasts it once, and every rank initialises the context's
+    communicator.  From then on the serial correction's allreduce of r doubles and
+    all-gather of qn's row blocks, and the TSQR all-gather, are NCCL calls the library
+    enqueues on its stream -- no Python callback per serial step.
+    """
+
+    def __init__(self, ctx, group=None):
+        from . import _lib
+
+        self.ctx = ctx
+        rank, world = tdist.get_rank(group), tdist.get_world_size(group)
+        idbuf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(ctx.lib.pw_nccl_unique_id(idbuf))
+        obj = [idbuf.raw]
+        tdist.broadcast_object_list(obj, src=tdist.get_global_rank(group, 0) if group is not None else 0,
+                                    group=group)
+        _lib.check(ctx.lib.pw_ctx_set_nccl(ctx.handle, obj[0], rank, world))
+        self.rank, self.world = rank, world
+
+    def allreduce(self, t: torch.Tensor) -> None:
+        from . import _lib
+
+        _lib.check(self.ctx.lib.pw_comm_allreduce(self.ctx.handle, _lib.ptr(t), t.numel()))
+
+    def allgather(self, t: torch.Tensor, block: int) -> None:
+        from . import _lib
+
+        _lib.check(self.ctx.lib.pw_comm_allgather(self.ctx.handle, _lib.ptr(t), int(block), t.numel()))
+
+
 class RowShardComm:
     """Collectives of the row-sharded serial correction (include/pitwave_b200.h,
     pw_ctx_set_comm): an in-place allreduce of the partial alpha (r doubles) and an
