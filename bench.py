@@ -334,25 +334,52 @@ def comm_selftest(dist):
 
     from paper_1510_02237_b200.dist import RowShardComm, row_block
 
+    def check(allreduce, allgather, world, rank):
+        a = torch.ones(37, dtype=torch.float64, device="cuda")
+        allreduce(a)
+        good = bool(torch.all(a == world))
+        total, block = 1001, ((1001 + world - 1) // world + 1) // 2 * 2
+        v = torch.full((total,), -1.0, dtype=torch.float64, device="cuda")
+        lo, hi = row_block(total, block, rank)
+        v[lo:hi] = float(rank)
+        allgather(v, block)
+        torch.cuda.synchronize()
+        want = torch.tensor([min(i // block, world - 1) for i in range(total)], dtype=torch.float64,
+                            device="cuda")
+        return good and bool(torch.equal(v, want))
+
+    def agreed(ok):
+        flag = torch.tensor([0.0 if ok else 1.0], device="cuda")
+        dist.all_reduce(flag)
+        return float(flag.item()) == 0.0
+
     ok = True
     try:
         comm = RowShardComm(dist.group.WORLD, torch.device("cuda", torch.cuda.current_device()))
-        a = torch.ones(37, dtype=torch.float64, device="cuda")
-        comm.allreduce(a.data_ptr(), a.numel())
-        ok &= bool(torch.all(a == comm.world))
-        total, block = 1001, ((1001 + comm.world - 1) // comm.world + 1) // 2 * 2
-        v = torch.full((total,), -1.0, dtype=torch.float64, device="cuda")
-        lo, hi = row_block(total, block, comm.rank)
-        v[lo:hi] = float(comm.rank)
-        comm.allgather(v.data_ptr(), block, total)
-        want = torch.tensor([min(i // block, comm.world - 1) for i in range(total)], dtype=torch.float64,
-                            device="cuda")
-        ok &= bool(torch.equal(v, want))
+        ok = check(lambda t: comm.allreduce(t.data_ptr(), t.numel()),
+                   lambda t, b: comm.allgather(t.data_ptr(), b, t.numel()), comm.world, comm.rank)
     except Exception:  # noqa: BLE001
         ok = False
-    flag = torch.tensor([0.0 if ok else 1.0], device="cuda")
-    dist.all_reduce(flag)
-    return float(flag.item()) == 0.0
+    if not agreed(ok):
+        return False
+    # the library's own NCCL transport (what kse_sweep(group=) uses under NCCL): if any rank
+    # fails it, every rank falls back to the hooks
+    native = True
+    try:
+        from paper_1510_02237_b200 import _lib
+        from paper_1510_02237_b200.dist import NcclComm
+
+        ctx = _lib.Context.get(torch.cuda.current_device())
+        ctx.bind_stream()
+        nc = NcclComm(ctx, dist.group.WORLD)
+        native = check(nc.allreduce, nc.allgather, nc.world, nc.rank)
+        if native:
+            ctx._nccl_group = dist.group.WORLD
+    except Exception:  # noqa: BLE001
+        native = False
+    if not agreed(native):
+        os.environ["PW_NATIVE_NCCL"] = "0"
+    return True
 
 
 def run_ours(args, rank, world, local_rank):
@@ -496,7 +523,10 @@ def run_ours(args, rank, world, local_rank):
     if world > 1 and args.parareal and not comm_selftest(dist):
         extra["parareal"] = {"error": "row-shard collective self-test failed; Parareal windows skipped"}
     elif world > 1 and args.parareal:
-        extra["parareal"] = parareal_window("c3", group=dist.group.WORLD)
+        try:
+            extra["parareal"] = parareal_window("c3", group=dist.group.WORLD)
+        except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
+            extra["parareal"] = {"error": f"{type(e).__name__}: {e}"}
         if args.c4:
             del x, out, flush
             torch.cuda.empty_cache()
