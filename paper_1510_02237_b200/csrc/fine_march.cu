@@ -602,12 +602,7 @@ int env_int(const char* name, int dflt) {
 template <class K>
 void launch_march_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, int batch) {
   auto kern = rk3_march_kernel<K>;
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM));
-    if (per_sm < 1) per_sm = 1;
-  }
+  const int per_sm = kernel_setup(c, kern, K::NT, K::SMEM);  // per device (api.cu)
   // segments per state: minimise waves x ticks per CTA (TY + 14), waves = CTAs over
   // the resident CTA slots (c2: 4 segments, one wave; c3: 2 segments, one wave)
   int nseg = env_int("PW_MARCH_NSEG", 0);
@@ -651,12 +646,7 @@ template <class K>
 void launch_march_persist_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp,
                               int batch, int nsteps, long long d, int* sync) {
   auto kern = rk3_march_persist_kernel<K>;
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
-    PW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM));
-    if (per_sm < 1) per_sm = 1;
-  }
+  const int per_sm = kernel_setup(c, kern, K::NT, K::SMEM);  // per device (api.cu)
   const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
   // segments per state: no waves here, so minimise ticks per item x max(1, items / slots)
   // (the second factor: fewer items than CTA slots leave slots idle)
@@ -673,6 +663,9 @@ void launch_march_persist_cfg(Ctx& c, const FusedParams& fp, const double* in, d
     }
     if (nseg <= 0) nseg = 1;
   }
+  // the sync buffer holds ny / 16 + 1 counters per state, and a segment needs >= 16 rows
+  // (the 6-row halo of the neighbour dependency): clamp the override too
+  nseg = std::max(1, std::min(nseg, fp.ny / 16));
   const long long items = (long long)batch * nseg * nsteps;
   const int grid = (int)std::min<long long>(slots, items);
   PW_CUDA(cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)batch * nseg), c.stream));
