@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "pw_internal.h"

@@ -58,7 +58,7 @@ def run_both(dev, spec, x, nsteps):
     return got, want
 
 
-@pytest.mark.parametrize("variant", ["2", "3", "4"])
+@pytest.mark.parametrize("variant", ["2", "3", "4", "5"])
 @pytest.mark.parametrize("nx,ny", [(512, 512), (256, 256), (512, 320), (1024, 1024), (128, 128), (256, 96)])
 def test_nf_coarse_bitwise(dev, monkeypatch, variant, nx, ny):
     monkeypatch.setenv("PW_COARSE_NF", variant)
