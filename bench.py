@@ -289,11 +289,14 @@ def parareal_window(name="c3", warm=True, group=None):
     peak, _ = load_peaks()
     fine_bytes = 48.0 * wl.n_p * len(res) * fine.nsteps * d / 3
     serial_bytes = sum(wl.n_p * (2.0 * r * d * 8 + 3.0 * d * 8) for r in ranks)
-    roof = {"peak_gbs": peak,
+    # N ranks: the fine slices and the serial row blocks are split over the ranks, so the
+    # fractions are of the aggregate peak (N x the per-GPU peak)
+    agg = peak * n_ranks
+    roof = {"peak_gbs": peak, "n_gpus": n_ranks,
             "fine": {"algorithmic_bytes": fine_bytes,
-                     "frac": fine_bytes / tm.fine / 1e9 / peak if tm.fine else None},
+                     "frac": fine_bytes / tm.fine / 1e9 / agg if tm.fine else None},
             "coarse_and_correction": {"algorithmic_bytes": serial_bytes,
-                                      "frac": serial_bytes / tm.coarse / 1e9 / peak if tm.coarse else None,
+                                      "frac": serial_bytes / tm.coarse / 1e9 / agg if tm.coarse else None,
                                       "note": "HBM bytes of the serial GEMV passes over the whole phase "
                                               "time (the latency-bound coarse G included)"}}
     extra = {"reference_window": c3_reference_window()} if name == "c3" else {}
@@ -304,8 +307,9 @@ def parareal_window(name="c3", warm=True, group=None):
             "fine_cell_updates_per_s": wl.n_p * wl.n_it * fine.nsteps * d / 3 / tm.fine if tm.fine else None,
             "memory_gib": _memory_gib(fine.ctx),
             "roofline": roof, "warm": warm, "n_gpus": n_ranks,
-            "parallelism": "fine sweep slice-sharded over ranks, serial correction replicated"
-                           if n_ranks > 1 else "single GPU"}
+            "parallelism": "fine sweep slice-sharded over ranks, serial correction row-sharded "
+                           "(collectives on the library's NCCL communicator, or the hooks if its "
+                           "self-test failed), coarse G replicated" if n_ranks > 1 else "single GPU"}
 
 
 def _memory_gib(ctx):
