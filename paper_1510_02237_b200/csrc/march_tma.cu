@@ -41,22 +41,30 @@
 namespace pw {
 namespace {
 
-template <int NX_>
+// NX columns per CTA; CL CTAs of a thread-block cluster share each grid row (rows of
+// NXT = CL NX cells: 1024 and 2048 as 2 and 4 CTAs of 512).  With CL > 1 a ring field row
+// carries a 32-double pad: its right halo (the right neighbour's first 4 columns) at
+// [NX, NX + 4), its left halo at [NX + 16, NX + 20) -- TMA-loaded for q, stored over DSMEM by
+// the neighbour's edge threads for s1 / s2.
+template <int NX_, int CL_ = 1>
 struct TK {
-  static constexpr int NX = NX_, BX = 4;
+  static constexpr int NX = NX_, BX = 4, CL = CL_, NXT = CL * NX;
   static constexpr int GS = NX / BX;   // threads per stage group
   static constexpr int NT = 3 * GS;
   static constexpr int CH = NX / 2;    // 16-byte chunks per field row
-  static constexpr int SLOT = 3 * NX;  // doubles per ring slot: u, v, p rows
+  static constexpr int FS = CL > 1 ? NX + 32 : NX;  // doubles per ring field row
+  static constexpr int HR = NX, HL = NX + 16;       // halo offsets in a ring field row (CL > 1)
+  static constexpr int SLOT = 3 * FS;  // doubles per ring slot: u, v, p rows
   static constexpr int NQ = 8, N1 = 3, N2 = 3;
   static constexpr size_t RING = sizeof(double) * SLOT * (NQ + N1 + N2);
   static constexpr size_t SMEM = RING + 1024 + 8 * NQ;  // + alignment slack + mbarriers
-  static constexpr uint32_t ROW_BYTES = SLOT * sizeof(double);
+  // bytes one q row brings: the CTA's 3 x NX cells (+ 3 x 2 halos of 4 cells with CL > 1)
+  static constexpr uint32_t ROW_BYTES = (3 * NX + (CL > 1 ? 24 : 0)) * sizeof(double);
   static constexpr int MB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MB_REGS = 65536 / (NT * 168);
   static constexpr int MINB = (MB_SMEM < MB_REGS ? MB_SMEM : MB_REGS) < 1 ? 1 : (MB_SMEM < MB_REGS ? MB_SMEM : MB_REGS);
   static_assert(GS % 32 == 0, "stage groups must be whole warps");
-  static_assert((SLOT * 8) % 1024 == 0, "ring slots keep the 1024-byte TMA alignment");
+  static_assert((FS * 8) % 256 == 0, "ring field rows keep the 256-byte alignment of the 32-byte swizzle");
 };
 
 __device__ __forceinline__ int swz(int c) { return c ^ ((c >> 3) & 1); }
@@ -86,6 +94,30 @@ __device__ __forceinline__ void tma_row(const CUtensorMap* map, double* slot, ui
       : "memory");
 }
 __device__ __forceinline__ void bar_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// the same shared-memory location in CTA `rank` of the cluster (generic address)
+template <class T>
+__device__ __forceinline__ T* peer_smem(T* p, unsigned rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<T*>(out);
+}
+// one 4-cell tile (16-byte chunks) of the TMA view at (col4, gy, field, b) -> smem
+__device__ __forceinline__ void tma_box(const CUtensorMap* map, void* dst, uint64_t* bar, int col4, int gy, int f,
+                                        int b) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(col4), "r"(gy), "r"(f), "r"(b), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -122,6 +154,7 @@ struct Acc {
 // Where the completed rows go: the next stage's ring (S < 2) or the state in HBM (S = 2).
 struct Sink {
   double* ring;     // S < 2: the output ring's slot 0
+  unsigned left, right;  // CL > 1: cluster ranks of the CTAs holding the columns left / right
   double* g;        // S = 2: this thread's columns of the segment's first row (u field)
   long long n;      // nx * ny (field stride)
   int TY;
@@ -180,26 +213,46 @@ __device__ __forceinline__ void xstencil(double (&acc)[4], double (&d1)[4], cons
 
 // Consume input row k (ring slot `in`; q row k+1 at `qb` for the births when S > 0), store
 // the completed rows: u, p of row k-1 and v of row k-2.  PH = k mod 3 (compile time).
-template <int NX, int S, int PH, bool PEERS>
+// CL > 1, S < 2: the edge threads also store their outer 4 cells into the neighbouring CTAs'
+// halos of the same ring row (DSMEM): g = 0's first cells are the left neighbour's right
+// halo, the last thread's last cells the right neighbour's left halo
+template <int NX, int FS, int CL>
+__device__ __forceinline__ void st_ring(double* row, const int* woff2, const double (&v)[4], int g, const Sink& o) {
+  st4(row, woff2, v);
+  if constexpr (CL > 1) {
+    if (g == 0) {
+      double2* h = reinterpret_cast<double2*>(peer_smem(row + NX, o.left));
+      h[0] = make_double2(v[0], v[1]);
+      h[1] = make_double2(v[2], v[3]);
+    } else if (g == NX / 4 - 1) {
+      double2* h = reinterpret_cast<double2*>(peer_smem(row + NX + 16, o.right));
+      h[0] = make_double2(v[0], v[1]);
+      h[1] = make_double2(v[2], v[3]);
+    }
+  }
+}
+
+template <int NX, int S, int PH, bool PEERS, int FS = NX, int CL = 1>
 __device__ __forceinline__ void row_step(Acc& A, const double* in, const double* qb, const int* woff,
-                                         const StageCoef& C, const Sink& o, int k) {
+                                         const StageCoef& C, const Sink& o, int k, int g = 0) {
+  constexpr int NXT = NX * CL;
   constexpr int U0 = (PH + 2) % 3, U1 = PH, U2 = (PH + 1) % 3;  // u, p: rows k-1, k, k+1
   constexpr int V0 = (PH + 1) % 3, V1 = (PH + 2) % 3, V2 = PH;  // v: rows k-2 (-> k+1), k-1, k
   double w[12], d1[4];
   // ---- v row k: x stencil of row k; completes v(k-2); births v(k+1); u_y-mixed / p_y terms
-  ld_chunks<6>(w, in + NX, woff);
+  ld_chunks<6>(w, in + FS, woff);
   // v: cxv equals cxp off the centre; the +-2 taps are plain advection
   xstencil(A.v[V2], d1, w, C.cxv[3], C.cxp[1], C.cxp[5], C);
 #pragma unroll
   for (int c = 0; c < 4; ++c) A.v[V0][c] = fma(C.dv2, w[c + 4], A.v[V0][c]);
   if constexpr (S < 2) {
-    st4(o.ring + ((PH + 1) % 3) * (3 * NX) + NX, woff + 2, A.v[V0]);
+    st_ring<NX, FS, CL>(o.ring + ((PH + 1) % 3) * (3 * FS) + FS, woff + 2, A.v[V0], g, o);
   } else {
-    if (k - 2 >= 0 && k - 2 < o.TY) st_out<PEERS>(o, o.g + o.n + (long long)(k - 2) * NX, A.v[V0]);
+    if (k - 2 >= 0 && k - 2 < o.TY) st_out<PEERS>(o, o.g + o.n + (long long)(k - 2) * NXT, A.v[V0]);
   }
   {
     double b[4];
-    if constexpr (S > 0) ld_own(b, qb + NX, woff + 2);
+    if constexpr (S > 0) ld_own(b, qb + FS, woff + 2);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       A.v[V0][c] = (S > 0) ? b[c] + A.h[c] : A.h[c];  // v(k+1) = q + dv2 v(k-1)
@@ -210,7 +263,7 @@ __device__ __forceinline__ void row_step(Acc& A, const double* in, const double*
     double bu[4], bp[4];
     if constexpr (S > 0) {
       ld_own(bu, qb, woff + 2);
-      ld_own(bp, qb + 2 * NX, woff + 2);
+      ld_own(bp, qb + 2 * FS, woff + 2);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -222,14 +275,14 @@ __device__ __forceinline__ void row_step(Acc& A, const double* in, const double*
     }
   }
   if constexpr (S < 2) {
-    double* r = o.ring + ((PH + 2) % 3) * (3 * NX);
-    st4(r, woff + 2, A.u[U0]);
-    st4(r + 2 * NX, woff + 2, A.p[U0]);
+    double* r = o.ring + ((PH + 2) % 3) * (3 * FS);
+    st_ring<NX, FS, CL>(r, woff + 2, A.u[U0], g, o);
+    st_ring<NX, FS, CL>(r + 2 * FS, woff + 2, A.p[U0], g, o);
   } else {
     if (k - 1 >= 0 && k - 1 < o.TY) {
-      double* g = o.g + (long long)(k - 1) * NX;
-      st_out<PEERS>(o, g, A.u[U0]);
-      st_out<PEERS>(o, g + 2 * o.n, A.p[U0]);
+      double* gp = o.g + (long long)(k - 1) * NXT;
+      st_out<PEERS>(o, gp, A.u[U0]);
+      st_out<PEERS>(o, gp + 2 * o.n, A.p[U0]);
     }
   }
   // ---- u row k: x stencil (advection + the symmetric x damping at +-2 and the centre);
@@ -243,7 +296,7 @@ __device__ __forceinline__ void row_step(Acc& A, const double* in, const double*
     t2[c] = C.cvu * d1[c];
   }
   // ---- p row k: x stencil; p_x for u(k), p_y for v(k-1), v(k+1)
-  ld_chunks<6>(w, in + 2 * NX, woff);
+  ld_chunks<6>(w, in + 2 * FS, woff);
   xstencil(A.p[U1], d1, w, C.cxp[3], C.cxp[1], C.cxp[5], C);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -256,8 +309,10 @@ __device__ __forceinline__ void row_step(Acc& A, const double* in, const double*
 
 struct Item {
   int y0, TY, b;
+  int col4;      // CL > 1: this CTA's first column / 4 in the cluster's row
   uint32_t seq;  // q rows this CTA issued before the item (ring slot / mbarrier phase base)
   const CUtensorMap* map;
+  const CUtensorMap* hmap;  // CL > 1: the 4-cell halo view of the same buffer
 };
 
 // q ring slot and mbarrier parity of segment row r (r >= -6)
@@ -270,15 +325,33 @@ __device__ __forceinline__ void issue(double* ring, uint64_t* full, const Item& 
   gy += (gy < 0) ? ny : 0;
   gy -= (gy >= ny) ? ny : 0;
   const uint32_t s = qslot(it.seq, r);
-  tma_row(it.map, ring + (size_t)s * K::SLOT, full + s, gy, it.b, K::ROW_BYTES);
+  if constexpr (K::CL == 1) {
+    tma_row(it.map, ring + (size_t)s * K::SLOT, full + s, gy, it.b, K::ROW_BYTES);
+  } else {  // per field: the CTA's NX cells, and the 4-cell halos on either side (periodic)
+    double* slot = ring + (size_t)s * K::SLOT;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + s)),
+                 "r"(K::ROW_BYTES)
+                 : "memory");
+    constexpr int C4 = K::NXT / 4;  // 4-cell columns of the whole row
+    const int lc = it.col4 == 0 ? C4 - 1 : it.col4 - 1;
+    const int rc = it.col4 + K::NX / 4 == C4 ? 0 : it.col4 + K::NX / 4;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double* row = slot + f * K::FS;
+      tma_box(it.map, row, full + s, it.col4, gy, f, it.b);
+      tma_box(it.hmap, row + K::HR, full + s, rc, gy, f, it.b);
+      tma_box(it.hmap, row + K::HL, full + s, lc, gy, f, it.b);
+    }
+  }
 }
 
 // One tick: the CTA barrier, the q row two ticks ahead, then stage S's row k = t - lag.
 template <class K, int I, bool PEERS>
 __device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const Item& it, const FusedParams& P,
-                                     int S, int t, const int* woff, const Sink& o, bool producer) {
+                                     int S, int t, const int* woff, const Sink& o, bool producer, int g) {
   constexpr int NX = K::NX;
-  bar_sync();
+  if constexpr (K::CL > 1) cluster_sync();  // the neighbours' halo stores of the last tick
+  else bar_sync();
   if (producer && t - 4 <= it.TY + 5) issue<K>(ring, full, it, P.ny, t - 4);
   double* q = ring;
   double* r1 = ring + K::NQ * K::SLOT;
@@ -289,26 +362,30 @@ __device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const
     if (k > it.TY + 5) return;
     const uint32_t s = qslot(it.seq, k);
     mbar_wait(full + s, qpar(it.seq, k));
-    row_step<NX, 0, I, PEERS>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k);
+    row_step<NX, 0, I, PEERS, K::FS, K::CL>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k, g);
   } else if (S == 1) {
     const int k = t - 9;
     if (k < -4 || k > it.TY + 3) return;
     const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
-    row_step<NX, 1, I, PEERS>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k);
+    row_step<NX, 1, I, PEERS, K::FS, K::CL>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k, g);
   } else {
     const int k = t - 12;
     if (k < -2 || k > it.TY + 1) return;
     const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
-    row_step<NX, 2, I, PEERS>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k);
+    row_step<NX, 2, I, PEERS, K::FS, K::CL>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k, g);
   }
 }
 
 template <class K, bool PEERS>
 __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
     const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_out,
-    const __grid_constant__ CUtensorMap map_tmp, double* out, double* tmp, long long ld_out, long long ld_tmp,
-    const __grid_constant__ FusedParams P, int nseg, int batch, int nsteps, int* sync) {
-  constexpr int NX = K::NX;
+    const __grid_constant__ CUtensorMap map_tmp, const __grid_constant__ CUtensorMap hmap_in,
+    const __grid_constant__ CUtensorMap hmap_out, const __grid_constant__ CUtensorMap hmap_tmp, double* out,
+    double* tmp, long long ld_out, long long ld_tmp, const __grid_constant__ FusedParams P, int nseg, int batch,
+    int nsteps, int* sync) {
+  constexpr int NX = K::NX, CL = K::CL;
+  // CL > 1: a cluster of CL CTAs marches each row, this CTA owns columns [crank NX, +NX)
+  const unsigned crank = CL > 1 ? cluster_rank() : 0u;
   extern __shared__ unsigned char smraw[];
   // 1024-byte aligned ring (offset arithmetic on smraw keeps the shared address space visible)
   double* ring = reinterpret_cast<double*>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
@@ -322,33 +399,47 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
   // warp-uniform stage index (through a shuffle, so the compiler knows it)
   const int S = __shfl_sync(0xffffffffu, tid / K::GS, 0);
   const int g = tid - S * K::GS;
-  // window chunk offsets: cols [4g - 4, 4g + 8) as 6 chunks, wrapped periodically
+  // window chunk offsets: cols [4g - 4, 4g + 8) as 6 chunks; one CTA per row: wrapped
+  // periodically; CL > 1: the outer chunks of the edge threads are the row's halos
   int woff[6];
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
     int c = 2 * g - 2 + j;
-    c += (c < 0) ? K::CH : 0;
-    c -= (c >= K::CH) ? K::CH : 0;
-    woff[j] = 2 * swz(c);
+    if constexpr (CL == 1) {
+      c += (c < 0) ? K::CH : 0;
+      c -= (c >= K::CH) ? K::CH : 0;
+      woff[j] = 2 * swz(c);
+    } else {
+      woff[j] = c < 0 ? K::HL + 2 * (c + 2) : (c >= K::CH ? K::HR + 2 * (c - K::CH) : 2 * swz(c));
+    }
   }
   const bool producer = (tid == 0);
   const int ny = P.ny;
-  const long long n = (long long)NX * ny;
+  const long long n = (long long)K::NXT * ny;
   const int per_step = nseg * batch;
   const long long total = (long long)per_step * nsteps;
   int* done = sync + 1;
   uint32_t seq = 0;
   double* ring_out = S == 0 ? ring + K::NQ * K::SLOT : ring + (K::NQ + K::N1) * K::SLOT;
   for (;;) {
-    __syncthreads();  // s_item of the previous item is no longer read; rings are free
-    if (tid == 0) s_item = atomicAdd(sync, 1);
-    __syncthreads();
+    if constexpr (CL == 1) {
+      __syncthreads();  // s_item of the previous item is no longer read; rings are free
+      if (tid == 0) s_item = atomicAdd(sync, 1);
+      __syncthreads();
+    } else {  // the cluster takes an item together: rank 0 draws it, every CTA gets a copy
+      cluster_sync();
+      if (tid == 0 && crank == 0) {
+        const int v = atomicAdd(sync, 1);
+        for (int r = 0; r < CL; ++r) *peer_smem(&s_item, (unsigned)r) = v;
+      }
+      cluster_sync();
+    }
     const int item = s_item;
     if (item >= total) break;
     const int s = item / per_step;
     const int rem = item - s * per_step;
     const int b = rem / nseg, j = rem - b * nseg;
-    if (s > 0 && tid < 3) {  // the three neighbouring segments finished step s-1
+    if (s > 0 && tid < 3 && crank == 0) {  // the three neighbouring segments finished step s-1
       int jj = j + tid - 1;
       jj += (jj < 0) ? nseg : 0;
       jj -= (jj >= nseg) ? nseg : 0;
@@ -359,7 +450,8 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
         if (++spins > (1LL << 26)) __trap();  // a broken dependency fails, never hangs
       }
     }
-    __syncthreads();
+    if constexpr (CL == 1) __syncthreads();
+    else cluster_sync();
     // the neighbours' generic-proxy stores (seen through the acquire) before this CTA's TMA reads
     if (producer) asm volatile("fence.proxy.async.global;" ::: "memory");
     // ping-pong so that the last step lands in out
@@ -370,7 +462,11 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
     it.b = b;
     it.seq = seq;
     it.map = s == 0 ? &map_in : (to_out ? &map_tmp : &map_out);
+    it.hmap = s == 0 ? &hmap_in : (to_out ? &hmap_tmp : &hmap_out);
+    it.col4 = (int)crank * (NX / 4);
     Sink o;
+    o.left = (crank + CL - 1) % CL;
+    o.right = (crank + 1) % CL;
     o.ring = ring_out;
     o.n = n;
     o.TY = it.TY;
@@ -378,7 +474,8 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
       o.npeer = (s == nsteps - 1) ? P.npeer : 0;  // peers get the final state only
       o.peer_delta = P.peer_delta;
     }
-    o.g = (to_out ? out + (long long)b * ld_out : tmp + (long long)b * ld_tmp) + (long long)it.y0 * NX + 4 * g;
+    o.g = (to_out ? out + (long long)b * ld_out : tmp + (long long)b * ld_tmp) + (long long)it.y0 * K::NXT +
+          (long long)crank * NX + 4 * g;
     if (producer) {  // prologue: q rows -6 and -5 (stage 1's ticks 0 and 1)
       issue<K>(ring, full, it, ny, -6);
       issue<K>(ring, full, it, ny, -5);
@@ -393,16 +490,18 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
     // tick count rounded up to the unroll (equal barrier counts for every warp)
     const int nt = (it.TY + 14 + 2) / 3 * 3;
     for (int t = 0; t < nt; t += 3) {
-      tick<K, 0, PEERS>(A, ring, full, it, P, S, t, woff, o, producer);
-      tick<K, 1, PEERS>(A, ring, full, it, P, S, t + 1, woff, o, producer);
-      tick<K, 2, PEERS>(A, ring, full, it, P, S, t + 2, woff, o, producer);
+      tick<K, 0, PEERS>(A, ring, full, it, P, S, t, woff, o, producer, g);
+      tick<K, 1, PEERS>(A, ring, full, it, P, S, t + 1, woff, o, producer, g);
+      tick<K, 2, PEERS>(A, ring, full, it, P, S, t + 2, woff, o, producer, g);
     }
     seq += (uint32_t)(it.TY + 12);
     asm volatile("fence.proxy.async.global;" ::: "memory");  // stores before later TMA reads
     __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(done + b * nseg + j, s + 1);
+    if constexpr (CL == 1) __syncthreads();
+    else cluster_sync();  // every CTA of the cluster has stored its columns
+    if (tid == 0 && crank == 0) st_release(done + b * nseg + j, s + 1);
   }
+  if constexpr (CL > 1) cluster_sync();  // no CTA leaves while a neighbour may still store its halo
 }
 
 // ---------------------------------------------------------------- host side
@@ -425,16 +524,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// view {4, nx/4, ny, 3, batch} of a batch of states (ld doubles apart); box = one grid row
-// of the three fields, 32-byte swizzle
-CUtensorMap row_map(const double* base, int nx, int ny, long long ld, int batch) {
+// view {4, nx/4, ny, 3, batch} of a batch of states (ld doubles apart); box = {4, bx4, 1, bf, 1}
+// (one grid row of bx4 4-cell chunks of bf fields), 32-byte swizzle -- or none for the halo
+// boxes, which the edge threads read unswizzled
+CUtensorMap row_map(const double* base, int nx, int ny, long long ld, int batch, int bx4 = 0, int bf = 3,
+                    bool swizzle = true) {
   CUtensorMap m;
   const cuuint64_t dims[5] = {4, (cuuint64_t)nx / 4, (cuuint64_t)ny, 3, (cuuint64_t)batch};
   const cuuint64_t strides[4] = {32, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8, (cuuint64_t)ld * 8};
-  const cuuint32_t box[5] = {4, (cuuint32_t)nx / 4, 1, 3, 1};
+  const cuuint32_t box[5] = {4, (cuuint32_t)(bx4 > 0 ? bx4 : nx / 4), 1, (cuuint32_t)bf, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides,
-                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 swizzle ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PW_CHECK(r == CUDA_SUCCESS, PW_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
@@ -446,7 +548,8 @@ void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, do
                 long long d, int* sync) {
   auto kern = fp.npeer > 0 ? rk3_mtma_kernel<K, true> : rk3_mtma_kernel<K, false>;
   const int per_sm = kernel_setup(c, kern, K::NT, K::SMEM);
-  const long long slots = (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm;
+  // item slots: CTAs, or clusters of CL CTAs (one CTA per SM at NX = 512)
+  const long long slots = std::max<long long>(1, (long long)(c.num_sms > 0 ? c.num_sms : 148) * per_sm / K::CL);
   // segments per state: ticks per item (TY + 14) x max(1, items / CTA slots), clamped so
   // every segment has >= 16 rows (the 6-row halo of the neighbour dependency, and the
   // sync buffer's ny / 16 + 1 counters per state)
@@ -463,14 +566,32 @@ void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, do
     }
   }
   nseg = std::max(1, std::min(nseg, fp.ny / 16));
-  const CUtensorMap m_in = row_map(in, fp.nx, fp.ny, fp.ld_in, batch);
-  const CUtensorMap m_out = row_map(out, fp.nx, fp.ny, fp.ld_out, batch);
-  const CUtensorMap m_tmp = row_map(tmp, fp.nx, fp.ny, d, batch);
+  // CL = 1: one box per row (3 fields); CL > 1: per field, the CTA's NX columns, plus
+  // 4-cell halo boxes (no swizzle)
+  const int bx4 = K::NX / 4, bf = K::CL == 1 ? 3 : 1;
+  const CUtensorMap m_in = row_map(in, fp.nx, fp.ny, fp.ld_in, batch, bx4, bf);
+  const CUtensorMap m_out = row_map(out, fp.nx, fp.ny, fp.ld_out, batch, bx4, bf);
+  const CUtensorMap m_tmp = row_map(tmp, fp.nx, fp.ny, d, batch, bx4, bf);
+  const CUtensorMap h_in = K::CL > 1 ? row_map(in, fp.nx, fp.ny, fp.ld_in, batch, 1, 1, false) : m_in;
+  const CUtensorMap h_out = K::CL > 1 ? row_map(out, fp.nx, fp.ny, fp.ld_out, batch, 1, 1, false) : m_out;
+  const CUtensorMap h_tmp = K::CL > 1 ? row_map(tmp, fp.nx, fp.ny, d, batch, 1, 1, false) : m_tmp;
   const long long items = (long long)batch * nseg * nsteps;
-  const int grid = (int)std::min<long long>(slots, items);
+  const int grid = (int)std::min<long long>(slots, items) * K::CL;
   PW_CUDA(cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)batch * nseg), c.stream));
-  kern<<<grid, K::NT, K::SMEM, c.stream>>>(m_in, m_out, m_tmp, out, tmp, fp.ld_out, d, fp, nseg, batch, nsteps,
-                                           sync);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(K::NT);
+  cfg.dynamicSmemBytes = K::SMEM;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = K::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = K::CL > 1 ? 1 : 0;
+  PW_CUDA(cudaLaunchKernelEx(&cfg, kern, m_in, m_out, m_tmp, h_in, h_out, h_tmp, out, tmp, fp.ld_out, d, fp, nseg,
+                             batch, nsteps, sync));
   c.launches += 1;
   PW_LAUNCH_CHECK();
 }
@@ -481,7 +602,8 @@ bool mtma_enabled() { return env_int2("PW_MARCH_V2", 1) != 0; }
 
 bool mtma_supported(int nx, int ny, long long ld_in, long long ld_out, const void* in, const void* out,
                     const void* tmp) {
-  if (!(nx == 128 || nx == 256 || nx == 384 || nx == 512)) return false;
+  const bool cluster = (nx == 1024 || nx == 2048) && env_int2("PW_MARCH_CLUSTER2", 1) != 0;
+  if (!(nx == 128 || nx == 256 || nx == 384 || nx == 512 || cluster)) return false;
   if (ny < 32) return false;
   if ((ld_in & 1) || (ld_out & 1)) return false;
   return (((uintptr_t)in | (uintptr_t)out | (uintptr_t)tmp) & 15) == 0;
@@ -494,7 +616,10 @@ void launch_rk3_mtma(Ctx& c, const FusedParams& fp, const double* in, double* ou
     case 256: return launch_cfg<TK<256>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
     case 384: return launch_cfg<TK<384>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
     case 512: return launch_cfg<TK<512>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
-    default: throw Error{PW_ERR_VALUE, "TMA row march needs nx in {128, 256, 384, 512}"};
+    // wider rows: clusters of 512-column CTAs (halos by TMA for q, over DSMEM for s1 / s2)
+    case 1024: return launch_cfg<TK<512, 2>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 2048: return launch_cfg<TK<512, 4>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    default: throw Error{PW_ERR_VALUE, "TMA row march needs nx in {128, 256, 384, 512, 1024, 2048}"};
   }
 }
 

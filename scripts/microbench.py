@@ -77,6 +77,18 @@ def bench_fine_grid(n, batch):
     print(f"fine fused {n}^2 x {batch}: 4 steps {t*1e3:.3f} ms  -> {cu/1e9:.2f} G cell-updates/s")
 
 
+def bench_fine_wide():
+    """K1 on wide rows (clusters): c4 (1024^2 x 64) and c5 (2048^2 x 16), 20 steps per launch"""
+    for n, batch in ((1024, 64), (2048, 16)):
+        f, _ = specs(n)
+        x = torch.as_tensor(harness.fine_batch_states(n, batch, 7)).cuda()
+        y = torch.empty_like(x)
+        p = SlicePropagator(f, nsteps=20)
+        t = timeit(lambda: p.apply(x, out=y), reps=3)
+        cu = batch * n * n * 20 / t
+        print(f"fine {n}^2 x {batch}: 20 steps {t*1e3:.3f} ms  -> {cu/1e9:.2f} G cell-updates/s")
+
+
 def bench_coarse():
     _, c = specs(512)
     x = torch.as_tensor(harness.initial_state("c3")).cuda()[None, :].contiguous()
@@ -130,6 +142,8 @@ if __name__ == "__main__":
         bench_fine_grid(512, 64)
     if what in ("fine1024", "all"):
         bench_fine_grid(1024, 16)
+    if what in ("wide", "all"):
+        bench_fine_wide()
     if what in ("coarse", "all"):
         bench_coarse()
     if what in ("qr", "all"):

@@ -189,3 +189,36 @@ def test_tma_march_all_steps_vs_one_step_launches(dev, monkeypatch, nx, ny, batc
     old = SlicePropagator(spec, nsteps=nsteps).apply(x)
     err = ((got - old).norm(dim=1) / old.norm(dim=1)).max().item()
     assert err <= 1e-13, err
+
+
+@pytest.mark.parametrize("nx,ny,batch,nsteps", [
+    (1024, 48, 2, 3),     # cluster pairs (2 x 512 columns)
+    (1024, 100, 3, 4),    # ragged segments
+    (2048, 32, 1, 2),     # clusters of 4
+    (1024, 256, 4, 5),
+])
+def test_tma_march_clusters_match_oracle_and_tile_kernel(dev, monkeypatch, nx, ny, batch, nsteps):
+    """K1 on 1024- and 2048-wide rows: thread-block clusters of 512-column CTAs (q halos by
+    TMA, s1 / s2 halos over DSMEM, a cluster barrier per tick).  Against the oracle
+    (<= 1e-12), against one-step launches (bitwise: same rows, same arithmetic) and against
+    the tile kernel (PW_MARCH_CLUSTER2=0; different operation order, <= 1e-13)."""
+    from paper_1510_02237_b200.integrators import SlicePropagator
+
+    spec = fine_spec(nx, ny)
+    q0 = random_states(nx, ny, batch, nx + 3 * ny)
+    got = SlicePropagator(spec, nsteps=nsteps).batch(q0)
+    want = oracle_batch(q0, nsteps, nx, ny)
+    for b in range(batch):
+        assert rel(got[b], want[b]) <= 1e-12
+    x = torch.as_tensor(q0).cuda()
+    full = SlicePropagator(spec, nsteps=nsteps).apply(x)
+    one = SlicePropagator(spec, nsteps=1)
+    step = x
+    for _ in range(nsteps):
+        step = one.apply(step)
+    torch.cuda.synchronize()
+    assert torch.equal(full, step)
+    monkeypatch.setenv("PW_MARCH_CLUSTER2", "0")
+    tile = SlicePropagator(spec, nsteps=nsteps).apply(x)
+    err = ((full - tile).norm(dim=1) / tile.norm(dim=1)).max().item()
+    assert err <= 1e-13, err
