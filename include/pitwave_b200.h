@@ -195,6 +195,18 @@ int pw_ctx_set_row_shards(pw_ctx* ctx, int nshards);
  * NCCL is resolved at run time (libnccl.so.2 already in the process, e.g. torch's).
  * pw_comm_allreduce / pw_comm_allgather expose the transport (hooks or NCCL) directly:
  * allreduce = in-place sum of count doubles; allgather = as the hook above. */
+/* Row-sharded coarse propagator: ONE state whose grid rows live in
+ * nshard row shards, shard s holding rows [s R, (s+1) R) (R = ny / nshard) as u, v, p planes
+ * of R x nx in state_rows[s], with work_rows[s] (pw_rowshard_sizes: work doubles) and
+ * flags[s] (its return value: ints) of its own.  Applies the split FE-FB propagator (its
+ * nsteps) to the sharded state in place: every tile waits only on its 8 neighbours'
+ * phase counters, and tiles on a shard edge read their halo rows from the neighbouring
+ * shard's buffers -- the halo exchange of a row-sharded G, here with every shard's tiles in
+ * one launch on one device.  Bitwise equal to pw_prop_apply (integrators.py:103-106).
+ * nx % 32 == 0, ny % nshard == 0, nshard <= 8. */
+int pw_prop_apply_rowshard(pw_prop* prop, int nshard, double* const* state_rows, double* const* work_rows,
+                           int* const* flags);
+long long pw_rowshard_sizes(pw_prop* prop, int nshard, long long* work_doubles);
 int pw_nccl_unique_id(unsigned char* id128);
 int pw_ctx_set_nccl(pw_ctx* ctx, const unsigned char* id128, int rank, int world);
 int pw_comm_allreduce(pw_ctx* ctx, double* data, long long count);

@@ -94,6 +94,9 @@ SIGNATURES = [
     ("pw_ctx_set_comm", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ALLREDUCE_HOOK, ALLGATHER_HOOK,
                                        c_vp]),
     ("pw_ctx_set_row_shards", ctypes.c_int, [c_vp, ctypes.c_int]),
+    ("pw_prop_apply_rowshard", ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                              ctypes.POINTER(c_vp)]),
+    ("pw_rowshard_sizes", ctypes.c_longlong, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)]),
     ("pw_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
     ("pw_ctx_set_nccl", ctypes.c_int, [c_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
     ("pw_comm_allreduce", ctypes.c_int, [c_vp, c_vp, ctypes.c_longlong]),

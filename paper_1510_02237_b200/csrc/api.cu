@@ -932,6 +932,27 @@ int pw_ctx_set_comm(pw_ctx* ctx, int rank, int world, pw_allreduce_hook allreduc
   });
 }
 
+int pw_prop_apply_rowshard(pw_prop* prop, int nshard, double* const* state_rows, double* const* work_rows,
+                           int* const* flags) {
+  return guarded([&] {
+    PW_CHECK(prop && state_rows && work_rows && flags, PW_ERR_VALUE, "bad argument");
+    PW_CHECK(prop->kind == 0 && prop->desc.scheme == PW_SCHEME_SPLIT_FE_FB, PW_ERR_VALUE,
+             "row-sharded apply is the split FE-FB coarse propagator's");
+    for (int s = 0; s < nshard; ++s)
+      PW_CHECK(state_rows[s] && work_rows[s] && flags[s] && (((uintptr_t)state_rows[s] | (uintptr_t)work_rows[s]) & 15) == 0,
+               PW_ERR_VALUE, "row shard buffers must be non-NULL and 16-byte aligned");
+    const pw_pde_desc& D = prop->desc;
+    pw::launch_fefb_rowshard(prop->ctx->c, prop->ex, nshard, state_rows, work_rows, flags, D.nsteps, D.h,
+                             D.n_sound);
+  });
+}
+
+long long pw_rowshard_sizes(pw_prop* prop, int nshard, long long* work_doubles) {
+  if (!prop || nshard < 1) return -1;
+  if (work_doubles) *work_doubles = (long long)pw::rowshard_work_doubles(prop->ex, nshard);
+  return pw::rowshard_flag_ints(prop->ex, nshard);
+}
+
 int pw_nccl_unique_id(unsigned char* id128) {
   return guarded([&] {
     PW_CHECK(id128 != nullptr, PW_ERR_VALUE, "id buffer is NULL");

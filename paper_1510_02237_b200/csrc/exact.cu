@@ -640,6 +640,69 @@ struct NfCfg {
   static_assert(NSTR >= 1, "the region must be at most NT columns wide");
 };
 
+// Global storage of the neighbour-flag G.  Three plane families of (u, v, p): the state (0),
+// the ping-pong state (1) and the frozen tendencies (2).  FlatAcc: one state and one work
+// buffer (the production layout).  ShardAcc: the grid's rows split into row shards
+// [s R, (s+1) R), each shard with its own state, work and flag buffers -- the storage of a
+// row-sharded G, where a tile reads its halo rows from the neighbouring
+// shard's buffers and waits on that shard's flags.
+constexpr int kMaxRowShards = 8;
+struct NfShards {
+  double* st[kMaxRowShards];    // rows [s R, (s+1) R) of u, v, p (field stride R nx)
+  double* work[kMaxRowShards];  // au, av, ap, then the ping-pong u, v, p (field stride R nx)
+  int* flags[kMaxRowShards];    // phase counters of the shard's tiles
+  int rows;                     // R
+  int tiles;                    // tiles per shard (tile rows per shard x tiles_x)
+};
+struct FlatAcc {
+  double* st;
+  double* work;
+  int* fl;
+  long long n;
+  int nx;
+  __device__ __forceinline__ double* pl(int fam, int f, int gy) const {
+    double* b = fam == 0 ? st : work + (fam == 1 ? 3 : 0) * n;
+    return b + f * n + (long long)gy * nx;
+  }
+  __device__ __forceinline__ int* flag(int t) const { return fl + t; }
+};
+struct ShardAcc {
+  NfShards sh;
+  int nx;
+  __device__ __forceinline__ double* pl(int fam, int f, int gy) const {
+    const int s = gy / sh.rows;
+    const long long fs = (long long)sh.rows * nx;
+    double* b = fam == 0 ? sh.st[s] : sh.work[s] + (fam == 1 ? 3 : 0) * fs;
+    return b + f * fs + (long long)(gy - s * sh.rows) * nx;
+  }
+  __device__ __forceinline__ int* flag(int t) const {
+    const int s = t / sh.tiles;
+    return sh.flags[s] + (t - s * sh.tiles);
+  }
+};
+
+// adv_at with the field's rows through an accessor (same expressions, same order)
+template <int ORD, class R>
+__device__ __forceinline__ double adv_at_rows(const ExactParams& p, const R& row, int j, int i) {
+  const int order = ORD > 0 ? ORD : p.order;
+  const int nx = p.nx, ny = p.ny;
+  const int ip = i + 1 < nx ? i + 1 : 0;
+  const int jp = j + 1 < ny ? j + 1 : 0;
+  auto fx = [&](int jj, int f) {
+    const double* r = row(jj);
+    return face_flux(order, p.uf[(size_t)jj * nx + f], r[wrapi(f - 3, nx)], r[wrapi(f - 2, nx)],
+                     r[wrapi(f - 1, nx)], r[f], r[wrapi(f + 1, nx)], r[wrapi(f + 2, nx)]);
+  };
+  auto gyf = [&](int f, int ii) {
+    return face_flux(order, p.vf[(size_t)f * nx + ii], row(wrapi(f - 3, ny))[ii], row(wrapi(f - 2, ny))[ii],
+                     row(wrapi(f - 1, ny))[ii], row(f)[ii], row(wrapi(f + 1, ny))[ii], row(wrapi(f + 2, ny))[ii]);
+  };
+  const double fxi = fx(j, i), fxp = fx(j, ip);
+  const double gyj = gyf(j, i), gyp = gyf(jp, i);
+  const double tx = -(fxp - fxi), ty = (gyp - gyj);
+  return (p.inv_dx != 0.0 ? tx * p.inv_dx : tx / p.dx) - (p.inv_dy != 0.0 ? ty * p.inv_dy : ty / p.dy);
+}
+
 __device__ __forceinline__ int nf_ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -650,14 +713,15 @@ __device__ __forceinline__ void nf_st_release(int* p, int v) {
 }
 
 // wait until the 8 neighbours of tile (ix, iy) have completed phase `ph`
-__device__ __forceinline__ void nf_wait(const int* flags, int ix, int iy, int tiles_x, int tiles_y, int ph) {
+template <class A>
+__device__ __forceinline__ void nf_wait(const A& acc, int ix, int iy, int tiles_x, int tiles_y, int ph) {
   if (ph > 0 && threadIdx.x < 9 && threadIdx.x != 4) {
     int jx = ix + (int)threadIdx.x % 3 - 1, jy = iy + (int)threadIdx.x / 3 - 1;
     jx += jx < 0 ? tiles_x : 0;
     jx -= jx >= tiles_x ? tiles_x : 0;
     jy += jy < 0 ? tiles_y : 0;
     jy -= jy >= tiles_y ? tiles_y : 0;
-    const int* f = flags + jy * tiles_x + jx;
+    const int* f = acc.flag(jy * tiles_x + jx);
     long long spins = 0;
     while (nf_ld_acquire(f) < ph) {
       __nanosleep(32);
@@ -668,18 +732,18 @@ __device__ __forceinline__ void nf_wait(const int* flags, int ix, int iy, int ti
 }
 // the CTA barrier orders every thread's stores before thread 0's fence (cumulative) and
 // release, as cooperative groups' grid barrier does
-__device__ __forceinline__ void nf_signal(int* flags, int tile, int ph) {
+template <class A>
+__device__ __forceinline__ void nf_signal(const A& acc, int tile, int ph) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    nf_st_release(flags + tile, ph);
+    nf_st_release(acc.flag(tile), ph);
   }
 }
 
-template <int TMY, int K, int NT, int ORD, int MINB = 1>
-__global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactParams p, int nsteps, double tau,
-                                                       int nsub, double* work, int tiles_x, int tiles_y,
-                                                       int* flags) {
+template <int TMY, int K, int NT, int ORD, class ACC>
+__device__ __forceinline__ void fefb_nf_body(const ACC& acc, ExactParams p, int nsteps, double tau, int nsub,
+                                             int tiles_x, int tiles_y, int tile_lo, int tile_hi) {
   using C = NfCfg<TMY, K, NT>;
   constexpr int TX = C::TX, H = C::H, HX = C::HX, RX = C::RX, PL = C::PL, S = C::S;
   extern __shared__ double sm[];
@@ -687,11 +751,7 @@ __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactPara
   const long long n = (long long)nx * ny;
   const double sx = 0.5 / p.dx, sy = 0.5 / p.dy, cs = p.cs, a1 = p.a1, a2 = p.a2;
   const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
-  double* au = work;
-  double* av = work + n;
-  double* ap = work + 2 * n;
-  double* ws = work + 3 * n;  // ping-pong state (u, v, p planes)
-  const int tiles = tiles_x * tiles_y;
+  (void)n;
   const int tid = threadIdx.x;
   const int cx = tid % RX, strip = tid / RX;  // this thread's column and strip of the region
   const bool comp = strip < C::NSTR;
@@ -700,32 +760,30 @@ __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactPara
   int ph = 0;
   for (int step = 0; step < nsteps; ++step) {
     // ---- phase A: frozen advective tendency of the tile's cells (physics.py:67-74)
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
       const int iy = t / tiles_x, ix = t - iy * tiles_x;
       const int ty0 = (int)((long long)iy * ny / tiles_y), ty1 = (int)((long long)(iy + 1) * ny / tiles_y);
-      nf_wait(flags, ix, iy, tiles_x, tiles_y, ph);
+      nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
       for (int c = tid; c < TX * (ty1 - ty0); c += NT) {
         const int j = ty0 + c / TX, i = ix * TX + c % TX;
-        const long long cell = (long long)j * nx + i;
-        au[cell] = adv_at<ORD>(p, st, j, i);
-        av[cell] = adv_at<ORD>(p, st + n, j, i);
-        ap[cell] = adv_at<ORD>(p, st + 2 * n, j, i);
+#pragma unroll
+        for (int f = 0; f < 3; ++f)
+          acc.pl(2, f, j)[i] = adv_at_rows<ORD>(p, [&](int r) -> const double* { return acc.pl(0, f, r); }, j, i);
       }
-      nf_signal(flags, t, ph + 1);
+      nf_signal(acc, t, ph + 1);
     }
     ++ph;
     // ---- substep blocks
     for (int blk = 0; blk < nblk; ++blk) {
       const int ks = min(K, nsub - blk * K);
-      const double* src = (blk % 2 == 0) ? st : ws;
-      double* dst = (blk % 2 == 0) ? ws : st;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int fsrc = (blk % 2 == 0) ? 0 : 1, fdst = 1 - fsrc;  // state <-> ping-pong planes
+      for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
         const int iy = t / tiles_x, ix = t - iy * tiles_x;
         const int tx0 = ix * TX;
         const int ty0 = (int)((long long)iy * ny / tiles_y);
         const int TY = (int)((long long)(iy + 1) * ny / tiles_y) - ty0;
         const int RY = TY + 2 * H;
-        nf_wait(flags, ix, iy, tiles_x, tiles_y, ph);
+        nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
         double* su = sm + RX;  // row 0 of the region (one padding row above)
         double* sv = su + PL;
         double* sp = sv + PL;
@@ -741,12 +799,12 @@ __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactPara
           gx -= gx >= nx ? nx : 0;
           gy += gy < 0 ? ny : 0;
           gy -= gy >= ny ? ny : 0;
-          const long long cell = (long long)gy * nx + gx;
           const int o = y * RX + x;
 #pragma unroll
           for (int f = 0; f < 3; ++f) {
             const unsigned sa = (unsigned)__cvta_generic_to_shared(su + f * PL + o);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + f * n + cell) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(acc.pl(fsrc, f, gy) + gx)
+                         : "memory");
           }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -759,15 +817,13 @@ __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactPara
           int gy = ty0 - H + y0s;
           gy += gy < 0 ? ny : 0;
           gy -= gy >= ny ? ny : 0;
-          const double* qa = au + (long long)gy * nx + gx;
 #pragma unroll
           for (int r = 0; r < S; ++r) {
-            tu[r] = __ldcg(qa);
-            tv[r] = __ldcg(qa + n);
-            tp[r] = __ldcg(qa + 2 * n);
+            tu[r] = __ldcg(acc.pl(2, 0, gy) + gx);
+            tv[r] = __ldcg(acc.pl(2, 1, gy) + gx);
+            tp[r] = __ldcg(acc.pl(2, 2, gy) + gx);
             // next row, wrapping at the bottom edge (rows past the region: any valid row)
-            qa += (++gy < ny) ? nx : -(long long)(ny - 1) * nx;
-            if (gy >= ny) gy = 0;
+            if (++gy >= ny) gy = 0;
           }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -845,31 +901,47 @@ __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactPara
         for (int c = tid; c < TX * TY; c += NT) {
           const int ly = c / TX, lx = c - ly * TX;
           const int o = (ly + H) * RX + lx + HX;
-          const long long cell = (long long)(ty0 + ly) * nx + tx0 + lx;
-          dst[cell] = su[o];
-          dst[n + cell] = sv[o];
-          dst[2 * n + cell] = sp[o];
+          const int gy = ty0 + ly, gx = tx0 + lx;
+          acc.pl(fdst, 0, gy)[gx] = su[o];
+          acc.pl(fdst, 1, gy)[gx] = sv[o];
+          acc.pl(fdst, 2, gy)[gx] = sp[o];
         }
-        nf_signal(flags, t, ph + 1);
+        nf_signal(acc, t, ph + 1);
       }
       ++ph;
     }
     if (nblk % 2 == 1) {  // the last block wrote ws: copy the tiles back (WAR on st: a phase)
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
         const int iy = t / tiles_x, ix = t - iy * tiles_x;
         const int ty0 = (int)((long long)iy * ny / tiles_y), ty1 = (int)((long long)(iy + 1) * ny / tiles_y);
-        nf_wait(flags, ix, iy, tiles_x, tiles_y, ph);
+        nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
         for (int c = tid; c < TX * (ty1 - ty0); c += NT) {
-          const long long cell = (long long)(ty0 + c / TX) * nx + ix * TX + c % TX;
-          st[cell] = ws[cell];
-          st[n + cell] = ws[n + cell];
-          st[2 * n + cell] = ws[2 * n + cell];
+          const int gy = ty0 + c / TX, gx = ix * TX + c % TX;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) acc.pl(0, f, gy)[gx] = acc.pl(1, f, gy)[gx];
         }
-        nf_signal(flags, t, ph + 1);
+        nf_signal(acc, t, ph + 1);
       }
       ++ph;
     }
   }
+}
+
+template <int TMY, int K, int NT, int ORD, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactParams p, int nsteps, double tau,
+                                                       int nsub, double* work, int tiles_x, int tiles_y,
+                                                       int* flags) {
+  const FlatAcc acc{st, work, flags, (long long)p.nx * p.ny, p.nx};
+  fefb_nf_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, 0, tiles_x * tiles_y);
+}
+
+// The row-sharded form (tiles [tile_lo, tile_hi) of a grid whose rows live in row shards).
+template <int TMY, int K, int NT, int ORD>
+__global__ void __launch_bounds__(NT, 1) fefb_nf_shard_kernel(NfShards sh, ExactParams p, int nsteps, double tau,
+                                                              int nsub, int tiles_x, int tiles_y, int tile_lo,
+                                                              int tile_hi) {
+  const ShardAcc acc{sh, p.nx};
+  fefb_nf_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, tile_lo, tile_hi);
 }
 
 template <int TMX, int TMY, int K>
@@ -995,6 +1067,46 @@ static bool launch_nf(Ctx& c, const ExactParams& p, double* states, int nsteps, 
 static int nf_variant() {
   const char* e = getenv("PW_COARSE_NF");  // 0: the grid-barrier kernels; 2 / 3 / 4: substeps per phase
   return (e && *e) ? atoi(e) : 3;
+}
+
+// Row-sharded G: one state whose rows live in nsh row shards, shard s holding
+// rows [s R, (s+1) R) in its own state / work / flag buffers.  All shards' tiles run in this one
+// launch; tile rows are aligned to the shard boundaries (tiles_y a multiple of nsh).  Same
+// arithmetic as launch_nf<60, 3, 512> -- bitwise equal to the replicated G.
+size_t rowshard_work_doubles(const ExactParams& p, int nsh) { return (size_t)6 * p.nx * (p.ny / nsh); }
+int rowshard_flag_ints(const ExactParams& p, int nsh) {
+  const int tiles_y = ((p.ny + 59) / 60 + nsh - 1) / nsh * nsh;
+  return (p.nx / 32) * tiles_y / nsh;
+}
+void launch_fefb_rowshard(Ctx& c, const ExactParams& p, int nsh, double* const* st, double* const* work,
+                          int* const* flags, int nsteps, double h, int nsub) {
+  PW_CHECK(nsh >= 1 && nsh <= kMaxRowShards, PW_ERR_VALUE, "row shards: 1..8");
+  PW_CHECK(p.nx % 32 == 0 && p.ny % nsh == 0, PW_ERR_VALUE, "row shards need nx % 32 == 0 and ny % nshard == 0");
+  constexpr int TMY = 60, K = 3, NT = 512;
+  using C = NfCfg<TMY, K, NT>;
+  const bool o1 = p.order == 1;
+  auto kern = o1 ? fefb_nf_shard_kernel<TMY, K, NT, 1> : fefb_nf_shard_kernel<TMY, K, NT, 0>;
+  const int per_sm = kernel_setup(c, kern, NT, C::SMEM);
+  const int tiles_x = p.nx / 32;
+  const int tiles_y = ((p.ny + TMY - 1) / TMY + nsh - 1) / nsh * nsh;  // shard-aligned tile rows
+  PW_CHECK(p.ny / tiles_y >= 3 * K, PW_ERR_VALUE, "row shards: tiles too short for the 9-row halo");
+  NfShards sh{};
+  sh.rows = p.ny / nsh;
+  sh.tiles = tiles_x * tiles_y / nsh;
+  for (int s = 0; s < nsh; ++s) {
+    sh.st[s] = st[s];
+    sh.work[s] = work[s];
+    sh.flags[s] = flags[s];
+    PW_CUDA(cudaMemsetAsync(flags[s], 0, sizeof(int) * (size_t)sh.tiles, c.stream));
+  }
+  const int tiles = tiles_x * tiles_y;
+  const int grid = std::min(tiles, c.num_sms * per_sm);
+  double tau = h / nsub;
+  ExactParams pp = p;
+  int tx = tiles_x, ty = tiles_y, lo = 0, hi = tiles;
+  void* args[] = {&sh, &pp, &nsteps, &tau, &nsub, &tx, &ty, &lo, &hi};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, C::SMEM, c.stream));
+  c.launches += 1;
 }
 
 void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, long long ld,

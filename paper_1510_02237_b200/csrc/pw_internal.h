@@ -172,6 +172,11 @@ size_t split_rk3_fb_work_doubles(const ExactParams& p, int batch);
 void launch_split_rk3_fb(Ctx& c, const ExactParams& p, double nu, double* states, int batch,
                          long long ld, int nsteps, double dt, int n_sound, double* work);
 size_t fefb_exact_work_doubles(const ExactParams& p, int batch);
+// row-sharded G (one state in nsh row shards, every shard's tiles in one launch)
+size_t rowshard_work_doubles(const ExactParams& p, int nsh);
+int rowshard_flag_ints(const ExactParams& p, int nsh);
+void launch_fefb_rowshard(Ctx& c, const ExactParams& p, int nsh, double* const* st, double* const* work,
+                          int* const* flags, int nsteps, double h, int nsub);
 
 // fine_fused.cu
 void make_fused_params(FusedParams& fp, int nx, int ny, double dx, double dy, double cs,

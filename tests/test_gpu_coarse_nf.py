@@ -7,7 +7,8 @@ the reference's operation order (-fmad=false), so every case is BITWISE equal to
 per-cell strict kernel -- for each substep blocking (PW_COARSE_NF = 2, 3, 4 substeps per
 phase), square and non-square grids, ragged tile heights, tiles per CTA > 1 (1024^2,
 2048^2), an odd block count (copy-back phase), several steps per call, flux orders 1
-and 3 (the generic-order instantiation), no damping, and upwind with U < 0.
+and 3 (the generic-order instantiation), no damping, and upwind with U < 0 -- and the
+row-sharded form (pw_prop_apply_rowshard) against the replicated G.
 """
 import numpy as np
 import pytest
@@ -83,4 +84,36 @@ def test_nf_coarse_cases_bitwise(dev, case):
     x = torch.as_tensor(harness.initial_state("c5" if case == "c5_grid" else "c3", n=nx)[None, :]).cuda() \
         if nx == ny else states(nx, ny, 3)
     got, want = run_both(dev, coarse(nx, ny, **kw), x, nsteps)
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("nx,ny,nshard", [(512, 512, 2), (512, 512, 4), (1024, 1024, 4), (256, 240, 3),
+                                          (512, 512, 8)])
+def test_rowsharded_coarse_bitwise_with_replicated(dev, nx, ny, nshard):
+    """Row-sharded G (pw_prop_apply_rowshard): the state's rows in nshard row
+    shards with their own state / work / flag buffers; tiles on a shard edge read their halo
+    rows from the neighbouring shard and wait on its flags.  Every shard's tiles run in one
+    launch on this one GPU (a multi-GPU run would launch each shard's tiles on its own device
+    with peer pointers).  Bitwise equal to the replicated G, two FE-FB steps."""
+    import ctypes
+
+    from paper_1510_02237_b200 import _lib
+    from paper_1510_02237_b200.integrators import SlicePropagator
+
+    prop = SlicePropagator(coarse(nx, ny), nsteps=2)
+    x = states(nx, ny, 7 + nshard)
+    want = prop.apply(x)
+    R = ny // nshard
+    full = x.view(3, ny, nx)
+    st = [full[:, s * R:(s + 1) * R, :].contiguous().reshape(-1) for s in range(nshard)]
+    wd = ctypes.c_longlong(0)
+    nflag = prop.ctx.lib.pw_rowshard_sizes(prop.handle, nshard, ctypes.byref(wd))
+    assert nflag > 0 and wd.value == 6 * R * nx
+    work = [torch.empty(wd.value, dtype=torch.float64, device="cuda") for _ in range(nshard)]
+    flags = [torch.zeros(nflag, dtype=torch.int32, device="cuda") for _ in range(nshard)]
+    arr = lambda ts: (_lib.c_vp * nshard)(*[_lib.c_vp(t.data_ptr()) for t in ts])  # noqa: E731
+    prop.ctx.bind_stream()
+    _lib.check(prop.ctx.lib.pw_prop_apply_rowshard(prop.handle, nshard, arr(st), arr(work), arr(flags)))
+    torch.cuda.synchronize()
+    got = torch.cat([b.view(3, R, nx) for b in st], dim=1).reshape(1, -1)
     assert torch.equal(got, want)
