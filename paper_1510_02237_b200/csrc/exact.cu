@@ -712,6 +712,12 @@ __device__ __forceinline__ void nf_st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef NF_SLEEP
+#define NF_SLEEP 1
+#endif
+#ifndef NF_FENCE
+#define NF_FENCE 1
+#endif
 // wait until the 8 neighbours of tile (ix, iy) have completed phase `ph`
 template <class A>
 __device__ __forceinline__ void nf_wait(const A& acc, int ix, int iy, int tiles_x, int tiles_y, int ph) {
@@ -724,8 +730,8 @@ __device__ __forceinline__ void nf_wait(const A& acc, int ix, int iy, int tiles_
     const int* f = acc.flag(jy * tiles_x + jx);
     long long spins = 0;
     while (nf_ld_acquire(f) < ph) {
-      __nanosleep(32);
-      if (++spins > (1LL << 26)) __trap();  // a broken dependency fails, never hangs
+      if (NF_SLEEP) __nanosleep(32);
+      if (++spins > (1LL << 28)) __trap();  // a broken dependency fails, never hangs
     }
   }
   __syncthreads();
@@ -736,7 +742,7 @@ template <class A>
 __device__ __forceinline__ void nf_signal(const A& acc, int tile, int ph) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (NF_FENCE) __threadfence();
     nf_st_release(acc.flag(tile), ph);
   }
 }
@@ -927,6 +933,493 @@ __device__ __forceinline__ void fefb_nf_body(const ACC& acc, ExactParams p, int 
   }
 }
 
+// ---- the same G with phase A folded into the first substep block of each step.
+// The first block stages the region with E more cells of margin (the flux stencil's reach:
+// 1 for the order-1 coarse flux, 3 otherwise) and computes the frozen advective tendencies
+// of every region cell within the 3K margin from shared memory (adv_at's expressions and
+// order, bitwise), so no phase of its own is needed and no tendency halo is exchanged.
+// When each CTA owns one tile the tendencies stay in registers for the whole step;
+// otherwise the tile's own cells are written to the tendency planes and later blocks read
+// them (neighbours' halo included) back, as the phase-A form does.
+template <int TMY, int K, int NT, int E>
+struct NfmCfg {
+  static constexpr int TX = 32, H = 3 * K, HE = H + E, HX = (HE + 1) / 2 * 2, RX = TX + 2 * HX, RYM = TMY + 2 * HE;
+  static constexpr int NSTR = NT / RX;
+  static constexpr int S = (RYM + NSTR - 1) / NSTR;
+  static constexpr int PL = RX * (NSTR * S + 2);
+  static constexpr size_t SMEM = sizeof(double) * 6 * PL;
+  static_assert(NSTR >= 1, "the region must be at most NT columns wide");
+};
+template <int ORD>
+__host__ __device__ constexpr int nfm_reach() { return ORD == 1 ? 1 : 3; }
+
+// adv_at (flux_divergence of flux_x / flux_y) of region cell (x, y) from a staged plane;
+// gx, gy: the cell's global column and row
+template <int ORD, int RX>
+__device__ __forceinline__ double adv_smem(const ExactParams& p, const double* pl, int x, int y, int gx, int gy) {
+  const int order = ORD > 0 ? ORD : p.order;
+  const int nx = p.nx, ny = p.ny;
+  const int gxp = gx + 1 < nx ? gx + 1 : 0;
+  const int gyp = gy + 1 < ny ? gy + 1 : 0;
+  const double* r = pl + y * RX;
+  auto fx = [&](int f, int gf) {  // face between region cells f-1 | f of row y
+    return face_flux(order, __ldg(p.uf + (size_t)gy * nx + gf), r[f - 3], r[f - 2], r[f - 1], r[f], r[f + 1], r[f + 2]);
+  };
+  auto gyf = [&](int f, int gf) {  // face between region rows f-1 | f of column x
+    const double* c = pl + x;
+    return face_flux(order, __ldg(p.vf + (size_t)gf * nx + gx), c[(f - 3) * RX], c[(f - 2) * RX], c[(f - 1) * RX],
+                     c[f * RX], c[(f + 1) * RX], c[(f + 2) * RX]);
+  };
+  const double fxi = fx(x, gx), fxp = fx(x + 1, gxp);
+  const double gyj = gyf(y, gy), gyq = gyf(y + 1, gyp);
+  const double tx = -(fxp - fxi), ty = (gyq - gyj);
+  return (p.inv_dx != 0.0 ? tx * p.inv_dx : tx / p.dx) - (p.inv_dy != 0.0 ? ty * p.inv_dy : ty / p.dy);
+}
+
+template <int TMY, int K, int NT, int ORD, class ACC>
+__device__ __forceinline__ void fefb_nfm_body(const ACC& acc, ExactParams p, int nsteps, double tau, int nsub,
+                                              int tiles_x, int tiles_y, int tile_lo, int tile_hi) {
+  using C = NfmCfg<TMY, K, NT, nfm_reach<ORD>()>;
+  constexpr int TX = C::TX, H = C::H, HE = C::HE, HX = C::HX, RX = C::RX, PL = C::PL, S = C::S;
+  extern __shared__ double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const double sx = 0.5 / p.dx, sy = 0.5 / p.dy, cs = p.cs, a1 = p.a1, a2 = p.a2;
+  const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
+  const int tid = threadIdx.x;
+  const int cx = tid % RX, strip = tid / RX;  // this thread's column and strip of the region
+  const bool comp = strip < C::NSTR;
+  const int y0s = strip * S;
+  const int nblk = (nsub + K - 1) / K;
+  const bool resident = tile_hi - tile_lo <= (int)gridDim.x;  // one tile per CTA: tendencies stay in registers
+  double tu[S], tv[S], tp[S];
+  int ph = 0;
+  for (int step = 0; step < nsteps; ++step) {
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int ks = min(K, nsub - blk * K);
+      const int fsrc = (blk % 2 == 0) ? 0 : 1, fdst = 1 - fsrc;  // state <-> ping-pong planes
+      for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int tx0 = ix * TX;
+        const int ty0 = (int)((long long)iy * ny / tiles_y);
+        const int TY = (int)((long long)(iy + 1) * ny / tiles_y) - ty0;
+        const int RY = TY + 2 * HE;
+        nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
+        double* su = sm + RX;  // row 0 of the region (one padding row above)
+        double* sv = su + PL;
+        double* sp = sv + PL;
+        double* sd = sp + PL;
+        double* sun = sd + PL;
+        double* svn = sun + PL;
+        for (int c = tid; c < (RX / 2) * RY; c += NT) {
+          const int y = c / (RX / 2), x = 2 * (c - y * (RX / 2));
+          int gx = tx0 - HX + x, gy = ty0 - HE + y;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          gy += gy < 0 ? ny : 0;
+          gy -= gy >= ny ? ny : 0;
+          const int o = y * RX + x;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(su + f * PL + o);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(acc.pl(fsrc, f, gy) + gx)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (blk > 0 && !resident && comp) {  // tendencies of this tile's region (own + neighbours')
+          int gx = tx0 - HX + cx;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          int gy = ty0 - HE + y0s;
+          gy += gy < 0 ? ny : 0;
+          gy -= gy >= ny ? ny : 0;
+#pragma unroll
+          for (int r = 0; r < S; ++r) {
+            tu[r] = __ldcg(acc.pl(2, 0, gy) + gx);
+            tv[r] = __ldcg(acc.pl(2, 1, gy) + gx);
+            tp[r] = __ldcg(acc.pl(2, 2, gy) + gx);
+            if (++gy >= ny) gy = 0;
+          }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (blk == 0 && comp) {  // frozen advective tendencies (physics.py:67-74) on margin H
+          int gx = tx0 - HX + cx;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          const bool colin = cx >= HX - H && cx < HX + TX + H;
+          const bool own_x = cx >= HX && cx < HX + TX;
+#pragma unroll
+          for (int r = 0; r < S; ++r) {
+            const int y = y0s + r;
+            if (colin && y >= HE - H && y < HE + TY + H) {
+              int gy = ty0 - HE + y;
+              gy += gy < 0 ? ny : 0;
+              gy -= gy >= ny ? ny : 0;
+              tu[r] = adv_smem<ORD, RX>(p, su, cx, y, gx, gy);
+              tv[r] = adv_smem<ORD, RX>(p, sv, cx, y, gx, gy);
+              tp[r] = adv_smem<ORD, RX>(p, sp, cx, y, gx, gy);
+              if (!resident && own_x && y >= HE && y < HE + TY) {
+                acc.pl(2, 0, gy)[gx] = tu[r];
+                acc.pl(2, 1, gy)[gx] = tv[r];
+                acc.pl(2, 2, gy)[gx] = tp[r];
+              }
+            } else {
+              tu[r] = tv[r] = tp[r] = 0.0;
+            }
+          }
+        }
+        for (int ss = 0; ss < ks; ++ss) {
+          const int M = H - 3 * ss;  // (u, v, p) valid on margin M of the tile
+          // D = dx(u) + dy(v) on margin M - 1 (damping_tendencies' div, numba_backend.py:108-111)
+          if (damp && comp && cx >= HX - (M - 1) && cx < HX + TX + (M - 1) &&
+              y0s + S > HE - (M - 1) && y0s < HE + TY + (M - 1)) {
+            double dd[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = (y0s + r) * RX + cx;
+              dd[r] = (su[o + 1] - su[o - 1]) * sx + (sv[o + RX] - sv[o - RX]) * sy;
+            }
+            const int lo = HE - (M - 1) - y0s, hi = HE + TY + (M - 1) - y0s;
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+              if (r >= lo && r < hi) sd[(y0s + r) * RX + cx] = dd[r];
+          }
+          __syncthreads();
+          // u', v' on margin M - 2 (fb_substeps, numba_backend.py:137-143)
+          if (comp && cx >= HX - (M - 2) && cx < HX + TX + (M - 2) &&
+              y0s + S > HE - (M - 2) && y0s < HE + TY + (M - 2)) {
+            double nu_[S], nv_[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = (y0s + r) * RX + cx;
+              double du = tu[r] - cs * ((sp[o + 1] - sp[o - 1]) * sx);
+              double dv = tv[r] - cs * ((sp[o + RX] - sp[o - RX]) * sy);
+              if (damp) {
+                du = du + a1 * ((sd[o + 1] - sd[o - 1]) * sx);
+                dv = dv + a2 * ((sd[o + RX] - sd[o - RX]) * sy);
+              }
+              nu_[r] = su[o] + tau * du;
+              nv_[r] = sv[o] + tau * dv;
+            }
+            const int lo = HE - (M - 2) - y0s, hi = HE + TY + (M - 2) - y0s;
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+              if (r >= lo && r < hi) {
+                sun[(y0s + r) * RX + cx] = nu_[r];
+                svn[(y0s + r) * RX + cx] = nv_[r];
+              }
+          }
+          __syncthreads();
+          // p' on margin M - 3 from the new velocities (numba_backend.py:144-145)
+          if (comp && cx >= HX - (M - 3) && cx < HX + TX + (M - 3) &&
+              y0s + S > HE - (M - 3) && y0s < HE + TY + (M - 3)) {
+            double np_[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = (y0s + r) * RX + cx;
+              const double divn = (sun[o + 1] - sun[o - 1]) * sx + (svn[o + RX] - svn[o - RX]) * sy;
+              np_[r] = sp[o] + tau * (tp[r] - cs * divn);
+            }
+            const int lo = HE - (M - 3) - y0s, hi = HE + TY + (M - 3) - y0s;
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+              if (r >= lo && r < hi) sp[(y0s + r) * RX + cx] = np_[r];
+          }
+          __syncthreads();
+          double* tt = su;
+          su = sun;
+          sun = tt;
+          tt = sv;
+          sv = svn;
+          svn = tt;
+        }
+        for (int c = tid; c < TX * TY; c += NT) {
+          const int ly = c / TX, lx = c - ly * TX;
+          const int o = (ly + HE) * RX + lx + HX;
+          const int gy = ty0 + ly, gx = tx0 + lx;
+          acc.pl(fdst, 0, gy)[gx] = su[o];
+          acc.pl(fdst, 1, gy)[gx] = sv[o];
+          acc.pl(fdst, 2, gy)[gx] = sp[o];
+        }
+        nf_signal(acc, t, ph + 1);
+      }
+      ++ph;
+    }
+    if (nblk % 2 == 1) {  // the last block wrote ws: copy the tiles back (WAR on st: a phase)
+      for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int ty0 = (int)((long long)iy * ny / tiles_y), ty1 = (int)((long long)(iy + 1) * ny / tiles_y);
+        nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
+        for (int c = tid; c < TX * (ty1 - ty0); c += NT) {
+          const int gy = ty0 + c / TX, gx = ix * TX + c % TX;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) acc.pl(0, f, gy)[gx] = acc.pl(1, f, gy)[gx];
+        }
+        nf_signal(acc, t, ph + 1);
+      }
+      ++ph;
+    }
+  }
+}
+
+template <int TMY, int K, int NT, int ORD, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) fefb_nfm_kernel(double* st, ExactParams p, int nsteps, double tau,
+                                                         int nsub, double* work, int tiles_x, int tiles_y,
+                                                         int* flags) {
+  const FlatAcc acc{st, work, flags, (long long)p.nx * p.ny, p.nx};
+  fefb_nfm_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, 0, tiles_x * tiles_y);
+}
+
+// ---- the folded G with register-resident columns.  Each thread keeps its column strip's
+// v, p, D (= div(u, v)) and frozen p-tendency in registers, so the y-neighbours of a
+// stencil are registers (only a strip's two end rows read the next strip's values from
+// shared memory) and only x-neighbours, u and the frozen u/v tendencies come from shared
+// memory: ~9 shared loads per cell and substep instead of 19.  The damping divergence of
+// substep k+1, dx(u) + dy(v) of the new velocities, is the same expression (same operands,
+// same order) as the divergence in substep k's pressure update, so it is taken from there:
+// two passes per substep (u'/v', then p' and D) plus one D pass per block.  Passes run
+// branch-free over every cell of the strip; cells outside a pass's valid margin hold values
+// no valid cell ever reads (the margins shrink by the stencil radius), as in fefb_nf_body.
+template <int TMY, int K, int NT, int ORD, class ACC>
+__device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int nsteps, double tau, int nsub,
+                                              int tiles_x, int tiles_y, int tile_lo, int tile_hi) {
+  using C = NfmCfg<TMY, K, NT, nfm_reach<ORD>()>;
+  constexpr int TX = C::TX, H = C::H, HE = C::HE, HX = C::HX, RX = C::RX, PL = C::PL, S = C::S;
+  extern __shared__ double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const double sx = 0.5 / p.dx, sy = 0.5 / p.dy, cs = p.cs, a1 = p.a1, a2 = p.a2;
+  const bool damp = (p.a1 != 0.0 || p.a2 != 0.0);
+  const int tid = threadIdx.x;
+  const int cx = tid % RX, strip = tid / RX;
+  const bool comp = strip < C::NSTR;
+  const int y0s = strip * S;
+  const int nblk = (nsub + K - 1) / K;
+  const bool resident = tile_hi - tile_lo <= (int)gridDim.x;
+  double* const U = sm + RX;  // row 0 of the region (one padding row above each plane)
+  double* const V = U + PL;
+  double* const P = V + PL;
+  double* const Dp = P + PL;
+  double* const TU = Dp + PL;
+  double* const TV = TU + PL;
+  const int oc = y0s * RX + cx;  // this thread's first cell
+  // does this thread's strip touch margin m of the tile (the cells a pass must produce)?
+  auto inm = [&](int m, int TY) {
+    return comp && cx >= HX - m && cx < HX + TX + m && y0s + S > HE - m && y0s < HE + TY + m;
+  };
+  double v[S], pr[S], dv_[S], tp[S];
+  int ph = 0;
+#ifdef PW_NF_PROF
+  long long pt[5] = {0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+#define NFP(k) do { t1 = clock64(); pt[k] += t1 - t0; t0 = t1; } while (0)
+#else
+#define NFP(k) do {} while (0)
+#endif
+  for (int step = 0; step < nsteps; ++step) {
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int ks = min(K, nsub - blk * K);
+      const int fsrc = (blk % 2 == 0) ? 0 : 1, fdst = 1 - fsrc;
+      for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int tx0 = ix * TX;
+        const int ty0 = (int)((long long)iy * ny / tiles_y);
+        const int TY = (int)((long long)(iy + 1) * ny / tiles_y) - ty0;
+        const int RY = TY + 2 * HE;
+#ifdef PW_NF_PROF
+        t0 = clock64();
+#endif
+        nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
+        NFP(0);
+        const bool ld_tend = blk > 0 && !resident;
+        for (int c = tid; c < (RX / 2) * RY; c += NT) {
+          const int y = c / (RX / 2), x = 2 * (c - y * (RX / 2));
+          int gx = tx0 - HX + x, gy = ty0 - HE + y;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          gy += gy < 0 ? ny : 0;
+          gy -= gy >= ny ? ny : 0;
+          const int o = y * RX + x;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(U + f * PL + o);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(acc.pl(fsrc, f, gy) + gx)
+                         : "memory");
+          }
+          if (ld_tend) {
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+              const unsigned sa = (unsigned)__cvta_generic_to_shared(TU + f * PL + o);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(acc.pl(2, f, gy) + gx)
+                           : "memory");
+            }
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (ld_tend && comp) {
+          int gx = tx0 - HX + cx;
+          gx += gx < 0 ? nx : 0;
+          gx -= gx >= nx ? nx : 0;
+          int gy = ty0 - HE + y0s;
+          gy += gy < 0 ? ny : 0;
+          gy -= gy >= ny ? ny : 0;
+#pragma unroll
+          for (int r = 0; r < S; ++r) {
+            tp[r] = __ldcg(acc.pl(2, 2, gy) + gx);
+            if (++gy >= ny) gy = 0;
+          }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        NFP(1);
+        if (comp) {
+          if (blk == 0) {  // frozen advective tendencies (physics.py:67-74) on margin H
+            int gx = tx0 - HX + cx;
+            gx += gx < 0 ? nx : 0;
+            gx -= gx >= nx ? nx : 0;
+            const bool colin = cx >= HX - H && cx < HX + TX + H;
+            const bool own_x = cx >= HX && cx < HX + TX;
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int y = y0s + r;
+              double au = 0.0, av = 0.0, ap = 0.0;
+              if (colin && y >= HE - H && y < HE + TY + H) {
+                int gy = ty0 - HE + y;
+                gy += gy < 0 ? ny : 0;
+                gy -= gy >= ny ? ny : 0;
+                au = adv_smem<ORD, RX>(p, U, cx, y, gx, gy);
+                av = adv_smem<ORD, RX>(p, V, cx, y, gx, gy);
+                ap = adv_smem<ORD, RX>(p, P, cx, y, gx, gy);
+                if (!resident && own_x && y >= HE && y < HE + TY) {
+                  acc.pl(2, 0, gy)[gx] = au;
+                  acc.pl(2, 1, gy)[gx] = av;
+                  acc.pl(2, 2, gy)[gx] = ap;
+                }
+              }
+              TU[oc + r * RX] = au;
+              TV[oc + r * RX] = av;
+              tp[r] = ap;
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < S; ++r) {
+            v[r] = V[oc + r * RX];
+            pr[r] = P[oc + r * RX];
+          }
+          if (damp && inm(H - 1, TY)) {  // D = dx(u) + dy(v) (damping_tendencies' div, numba_backend.py:108-111)
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = oc + r * RX;
+              const double vm = r > 0 ? v[r - 1] : V[o - RX];
+              const double vp = r < S - 1 ? v[r + 1] : V[o + RX];
+              dv_[r] = (U[o + 1] - U[o - 1]) * sx + (vp - vm) * sy;
+              Dp[o] = dv_[r];
+            }
+          }
+        }
+        __syncthreads();
+        NFP(2);
+        for (int ss = 0; ss < ks; ++ss) {
+          const int M = H - 3 * ss;  // (u, v, p) valid on margin M of the tile
+          // u', v' on margin M - 2 (fb_substeps, numba_backend.py:137-143)
+          if (inm(M - 2, TY)) {
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = oc + r * RX;
+              const double pm = r > 0 ? pr[r - 1] : P[o - RX];
+              const double pp = r < S - 1 ? pr[r + 1] : P[o + RX];
+              double du = TU[o] - cs * ((P[o + 1] - P[o - 1]) * sx);
+              double dv = TV[o] - cs * ((pp - pm) * sy);
+              if (damp) {
+                const double dm = r > 0 ? dv_[r - 1] : Dp[o - RX];
+                const double dq = r < S - 1 ? dv_[r + 1] : Dp[o + RX];
+                du = du + a1 * ((Dp[o + 1] - Dp[o - 1]) * sx);
+                dv = dv + a2 * ((dq - dm) * sy);
+              }
+              U[o] = U[o] + tau * du;
+              v[r] = v[r] + tau * dv;
+            }
+            V[oc] = v[0];
+            V[oc + (S - 1) * RX] = v[S - 1];
+          }
+          __syncthreads();
+          // p' on margin M - 3 from the new velocities (numba_backend.py:144-145); its
+          // divergence is the next substep's D (needed on margin M - 4)
+          if (inm(M - 3, TY)) {
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int o = oc + r * RX;
+              const double vm = r > 0 ? v[r - 1] : V[o - RX];
+              const double vp = r < S - 1 ? v[r + 1] : V[o + RX];
+              const double divn = (U[o + 1] - U[o - 1]) * sx + (vp - vm) * sy;
+              pr[r] = pr[r] + tau * (tp[r] - cs * divn);
+              dv_[r] = divn;
+            }
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              P[oc + r * RX] = pr[r];
+              if (damp) Dp[oc + r * RX] = dv_[r];
+            }
+          }
+          __syncthreads();
+        }
+        NFP(3);
+        if (comp) {
+#pragma unroll
+          for (int r = 0; r < S; ++r) V[oc + r * RX] = v[r];
+        }
+        __syncthreads();
+        for (int c = tid; c < TX * TY; c += NT) {
+          const int ly = c / TX, lx = c - ly * TX;
+          const int o = (ly + HE) * RX + lx + HX;
+          const int gy = ty0 + ly, gx = tx0 + lx;
+          acc.pl(fdst, 0, gy)[gx] = U[o];
+          acc.pl(fdst, 1, gy)[gx] = V[o];
+          acc.pl(fdst, 2, gy)[gx] = P[o];
+        }
+        nf_signal(acc, t, ph + 1);
+        NFP(4);
+      }
+      ++ph;
+    }
+    if (nblk % 2 == 1) {
+      for (int t = tile_lo + blockIdx.x; t < tile_hi; t += gridDim.x) {
+        const int iy = t / tiles_x, ix = t - iy * tiles_x;
+        const int ty0 = (int)((long long)iy * ny / tiles_y), ty1 = (int)((long long)(iy + 1) * ny / tiles_y);
+        nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
+        for (int c = tid; c < TX * (ty1 - ty0); c += NT) {
+          const int gy = ty0 + c / TX, gx = ix * TX + c % TX;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) acc.pl(0, f, gy)[gx] = acc.pl(1, f, gy)[gx];
+        }
+        nf_signal(acc, t, ph + 1);
+      }
+      ++ph;
+    }
+  }
+#ifdef PW_NF_PROF
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 70))
+    printf("nfr cta %d: wait %lld stage %lld adv+D %lld passes %lld store+signal %lld cycles\n", blockIdx.x,
+           pt[0], pt[1], pt[2], pt[3], pt[4]);
+#endif
+}
+
+template <int TMY, int K, int NT, int ORD>
+__global__ void __launch_bounds__(NT, 1) fefb_nfr_shard_kernel(NfShards sh, ExactParams p, int nsteps, double tau,
+                                                               int nsub, int tiles_x, int tiles_y, int tile_lo,
+                                                               int tile_hi) {
+  const ShardAcc acc{sh, p.nx};
+  fefb_nfr_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, tile_lo, tile_hi);
+}
+
+template <int TMY, int K, int NT, int ORD>
+__global__ void __launch_bounds__(NT, 1) fefb_nfr_kernel(double* st, ExactParams p, int nsteps, double tau,
+                                                         int nsub, double* work, int tiles_x, int tiles_y,
+                                                         int* flags) {
+  const FlatAcc acc{st, work, flags, (long long)p.nx * p.ny, p.nx};
+  fefb_nfr_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, 0, tiles_x * tiles_y);
+}
+
+
 template <int TMY, int K, int NT, int ORD, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactParams p, int nsteps, double tau,
                                                        int nsub, double* work, int tiles_x, int tiles_y,
@@ -935,14 +1428,6 @@ __global__ void __launch_bounds__(NT, MINB) fefb_nf_kernel(double* st, ExactPara
   fefb_nf_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, 0, tiles_x * tiles_y);
 }
 
-// The row-sharded form (tiles [tile_lo, tile_hi) of a grid whose rows live in row shards).
-template <int TMY, int K, int NT, int ORD>
-__global__ void __launch_bounds__(NT, 1) fefb_nf_shard_kernel(NfShards sh, ExactParams p, int nsteps, double tau,
-                                                              int nsub, int tiles_x, int tiles_y, int tile_lo,
-                                                              int tile_hi) {
-  const ShardAcc acc{sh, p.nx};
-  fefb_nf_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, tile_lo, tile_hi);
-}
 
 template <int TMX, int TMY, int K>
 constexpr size_t tb_smem() {
@@ -1064,32 +1549,66 @@ static bool launch_nf(Ctx& c, const ExactParams& p, double* states, int nsteps, 
   return true;
 }
 
+// The folded form of launch_nf (fefb_nfm_kernel): same tiling rule, E more margin.
+template <int TMY_, int K, int NT, int ORD, int MINB = 1, bool REG = false>
+static bool launch_nfm(Ctx& c, const ExactParams& p, double* states, int nsteps, double h, int nsub, double* work) {
+  constexpr int TMY = ORD == 1 ? TMY_ : TMY_ - 8;  // reach 3: shorter tiles keep the planes in shared memory
+  using C = NfmCfg<TMY, K, NT, nfm_reach<ORD>()>;
+  auto kern = REG ? fefb_nfr_kernel<TMY, K, NT, ORD> : fefb_nfm_kernel<TMY, K, NT, ORD, MINB>;
+  const int per_sm = kernel_setup(c, kern, NT, C::SMEM);
+  const int tiles_x = p.nx / 32;
+  const int slots = c.num_sms * per_sm;
+  int tiles_y = (p.ny + TMY - 1) / TMY;
+  const int fill = std::max(1, slots / std::max(1, tiles_x));
+  if (tiles_x * tiles_y < slots) tiles_y = std::max(tiles_y, std::min(p.ny / C::HE, fill));
+  if (p.ny / tiles_y < C::HE || tiles_x * 32 != p.nx) return false;  // halo must stay in the 8 neighbours
+  if (((uintptr_t)states | (uintptr_t)work) & 15) return false;
+  const int tiles = tiles_x * tiles_y;
+  const int grid = std::min(tiles, slots);
+  int* flags = reinterpret_cast<int*>(work + 6 * (size_t)p.nx * p.ny);
+  PW_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)tiles, c.stream));
+  double tau = h / nsub;
+  ExactParams pp = p;
+  int tx = tiles_x, ty = tiles_y;
+  void* args[] = {&states, &pp, &nsteps, &tau, &nsub, &work, &tx, &ty, &flags};
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, C::SMEM, c.stream));
+  c.launches += 1;
+  return true;
+}
+
 static int nf_variant() {
-  const char* e = getenv("PW_COARSE_NF");  // 0: the grid-barrier kernels; 2 / 3 / 4: substeps per phase
-  return (e && *e) ? atoi(e) : 3;
+  // 0: the grid-barrier kernels; 2 / 3 / 4: substeps per phase (phase-A form); 6 / 10: phase A
+  // folded into the first block (K = 3 / 2); 11 / 12: folded + register-resident columns
+  // (K = 3 / 2; 12 is the default: 512^2 2-step call 160 us, 1024^2 623 us, from 200 / 698)
+  const char* e = getenv("PW_COARSE_NF");
+  return (e && *e) ? atoi(e) : 12;
 }
 
 // Row-sharded G: one state whose rows live in nsh row shards, shard s holding
 // rows [s R, (s+1) R) in its own state / work / flag buffers.  All shards' tiles run in this one
-// launch; tile rows are aligned to the shard boundaries (tiles_y a multiple of nsh).  Same
-// arithmetic as launch_nf<60, 3, 512> -- bitwise equal to the replicated G.
+// launch; tile rows are aligned to the shard boundaries (tiles_y a multiple of nsh).  The
+// default G's body (fefb_nfr_body, K = 2) through the shard accessor -- bitwise equal to the
+// replicated G.
+constexpr int kRsK = 2;
+static int rs_tmy(const ExactParams& p) { return p.order == 1 ? 64 : 56; }
+static int rs_tiles_y(const ExactParams& p, int nsh) { return ((p.ny + rs_tmy(p) - 1) / rs_tmy(p) + nsh - 1) / nsh * nsh; }
 size_t rowshard_work_doubles(const ExactParams& p, int nsh) { return (size_t)6 * p.nx * (p.ny / nsh); }
-int rowshard_flag_ints(const ExactParams& p, int nsh) {
-  const int tiles_y = ((p.ny + 59) / 60 + nsh - 1) / nsh * nsh;
-  return (p.nx / 32) * tiles_y / nsh;
-}
+int rowshard_flag_ints(const ExactParams& p, int nsh) { return (p.nx / 32) * rs_tiles_y(p, nsh) / nsh; }
 void launch_fefb_rowshard(Ctx& c, const ExactParams& p, int nsh, double* const* st, double* const* work,
                           int* const* flags, int nsteps, double h, int nsub) {
   PW_CHECK(nsh >= 1 && nsh <= kMaxRowShards, PW_ERR_VALUE, "row shards: 1..8");
   PW_CHECK(p.nx % 32 == 0 && p.ny % nsh == 0, PW_ERR_VALUE, "row shards need nx % 32 == 0 and ny % nshard == 0");
-  constexpr int TMY = 60, K = 3, NT = 512;
-  using C = NfCfg<TMY, K, NT>;
+  constexpr int NT = 512;
   const bool o1 = p.order == 1;
-  auto kern = o1 ? fefb_nf_shard_kernel<TMY, K, NT, 1> : fefb_nf_shard_kernel<TMY, K, NT, 0>;
-  const int per_sm = kernel_setup(c, kern, NT, C::SMEM);
+  using C1 = NfmCfg<64, kRsK, NT, 1>;
+  using C0 = NfmCfg<56, kRsK, NT, 3>;
+  auto kern = o1 ? fefb_nfr_shard_kernel<64, kRsK, NT, 1> : fefb_nfr_shard_kernel<56, kRsK, NT, 0>;
+  const size_t smem = o1 ? C1::SMEM : C0::SMEM;
+  const int he = o1 ? C1::HE : C0::HE;
+  const int per_sm = kernel_setup(c, kern, NT, smem);
   const int tiles_x = p.nx / 32;
-  const int tiles_y = ((p.ny + TMY - 1) / TMY + nsh - 1) / nsh * nsh;  // shard-aligned tile rows
-  PW_CHECK(p.ny / tiles_y >= 3 * K, PW_ERR_VALUE, "row shards: tiles too short for the 9-row halo");
+  const int tiles_y = rs_tiles_y(p, nsh);  // shard-aligned tile rows
+  PW_CHECK(p.ny / tiles_y >= he, PW_ERR_VALUE, "row shards: tiles too short for the halo");
   NfShards sh{};
   sh.rows = p.ny / nsh;
   sh.tiles = tiles_x * tiles_y / nsh;
@@ -1105,7 +1624,7 @@ void launch_fefb_rowshard(Ctx& c, const ExactParams& p, int nsh, double* const* 
   ExactParams pp = p;
   int tx = tiles_x, ty = tiles_y, lo = 0, hi = tiles;
   void* args[] = {&sh, &pp, &nsteps, &tau, &nsub, &tx, &ty, &lo, &hi};
-  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, C::SMEM, c.stream));
+  PW_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, smem, c.stream));
   c.launches += 1;
 }
 
@@ -1125,6 +1644,20 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
       case 5:  // smaller tiles, 2 CTAs (2 tiles in flight) per SM: measured 207 vs 195 us at 512^2
         ok = o1 ? launch_nf<32, 2, 256, 1, 2>(c, p, states, nsteps, h, nsub, work)
                 : launch_nf<32, 2, 256, 0, 2>(c, p, states, nsteps, h, nsub, work); break;
+      case 6: ok = o1 ? launch_nfm<60, 3, 512, 1>(c, p, states, nsteps, h, nsub, work)
+                      : launch_nfm<60, 3, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
+      case 7: ok = o1 ? launch_nf<32, 2, 512, 1, 2>(c, p, states, nsteps, h, nsub, work)
+                      : launch_nf<32, 2, 512, 0, 2>(c, p, states, nsteps, h, nsub, work); break;
+      case 8: ok = o1 ? launch_nfm<26, 2, 512, 1, 2>(c, p, states, nsteps, h, nsub, work)
+                      : launch_nfm<26, 2, 512, 0, 2>(c, p, states, nsteps, h, nsub, work); break;
+      case 9: ok = o1 ? launch_nfm<46, 4, 512, 1>(c, p, states, nsteps, h, nsub, work)
+                      : launch_nfm<46, 4, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
+      case 10: ok = o1 ? launch_nfm<64, 2, 512, 1>(c, p, states, nsteps, h, nsub, work)
+                       : launch_nfm<64, 2, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
+      case 11: ok = o1 ? launch_nfm<60, 3, 512, 1, 1, true>(c, p, states, nsteps, h, nsub, work)
+                       : launch_nfm<60, 3, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
+      case 12: ok = o1 ? launch_nfm<64, 2, 512, 1, 1, true>(c, p, states, nsteps, h, nsub, work)
+                       : launch_nfm<64, 2, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
       default: ok = o1 ? launch_nf<60, 3, 512, 1>(c, p, states, nsteps, h, nsub, work)
                        : launch_nf<60, 3, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
     }

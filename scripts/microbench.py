@@ -97,6 +97,13 @@ def bench_coarse():
         p = SlicePropagator(c, nsteps=steps)
         t = timeit(lambda: p.apply(x, out=y), reps=10)
         print(f"coarse FE-FB 512^2: {steps} step(s) {t*1e6:.1f} us")
+    _, c4 = specs(1024)
+    x4 = torch.as_tensor(harness.initial_state("c4")).cuda()[None, :].contiguous()
+    y4 = torch.empty_like(x4)
+    for steps in (1, 2):
+        p = SlicePropagator(c4, nsteps=steps)
+        t = timeit(lambda: p.apply(x4, out=y4), reps=10)
+        print(f"coarse FE-FB 1024^2: {steps} step(s) {t*1e6:.1f} us")
     p = SlicePropagator(c, nsteps=2)
     xb = x.repeat(64, 1)
     yb = torch.empty_like(xb)

@@ -10,6 +10,9 @@ the fine sweep, and stores what a multi-GB window can be pinned by in a small fi
 (<config>_reference.npz): the residual history, the ranks, the per-slice L2 norms of
 qn[1:] after every iteration and 512 fixed-seed sampled entries per slice.  The states
 themselves (6 GB per iteration at c4) are not stored.
+
+PW_GOLDEN_SPILL=<dir> keeps the subspace's d x m matrices in file-backed memmaps
+(see _SpillNumpy), which is how the K=2 c4 fixtures were made in a 62 GB container.
 """
 from __future__ import annotations
 
@@ -31,6 +34,50 @@ from make_golden import slice_closures  # noqa: E402
 from paper_1510_02237_b200 import harness  # noqa: E402  (seeded generators only)
 
 N_SAMPLE = 512
+
+
+class _SpillNumpy:
+    """numpy as the reference's subspace module sees it, except that the two d x m
+    allocations of Subspace.update (column_stack of the snapshots / images and the
+    F-order scratch copy handed to LAPACK) are file-backed memmaps under ``root``.
+    Same values, same LAPACK calls; only the pages live on disk, so a c4 window with
+    K=2 (~100 GB of working set) runs in a 62 GB container.  PW_GOLDEN_SPILL=<dir>.
+    """
+
+    def __init__(self, root):
+        self._root = root
+        self._n = 0
+        os.makedirs(root, exist_ok=True)
+
+    def _alloc(self, shape, order):
+        self._n += 1
+        path = os.path.join(self._root, f"spill_{self._n}.bin")
+        a = np.lib.format.open_memmap(path, mode="w+", dtype=np.float64, shape=shape,
+                                      fortran_order=(order == "F"))
+        os.unlink(path)  # pages stay mapped; the file disappears with the array
+        return a
+
+    def column_stack(self, cols):
+        cols = [np.asarray(c) for c in cols]
+        m = sum(1 if c.ndim == 1 else c.shape[1] for c in cols)
+        out = self._alloc((cols[0].shape[0], m), "C")
+        j = 0
+        for c in cols:
+            if c.ndim == 1:
+                out[:, j] = c
+                j += 1
+            elif c.shape[1]:
+                out[:, j:j + c.shape[1]] = c
+                j += c.shape[1]
+        return out
+
+    def asfortranarray(self, a):
+        out = self._alloc(a.shape, "F")
+        out[...] = a
+        return out
+
+    def __getattr__(self, name):
+        return getattr(np, name)
 
 
 def main(n_it=1, name="c4", suffix=""):
@@ -59,6 +106,9 @@ def main(n_it=1, name="c4", suffix=""):
         print(f"  iteration {len(norms)}: residual {r:.6e} ({time.time() - t0:.0f} s)", flush=True)
         return r
 
+    spill = os.environ.get("PW_GOLDEN_SPILL")
+    if spill:
+        ref_sub.np = _SpillNumpy(spill)
     ref_sub.Subspace.update = spy_update
     ref_par.iteration_residual = spy_res
     t0 = time.time()
@@ -68,6 +118,7 @@ def main(n_it=1, name="c4", suffix=""):
     finally:
         ref_sub.Subspace.update = orig_update
         ref_par.iteration_residual = orig_res
+        ref_sub.np = np
     np.savez_compressed(os.path.join(HERE, f"{name}_reference{suffix}.npz"), res=np.array(res), ranks=np.array(ranks),
                         norms=np.array(norms), samples=np.array(samples), idx=idx,
                         seconds=time.time() - t0, threads=os.cpu_count())
