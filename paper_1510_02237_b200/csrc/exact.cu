@@ -1411,8 +1411,8 @@ __global__ void __launch_bounds__(NT, 1) fefb_nfr_shard_kernel(NfShards sh, Exac
   fefb_nfr_body<TMY, K, NT, ORD>(acc, p, nsteps, tau, nsub, tiles_x, tiles_y, tile_lo, tile_hi);
 }
 
-template <int TMY, int K, int NT, int ORD>
-__global__ void __launch_bounds__(NT, 1) fefb_nfr_kernel(double* st, ExactParams p, int nsteps, double tau,
+template <int TMY, int K, int NT, int ORD, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) fefb_nfr_kernel(double* st, ExactParams p, int nsteps, double tau,
                                                          int nsub, double* work, int tiles_x, int tiles_y,
                                                          int* flags) {
   const FlatAcc acc{st, work, flags, (long long)p.nx * p.ny, p.nx};
@@ -1554,7 +1554,7 @@ template <int TMY_, int K, int NT, int ORD, int MINB = 1, bool REG = false>
 static bool launch_nfm(Ctx& c, const ExactParams& p, double* states, int nsteps, double h, int nsub, double* work) {
   constexpr int TMY = ORD == 1 ? TMY_ : TMY_ - 8;  // reach 3: shorter tiles keep the planes in shared memory
   using C = NfmCfg<TMY, K, NT, nfm_reach<ORD>()>;
-  auto kern = REG ? fefb_nfr_kernel<TMY, K, NT, ORD> : fefb_nfm_kernel<TMY, K, NT, ORD, MINB>;
+  auto kern = REG ? fefb_nfr_kernel<TMY, K, NT, ORD, MINB> : fefb_nfm_kernel<TMY, K, NT, ORD, MINB>;
   const int per_sm = kernel_setup(c, kern, NT, C::SMEM);
   const int tiles_x = p.nx / 32;
   const int slots = c.num_sms * per_sm;
@@ -1658,6 +1658,8 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
                        : launch_nfm<60, 3, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
       case 12: ok = o1 ? launch_nfm<64, 2, 512, 1, 1, true>(c, p, states, nsteps, h, nsub, work)
                        : launch_nfm<64, 2, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
+      case 13: ok = o1 ? launch_nfm<30, 2, 256, 1, 2, true>(c, p, states, nsteps, h, nsub, work)
+                       : launch_nfm<30, 2, 256, 0, 2, true>(c, p, states, nsteps, h, nsub, work); break;
       default: ok = o1 ? launch_nf<60, 3, 512, 1>(c, p, states, nsteps, h, nsub, work)
                        : launch_nf<60, 3, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
     }
