@@ -1210,7 +1210,7 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
   double v[S], pr[S], dv_[S], tp[S];
   int ph = 0;
 #ifdef PW_NF_PROF
-  long long pt[5] = {0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+  long long pt[7] = {0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
 #define NFP(k) do { t1 = clock64(); pt[k] += t1 - t0; t0 = t1; } while (0)
 #else
 #define NFP(k) do {} while (0)
@@ -1368,6 +1368,7 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
           for (int r = 0; r < S; ++r) V[oc + r * RX] = v[r];
         }
         __syncthreads();
+        NFP(4);
         for (int c = tid; c < TX * TY; c += NT) {
           const int ly = c / TX, lx = c - ly * TX;
           const int o = (ly + HE) * RX + lx + HX;
@@ -1376,8 +1377,9 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
           acc.pl(fdst, 1, gy)[gx] = V[o];
           acc.pl(fdst, 2, gy)[gx] = P[o];
         }
+        NFP(5);
         nf_signal(acc, t, ph + 1);
-        NFP(4);
+        NFP(6);
       }
       ++ph;
     }
@@ -1398,8 +1400,8 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
   }
 #ifdef PW_NF_PROF
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 70))
-    printf("nfr cta %d: wait %lld stage %lld adv+D %lld passes %lld store+signal %lld cycles\n", blockIdx.x,
-           pt[0], pt[1], pt[2], pt[3], pt[4]);
+    printf("nfr cta %d: wait %lld stage %lld adv+D %lld passes %lld vsync %lld store %lld signal %lld cycles\n",
+           blockIdx.x, pt[0], pt[1], pt[2], pt[3], pt[4], pt[5], pt[6]);
 #endif
 }
 
