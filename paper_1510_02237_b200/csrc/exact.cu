@@ -1196,6 +1196,11 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
   const int y0s = strip * S;
   const int nblk = (nsub + K - 1) / K;
   const bool resident = tile_hi - tile_lo <= (int)gridDim.x;
+  // one tile per CTA and an even block count per step: the tile's own cells stay in shared
+  // memory from block to block (and step to step).  A block then stages only the halo ring
+  // and stores only the band its neighbours' regions reach (HX columns / HE rows from the
+  // tile's edges); the whole tile goes out after the call's last block.
+  const bool keep = resident && nblk % 2 == 0;
   double* const U = sm + RX;  // row 0 of the region (one padding row above each plane)
   double* const V = U + PL;
   double* const P = V + PL;
@@ -1231,8 +1236,11 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
         nf_wait(acc, ix, iy, tiles_x, tiles_y, ph);
         NFP(0);
         const bool ld_tend = blk > 0 && !resident;
+        const bool ring_only = keep && (step > 0 || blk > 0);
+        const bool last = step == nsteps - 1 && blk == nblk - 1;
         for (int c = tid; c < (RX / 2) * RY; c += NT) {
           const int y = c / (RX / 2), x = 2 * (c - y * (RX / 2));
+          if (ring_only && x >= HX && x < HX + TX && y >= HE && y < HE + TY) continue;  // own cells: on chip
           int gx = tx0 - HX + x, gy = ty0 - HE + y;
           gx += gx < 0 ? nx : 0;
           gx -= gx >= nx ? nx : 0;
@@ -1371,6 +1379,7 @@ __device__ __forceinline__ void fefb_nfr_body(const ACC& acc, ExactParams p, int
         NFP(4);
         for (int c = tid; c < TX * TY; c += NT) {
           const int ly = c / TX, lx = c - ly * TX;
+          if (keep && !last && lx >= HX && lx < TX - HX && ly >= HE && ly < TY - HE) continue;  // no neighbour reads it
           const int o = (ly + HE) * RX + lx + HX;
           const int gy = ty0 + ly, gx = tx0 + lx;
           acc.pl(fdst, 0, gy)[gx] = U[o];
