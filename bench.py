@@ -99,6 +99,17 @@ def load_traffic(persistent=False):
     return None, None
 
 
+def load_shared_wavefronts():
+    """Shared-memory data-pipe wavefronts (128 B each) of one K1 launch at c2, from the same
+    committed ncu capture as the DRAM traffic; None for the previous-generation kernels."""
+    if k1_generation() != "tma" or not os.path.exists(TRAFFIC_FILE):
+        return None, None
+    with open(TRAFFIC_FILE) as fh:
+        d = json.load(fh).get("persistent_tma") or {}
+    w = d.get("shared_wavefronts_per_launch")
+    return (float(w), d.get("shared_source")) if w else (None, None)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -522,6 +533,21 @@ def run_ours(args, rank, world, local_rank):
     traffic, traffic_src = load_traffic(persistent)
     fp64_peak = ctx.fp64_peak_tflops() if rank == 0 else None  # outside the timed region
     fp64_achieved = FLOP_PER_CELL_UPDATE * value / world / 1e12
+    # the resource K1 actually saturates: the SMs' shared-memory data pipes (one 128-byte
+    # wavefront per SM and clock); wavefronts per launch from the ncu capture, time measured here
+    shared = None
+    wf, wf_src = load_shared_wavefronts() if persistent else (None, None)
+    if wf and rank == 0:
+        sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+        n_sm = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        sh_peak = 128.0 * n_sm * sm_mhz * 1e6 / 1e12
+        sh_ach = wf * 128.0 / launch_s / 1e12
+        shared = {"achieved": sh_ach, "peak": sh_peak, "unit": "TB/s", "frac": sh_ach / sh_peak,
+                  "wavefronts_per_launch": wf, "wavefronts_per_cell_update": wf / (algo_bytes / BYTES_PER_CELL_UPDATE),
+                  "peak_source": "128 B x SMs x SM clock (scripts/ubench_shfl.cu measured 36.0 TB/s of LDS.128 on this pool)",
+                  "source": wf_src,
+                  "note": "K1 is bound by on-chip (shared-memory) bandwidth, not by HBM: every stage re-reads "
+                          "3x-overlapping x-windows from shared memory; see DESIGN.md K1"}
 
     extra = {}
     if world > 1 and args.parareal and not comm_selftest(dist):
@@ -570,7 +596,8 @@ def run_ours(args, rank, world, local_rank):
                          "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": (fp64_achieved / fp64_peak) if fp64_peak else None,
                                   "flop_per_cell_update": FLOP_PER_CELL_UPDATE,
-                                  "peak_source": "measured live: DFMA probe kernel (pw_probe_fp64_peak)"}},
+                                  "peak_source": "measured live: DFMA probe kernel (pw_probe_fp64_peak)"},
+                         "shared": shared},
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": int(q_host.numel() * 8),
                     "d2h_bytes_per_step": int(q_host.numel() * 8), "finite": ok,
                     "copies": "pinned host buffers; H2D/D2H on a second stream, double-buffered "

@@ -339,6 +339,13 @@ struct pw_basis {
   std::vector<double> diag_h;
   std::vector<int> piv_h;
   bool fq_valid = false, img_valid = false;
+  // Q kept implicit (sweeps on one unsharded GPU): Q = [Q2; 0] - V X2 is never formed; the
+  // serial step takes Q^T x = Cq^T [x[0:mr]; V^T x] with Cq = [Q2; -X2] ((mr + k) x r).  The
+  // explicit Q (d x r, 2 d k r flops) is formed on first use by basis_q().
+  bool implicit_q = false, q_valid = false;
+  int implicit_steps = 0;  // serial steps per update (the pass over V reads m columns, Q has r)
+  DBuf Cq;
+  int cq_n1 = 0, cq_n2 = 0;
 };
 
 namespace {
@@ -681,6 +688,21 @@ static void form_q_tsqr(pw_basis* B, const double* Q2, int r, double* Q) {
   mark("tsqr.Q");
 }
 
+// The explicit orthonormal basis Q (d x r), formed on first use: Q = [Q2; 0] + V Cq[mr:, :]
+static const double* basis_q(pw_basis* B) {
+  if (B->q_valid || B->r == 0) return B->Q.p;
+  Ctx& c = B->ctx->c;
+  const long long d = B->dim;
+  const int r = B->r, mr = B->cq_n1, k = B->cq_n2, lc = mr + k;
+  PW_CHECK(mr > 0 && B->Cq.p, PW_ERR_STATE, "subspace basis is not factored");
+  double* Q = B->Q.ensure(c, (size_t)d * std::min<size_t>((size_t)B->cap, (size_t)d));
+  PW_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * (size_t)d * r, c.stream));
+  copy_cols(c, Q, d, B->Cq.p, lc, mr, r);
+  gemm(c, false, false, d, r, k, 1.0, B->W.p, d, B->Cq.p + mr, lc, 1.0, Q, d);
+  B->q_valid = true;
+  return Q;
+}
+
 // Everything of the refactorisation that depends on the snapshots only: the QR of S, the
 // pivoted QR of R1 and the rank, Q, and the scattered R11^-1 (X).  The sweep runs it on the
 // side stream while the fine propagator runs (the images are not needed until Y).
@@ -727,18 +749,28 @@ void basis_factor(pw_basis* B, int m_old) {
   // Q = Q1 [Q2[:, :r]; 0] = [Q2; 0] - V (T (V[0:mr]^T Q2))
   double* Q2 = B->Q2.ensure(c, capc * capc);
   pw::form_q2(c, Rs, mr, piv, tau2, r, Q2);
-  double* Q = B->Q.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
+  B->q_valid = false;
+  B->cq_n1 = B->cq_n2 = 0;
   if (tsqr) {
+    double* Q = B->Q.ensure(c, (size_t)d * std::min<size_t>(capc, (size_t)d));
     form_q_tsqr(B, Q2, r, Q);
+    B->q_valid = true;
   } else {
+    // Cq = [Q2; -X2], X2 = T (V[0:mr]^T Q2): the small factors of Q = [Q2; 0] - V X2
     const int k = B->v_cols;  // == mr
+    const int lc = mr + k;
     double* X1 = B->wy1.ensure(c, capc * capc);
-    double* X2 = B->wy2.ensure(c, capc * capc);
+    double* Cq = B->Cq.ensure(c, 2 * capc * capc);
     gemm(c, true, false, k, r, mr, 1.0, B->W.p, d, Q2, mr, 0.0, X1, k);
-    gemm(c, false, false, k, r, k, 1.0, B->T.p, B->cap, X1, k, 0.0, X2, k);
-    PW_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * (size_t)d * r, c.stream));
-    copy_cols(c, Q, d, Q2, mr, mr, r);
-    gemm(c, false, false, d, r, k, -1.0, B->W.p, d, X2, k, 1.0, Q, d);
+    copy_cols(c, Cq, lc, Q2, mr, mr, r);
+    gemm(c, false, false, k, r, k, -1.0, B->T.p, B->cap, X1, k, 0.0, Cq + mr, lc);
+    B->cq_n1 = mr;
+    B->cq_n2 = k;
+    // worth it while the m - r extra columns the serial passes read (V has m columns, Q r)
+    // cost less than the 2 d k r flops of forming Q: HBM at ~6.5 TB/s against ~25 TFLOP/s
+    const double extra_s = (double)(k - r) * B->implicit_steps * 8.0 / 6.5e12;
+    const double form_s = 2.0 * (double)k * r / 25e12;
+    if (!B->implicit_q || extra_s >= form_s) basis_q(B);
   }
   clk.mark("Q=Q1Q2");
   double* X = B->X.ensure(c, capc * capc);
@@ -803,7 +835,7 @@ void basis_append(pw_basis* B, const double* states, long long lds, const double
 double* basis_coeffs(pw_basis* B, const double* v, int batch, long long ld) {
   Ctx& c = B->ctx->c;
   double* a = B->alpha.ensure(c, (size_t)std::max(B->r, 1) * batch);
-  gemm(c, true, false, B->r, batch, B->dim, 1.0, B->Q.p, B->dim, v, ld, 0.0, a, std::max(B->r, 1));
+  gemm(c, true, false, B->r, batch, B->dim, 1.0, basis_q(B), B->dim, v, ld, 0.0, a, std::max(B->r, 1));
   return a;
 }
 
@@ -813,7 +845,7 @@ const double* basis_fq(pw_basis* B) {
   if (!B->fq_valid && B->r > 0) {
     // FQ = D + G(Q)   (G linear: D = (F - G)(S) R^-1 and Q = S R^-1)
     double* fq = B->lazy_fq.ensure(c, (size_t)B->dim * B->r);
-    prop_apply(B->coarse, B->Q.p, fq, B->r, B->dim);
+    prop_apply(B->coarse, basis_q(B), fq, B->r, B->dim);
     pw::launch_axpby_cols(c, fq, fq, B->Y.p, 1.0, 1.0, (size_t)B->dim * B->r);
     B->fq_valid = true;
   }
@@ -1255,7 +1287,7 @@ int pw_basis_views(const pw_basis* basis, const double** q, const double** fq,
   return guarded([&] {
     PW_CHECK(basis, PW_ERR_VALUE, "NULL basis");
     pw_basis* B = const_cast<pw_basis*>(basis);
-    if (q) *q = B->Q.p;
+    if (q) *q = basis_q(B);
     if (fq) *fq = B->r > 0 ? basis_fq(B) : nullptr;
     if (snapshots) *snapshots = B->lean ? nullptr : B->S.p;
     if (images) *images = (B->m > 0 && !B->lean) ? basis_images(B) : nullptr;
@@ -1282,7 +1314,7 @@ int pw_basis_project(pw_basis* basis, const double* v, double* out, int batch, l
       return;
     }
     double* a = basis_coeffs(basis, v, batch, ld);
-    gemm(c, false, false, basis->dim, batch, basis->r, 1.0, basis->Q.p, basis->dim, a, basis->r,
+    gemm(c, false, false, basis->dim, batch, basis->r, 1.0, basis_q(basis), basis->dim, a, basis->r,
          0.0, out, ld);
   });
 }
@@ -1318,7 +1350,7 @@ int pw_kse_coarse(pw_basis* basis, pw_prop* coarse, const double* v, double* out
     double* a = basis_coeffs(basis, v, batch, ld);
     double* w = basis->tmp.ensure(c, (size_t)d * batch);
     copy_cols(c, w, d, v, ld, d, batch);
-    gemm(c, false, false, d, batch, basis->r, -1.0, basis->Q.p, d, a, basis->r, 1.0, w, d);
+    gemm(c, false, false, d, batch, basis->r, -1.0, basis_q(basis), d, a, basis->r, 1.0, w, d);
     prop_apply(coarse, w, out, batch, ld);
     // out is (d x batch) with stride ld; add FQ a
     gemm(c, false, false, d, batch, basis->r, 1.0, fq, d, a, basis->r, 1.0, out, ld);
@@ -1437,6 +1469,10 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     // coarse images (GK, GN) hold only this rank's rows [lo, lo + ldr); the iterates QK,
     // QN stay whole (G and the fine sweep need whole states).  Otherwise ldr = d, roff = 0.
     const bool local = kse && c.comm_world > 1 && c.tsqr;
+    // one unsharded GPU: the serial step works on the reflectors, Q is never formed
+    // (PW_IMPLICIT_Q=0 keeps the explicit Q = Q1 Q2 product of every update)
+    const char* iq_env = std::getenv("PW_IMPLICIT_Q");
+    const bool implicit_q = kse && c.comm_world <= 1 && c.vshards <= 1 && !(iq_env && *iq_env == '0');
     long long roff = 0, ldr = d;
     if (local) {
       const long long blk = ((d + c.comm_world - 1) / c.comm_world + 1) / 2 * 2;
@@ -1444,7 +1480,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       ldr = std::min<long long>(d, roff + blk) - roff;
       PW_CHECK(ldr >= 1, PW_ERR_VALUE, "row-sharded sweep: this rank has no rows");
     }
-    DBuf bQK, bQN, bPred, bGK, bGN, bGF, bRes, bScr, bAlpha, bPart, bAlphaPart;
+    DBuf bQK, bQN, bPred, bGK, bGN, bGF, bRes, bScr, bAlpha, bPart, bAlphaPart, bGv;
     double* QK = bQK.ensure(c, (size_t)d * (n_c + 1));
     double* QN = bQN.ensure(c, (size_t)d * (n_c + 1));
     double* PRED = bPred.ensure(c, (size_t)ldr * n_c);
@@ -1555,6 +1591,8 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
       if (kse) {
         StreamScope side(c, c.qr_overlap ? c.side : c.stream);
         PW_CUDA(cudaStreamWaitEvent(c.stream, sync.snap, 0));
+        B->implicit_q = implicit_q;
+        B->implicit_steps = n_c;
         basis_append_snapshots(B.get(), QK + B->row_lo, d, n_c);
         basis_factor(B.get(), m_old);  // blocks the host at the rank read; the fine sweep runs on
         PW_CUDA(cudaEventRecord(sync.fact, c.stream));
@@ -1577,11 +1615,19 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             // ranks of Q_g^T qk_g, and only this rank's rows of c_i are corrected (the serial
             // correction reads no others)
             const long long lo = B->row_lo, nr = B->dim;
-            gemm(c, true, false, r, n_c, nr, 1.0, B->Q.p, nr, QK + lo, d, 0.0, ab, r);
+            gemm(c, true, false, r, n_c, nr, 1.0, basis_q(B.get()), nr, QK + lo, d, 0.0, ab, r);
             pw::comm_allreduce(c, ab, (long long)r * n_c);  // TSQR projection partials
             gemm(c, false, false, nr, n_c, r, -1.0, B->Y.p, nr, ab, r, 1.0, PRED, ldr);
+          } else if (B->cq_n1 > 0 && !B->q_valid) {
+            // implicit Q: Q^T QK = Q2^T QK[0:mr] - X2^T (V^T QK)
+            const int mr = B->cq_n1, kv = B->cq_n2, lc = mr + kv;
+            double* gv = bGv.ensure(c, (size_t)kv * (n_c + 1));
+            gemm(c, true, false, kv, n_c, d, 1.0, B->W.p, d, QK, d, 0.0, gv, kv);
+            gemm(c, true, false, r, n_c, mr, 1.0, B->Cq.p, lc, QK, d, 0.0, ab, r);
+            gemm(c, true, false, r, n_c, kv, 1.0, B->Cq.p + mr, lc, gv, kv, 1.0, ab, r);
+            gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           } else {
-            gemm(c, true, false, r, n_c, d, 1.0, B->Q.p, d, QK, d, 0.0, ab, r);
+            gemm(c, true, false, r, n_c, d, 1.0, basis_q(B.get()), d, QK, d, 0.0, ab, r);
             gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           }
           alpha = ab;                             // column 0 = Q^T q0
@@ -1634,7 +1680,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             const long long boff = B->local_rows ? 0 : lo, bld = B->local_rows ? B->dim : d;
             const double* ci = local ? PRED + (size_t)i * ldr : PRED + (size_t)i * d + lo;
             pw::launch_combine_gemv(c, c.stream, gi + lo, r > 0 ? B->Y.p + boff : nullptr, r, ci, a_cur,
-                                    r > 0 ? B->Q.p + boff : nullptr, r, hi - lo,
+                                    r > 0 ? basis_q(B.get()) + boff : nullptr, r, hi - lo,
                                     QN + (size_t)(i + 1) * d + lo, dst, part, 0, bld);
             if (local)
               PW_CUDA(cudaMemcpyAsync(GN + (size_t)i * ldr, gi + lo, sizeof(double) * (size_t)ldr,
@@ -1654,9 +1700,19 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
         for (int i = 0; i < n_c; ++i) {
           prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
           double* a_nxt = (r > 0) ? a_buf[i % 2] : nullptr;
-          pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B ? B->Y.p : nullptr, r,
-                                  PRED + (size_t)i * d, a_cur, B ? B->Q.p : nullptr, r, d,
-                                  QN + (size_t)(i + 1) * d, a_nxt, part);
+          if (r > 0 && B->cq_n1 > 0 && !B->q_valid) {
+            // implicit Q: the pass reduces against the reflectors V (d x kv), then
+            // alpha_{i+1} = Cq^T [qn_{i+1}[0:mr]; V^T qn_{i+1}]
+            const int mr = B->cq_n1, kv = B->cq_n2;
+            double* gv = bGv.p + (size_t)kv * n_c;
+            pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B->Y.p, r, PRED + (size_t)i * d, a_cur,
+                                    B->W.p, kv, d, QN + (size_t)(i + 1) * d, gv, part);
+            pw::launch_implicit_alpha(c, B->Cq.p, mr + kv, QN + (size_t)(i + 1) * d, mr, gv, kv, r, a_nxt);
+          } else {
+            pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B ? B->Y.p : nullptr, r,
+                                    PRED + (size_t)i * d, a_cur, (B && r > 0) ? basis_q(B.get()) : nullptr, r, d,
+                                    QN + (size_t)(i + 1) * d, a_nxt, part);
+          }
           a_cur = a_nxt;
         }
       }

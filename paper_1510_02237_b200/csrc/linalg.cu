@@ -997,6 +997,43 @@ void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const doub
   PW_LAUNCH_CHECK();
 }
 
+// one warp per output: fixed summation order (4 interleaved chains per lane, then the
+// shuffle tree), so the serial sweep stays deterministic
+__global__ void __launch_bounds__(256) implicit_alpha_kernel(const double* __restrict__ C, int ldc,
+                                                             const double* __restrict__ xt, int n1,
+                                                             const double* __restrict__ g, int n2, int r,
+                                                             double* __restrict__ alpha) {
+  const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= r) return;
+  const double* col = C + (size_t)w * ldc;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int i = lane;
+  for (; i + 96 < n1; i += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = fma(col[i + 32 * u], xt[i + 32 * u], s[u]);
+  }
+  for (; i < n1; i += 32) s[0] = fma(col[i], xt[i], s[0]);
+  col += n1;
+  i = lane;
+  for (; i + 96 < n2; i += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = fma(col[i + 32 * u], g[i + 32 * u], s[u]);
+  }
+  for (; i < n2; i += 32) s[0] = fma(col[i], g[i], s[0]);
+  double t = (s[0] + s[1]) + (s[2] + s[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) alpha[w] = t;
+}
+
+void launch_implicit_alpha(Ctx& c, const double* C, int ldc, const double* xt, int n1, const double* g, int n2,
+                           int r, double* alpha) {
+  if (r <= 0) return;
+  implicit_alpha_kernel<<<(r + 7) / 8, 256, 0, c.stream>>>(C, ldc, xt, n1, g, n2, r, alpha);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
 size_t combine_part_doubles(long long d, int r) {
   // >= grid x r for both the 1024-row LSU kernel and the 512-row TMA kernel
   return (size_t)((d + kTmaRows - 1) / kTmaRows) * (size_t)std::max(r, 1);

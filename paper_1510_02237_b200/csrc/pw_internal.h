@@ -254,6 +254,10 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
                          const double* cvec, const double* alpha, const double* Q, int rq,
                          long long d, double* y, double* alpha_next, double* part, int nblk = 0,
                          long long ld = 0);
+// alpha[j] = C[0:n1, j] . xt + C[n1:n1+n2, j] . g for j < r (C column-major, ld ldc): the
+// small step that turns the reflector products V^T x into Q^T x when Q is kept implicit
+void launch_implicit_alpha(Ctx& c, const double* C, int ldc, const double* xt, int n1, const double* g, int n2,
+                           int r, double* alpha);
 void launch_project_gemv(Ctx& c, const double* Q, int r, long long d, const double* v,
                          double* alpha, double* part);
 
