@@ -46,9 +46,16 @@ namespace {
 // carries a 32-double pad: its right halo (the right neighbour's first 4 columns) at
 // [NX, NX + 4), its left halo at [NX + 16, NX + 20) -- TMA-loaded for q, stored over DSMEM by
 // the neighbour's edge threads for s1 / s2.
-template <int NX_, int CL_ = 1>
+// BX columns per thread: 4 (32-byte swizzle, 6-chunk windows) or 8 (64-byte swizzle, 8-chunk
+// windows: a third less shared-memory traffic per cell, half the threads; CL = 1 only).
+// UNI: the three stage groups run ONE copy of the row code with the stage as a warp-uniform
+// run-time value (coefficients in uniform registers), a third of the instruction footprint:
+// with BX = 8 the stage-specialised code (72 KB) left the warps waiting on instruction fetch.
+template <int NX_, int CL_ = 1, int BX_ = 4, bool UNI_ = (BX_ == 8)>
 struct TK {
-  static constexpr int NX = NX_, BX = 4, CL = CL_, NXT = CL * NX;
+  static constexpr int NX = NX_, BX = BX_, CL = CL_, NXT = CL * NX;
+  static constexpr bool UNI = UNI_;
+  static constexpr int NCH = BX / 2 + 4;  // 16-byte chunks of a thread's x window (BX + 8 cells)
   static constexpr int GS = NX / BX;   // threads per stage group
   static constexpr int NT = 3 * GS;
   static constexpr int CH = NX / 2;    // 16-byte chunks per field row
@@ -61,13 +68,22 @@ struct TK {
   // bytes one q row brings: the CTA's 3 x NX cells (+ 3 x 2 halos of 4 cells with CL > 1)
   static constexpr uint32_t ROW_BYTES = (3 * NX + (CL > 1 ? 24 : 0)) * sizeof(double);
   static constexpr int MB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
-  static constexpr int MB_REGS = 65536 / (NT * 168);
+  static constexpr int MB_REGS = 65536 / (NT * (BX == 4 ? 168 : 255));
   static constexpr int MINB = (MB_SMEM < MB_REGS ? MB_SMEM : MB_REGS) < 1 ? 1 : (MB_SMEM < MB_REGS ? MB_SMEM : MB_REGS);
   static_assert(GS % 32 == 0, "stage groups must be whole warps");
+  static_assert(BX == 4 || (BX == 8 && CL == 1), "8 columns per thread: one CTA per row only");
   static_assert((FS * 8) % 256 == 0, "ring field rows keep the 256-byte alignment of the 32-byte swizzle");
 };
 
-__device__ __forceinline__ int swz(int c) { return c ^ ((c >> 3) & 1); }
+// 16-byte chunk c of a ring field row lands at swz(c): TMA's 32-byte swizzle (address bit 4 ^=
+// bit 7) for BX = 4, its 64-byte swizzle (bits 4-5 ^= bits 7-8) for BX = 8.  With 64 bytes per
+// lane the bank group of chunk 4 m + r is (m & 1, r ^ ((m >> 1) & 3)): 8 consecutive lanes hit 8
+// distinct groups for EVERY window chunk r (the 128-byte swizzle conflicts 2-way on the halo
+// chunks: measured, 28 % of the wavefronts).
+template <int BX>
+__device__ __forceinline__ int swz(int c) {
+  return BX == 4 ? c ^ ((c >> 3) & 1) : c ^ ((c >> 3) & 3);
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -136,19 +152,22 @@ __device__ __forceinline__ void ld_chunks(double (&w)[2 * N], const double* row,
     w[2 * j + 1] = t.y;
   }
 }
-__device__ __forceinline__ void st4(double* row, const int* off, const double (&v)[4]) {
-  *reinterpret_cast<double2*>(row + off[0]) = make_double2(v[0], v[1]);
-  *reinterpret_cast<double2*>(row + off[1]) = make_double2(v[2], v[3]);
+template <int BX>
+__device__ __forceinline__ void st4(double* row, const int* off, const double (&v)[BX]) {
+#pragma unroll
+  for (int j = 0; j < BX / 2; ++j) *reinterpret_cast<double2*>(row + off[j]) = make_double2(v[2 * j], v[2 * j + 1]);
 }
-__device__ __forceinline__ void stg4(double* p, const double (&v)[4]) {
-  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
-  *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+template <int BX>
+__device__ __forceinline__ void stg4(double* p, const double (&v)[BX]) {
+#pragma unroll
+  for (int j = 0; j < BX / 2; ++j) *reinterpret_cast<double2*>(p + 2 * j) = make_double2(v[2 * j], v[2 * j + 1]);
 }
 
 // One stage thread's registers: u, p rows k-1..k+1 and v rows k-2..k (slot = row mod 3),
 // h = dv2 v(k-1) for the birth of v row k+1.
+template <int BX>
 struct Acc {
-  double u[3][4], p[3][4], v[3][4], h[4];
+  double u[3][BX], p[3][BX], v[3][BX], h[BX];
 };
 
 // Where the completed rows go: the next stage's ring (S < 2) or the state in HBM (S = 2).
@@ -166,14 +185,15 @@ struct Sink {
 // pw_prop_apply_to_peers) the same bytes into each peer's buffer over NVLink, from the
 // registers that hold them.  A separate instantiation: the peer loop in the plain kernel
 // cost 11 % (64.6 vs 72.4 G/s at c2).
-template <bool PEERS>
-__device__ __forceinline__ void st_out(const Sink& o, double* p, const double (&v)[4]) {
-  stg4(p, v);
+template <bool PEERS, int BX>
+__device__ __forceinline__ void st_out(const Sink& o, double* p, const double (&v)[BX]) {
+  stg4<BX>(p, v);
   if constexpr (PEERS)
   for (int i = 0; i < o.npeer; ++i) {
     double* q = reinterpret_cast<double*>(reinterpret_cast<char*>(p) + o.peer_delta[i]);
-    __stcg(reinterpret_cast<double2*>(q), make_double2(v[0], v[1]));
-    __stcg(reinterpret_cast<double2*>(q + 2), make_double2(v[2], v[3]));
+#pragma unroll
+    for (int j = 0; j < BX / 2; ++j)
+      __stcg(reinterpret_cast<double2*>(q + 2 * j), make_double2(v[2 * j], v[2 * j + 1]));
   }
 }
 
@@ -183,12 +203,14 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   return v;
 }
 // this thread's 4 cells of a ring row (two 16-byte chunks, always 128-bit loads)
-__device__ __forceinline__ void ld_own(double (&b)[4], const double* row, const int* off) {
-  const double2 x = lds2(row + off[0]), y = lds2(row + off[1]);
-  b[0] = x.x;
-  b[1] = x.y;
-  b[2] = y.x;
-  b[3] = y.y;
+template <int BX>
+__device__ __forceinline__ void ld_own(double (&b)[BX], const double* row, const int* off) {
+#pragma unroll
+  for (int j = 0; j < BX / 2; ++j) {
+    const double2 x = lds2(row + off[j]);
+    b[2 * j] = x.x;
+    b[2 * j + 1] = x.y;
+  }
 }
 
 // x stencil of one field row into acc (7 taps, cen / e2m / e2p: the centre and -2 / +2
@@ -196,10 +218,11 @@ __device__ __forceinline__ void ld_own(double (&b)[4], const double* row, const 
 // the centred difference the other fields need (pressure gradient, divergence, mixed damping).
 // (Pairing the antisymmetric advection taps, c_j (w_j - w_{-j}), saves 3 of 38 DP ops per cell
 // and stage but measured slower: 71.1 vs 72.7 G cell-updates/s at c2, more live registers.)
-__device__ __forceinline__ void xstencil(double (&acc)[4], double (&d1)[4], const double (&w)[12], double cen,
+template <int BX>
+__device__ __forceinline__ void xstencil(double (&acc)[BX], double (&d1)[BX], const double (&w)[BX + 8], double cen,
                                          double e2m, double e2p, const StageCoef& C) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < BX; ++c) {
     d1[c] = w[c + 5] - w[c + 3];
     acc[c] = fma(C.cxp[0], w[c + 1], acc[c]);
     acc[c] = fma(e2m, w[c + 2], acc[c]);
@@ -216,9 +239,9 @@ __device__ __forceinline__ void xstencil(double (&acc)[4], double (&d1)[4], cons
 // CL > 1, S < 2: the edge threads also store their outer 4 cells into the neighbouring CTAs'
 // halos of the same ring row (DSMEM): g = 0's first cells are the left neighbour's right
 // halo, the last thread's last cells the right neighbour's left halo
-template <int NX, int FS, int CL>
-__device__ __forceinline__ void st_ring(double* row, const int* woff2, const double (&v)[4], int g, const Sink& o) {
-  st4(row, woff2, v);
+template <int NX, int FS, int CL, int BX>
+__device__ __forceinline__ void st_ring(double* row, const int* woff2, const double (&v)[BX], int g, const Sink& o) {
+  st4<BX>(row, woff2, v);
   if constexpr (CL > 1) {
     if (g == 0) {
       double2* h = reinterpret_cast<double2*>(peer_smem(row + NX, o.left));
@@ -232,74 +255,87 @@ __device__ __forceinline__ void st_ring(double* row, const int* woff2, const dou
   }
 }
 
-template <int NX, int S, int PH, bool PEERS, int FS = NX, int CL = 1>
-__device__ __forceinline__ void row_step(Acc& A, const double* in, const double* qb, const int* woff,
-                                         const StageCoef& C, const Sink& o, int k, int g = 0) {
+// S_ >= 0: the stage at compile time; S_ < 0: the stage is the warp-uniform run-time `srt`
+// (one copy of the code for the three stage groups; stage 1's missing q base is a zero row in
+// registers, so only the sign of a zero can differ from the specialised code)
+template <int NX, int S_, int PH, bool PEERS, int FS = NX, int CL = 1, int BX = 4>
+__device__ __forceinline__ void row_step(Acc<BX>& A, const double* in, const double* qb, const int* woff,
+                                         const StageCoef& C, const Sink& o, int k, int g = 0, int srt = 0) {
   constexpr int NXT = NX * CL;
+  constexpr bool RT = S_ < 0;
+  const int S = RT ? srt : S_;
+  constexpr int NCH = BX / 2 + 4;
   constexpr int U0 = (PH + 2) % 3, U1 = PH, U2 = (PH + 1) % 3;  // u, p: rows k-1, k, k+1
   constexpr int V0 = (PH + 1) % 3, V1 = (PH + 2) % 3, V2 = PH;  // v: rows k-2 (-> k+1), k-1, k
-  double w[12], d1[4];
+  double w[BX + 8], d1[BX];
   // ---- v row k: x stencil of row k; completes v(k-2); births v(k+1); u_y-mixed / p_y terms
-  ld_chunks<6>(w, in + FS, woff);
+  ld_chunks<NCH>(w, in + FS, woff);
   // v: cxv equals cxp off the centre; the +-2 taps are plain advection
-  xstencil(A.v[V2], d1, w, C.cxv[3], C.cxp[1], C.cxp[5], C);
+  xstencil<BX>(A.v[V2], d1, w, C.cxv[3], C.cxp[1], C.cxp[5], C);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) A.v[V0][c] = fma(C.dv2, w[c + 4], A.v[V0][c]);
-  if constexpr (S < 2) {
-    st_ring<NX, FS, CL>(o.ring + ((PH + 1) % 3) * (3 * FS) + FS, woff + 2, A.v[V0], g, o);
+  for (int c = 0; c < BX; ++c) A.v[V0][c] = fma(C.dv2, w[c + 4], A.v[V0][c]);
+  if (S < 2) {
+    st_ring<NX, FS, CL, BX>(o.ring + ((PH + 1) % 3) * (3 * FS) + FS, woff + 2, A.v[V0], g, o);
   } else {
-    if (k - 2 >= 0 && k - 2 < o.TY) st_out<PEERS>(o, o.g + o.n + (long long)(k - 2) * NXT, A.v[V0]);
+    if (k - 2 >= 0 && k - 2 < o.TY) st_out<PEERS, BX>(o, o.g + o.n + (long long)(k - 2) * NXT, A.v[V0]);
   }
   {
-    double b[4];
-    if constexpr (S > 0) ld_own(b, qb + FS, woff + 2);
+    double b[BX];
+    if (S > 0) ld_own<BX>(b, qb + FS, woff + 2);
+    else if constexpr (RT) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      A.v[V0][c] = (S > 0) ? b[c] + A.h[c] : A.h[c];  // v(k+1) = q + dv2 v(k-1)
+      for (int c = 0; c < BX; ++c) b[c] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < BX; ++c) {
+      A.v[V0][c] = (RT || S > 0) ? b[c] + A.h[c] : A.h[c];  // v(k+1) = q + dv2 v(k-1)
       A.h[c] = C.dv2 * w[c + 4];
     }
   }
   {
-    double bu[4], bp[4];
-    if constexpr (S > 0) {
-      ld_own(bu, qb, woff + 2);
-      ld_own(bp, qb + 2 * FS, woff + 2);
+    double bu[BX], bp[BX];
+    if (S > 0) {
+      ld_own<BX>(bu, qb, woff + 2);
+      ld_own<BX>(bp, qb + 2 * FS, woff + 2);
+    } else if constexpr (RT) {
+#pragma unroll
+      for (int c = 0; c < BX; ++c) bu[c] = bp[c] = 0.0;
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < BX; ++c) {
       // mixed damping of u (cuv v_x) into rows k-1 (+) and k+1 (-); p_y of p into p(k-1), p(k+1)
       A.u[U0][c] = fma(C.cuv, d1[c], A.u[U0][c]);
-      A.u[U2][c] = (S > 0) ? fma(-C.cuv, d1[c], bu[c]) : -C.cuv * d1[c];
+      A.u[U2][c] = (RT || S > 0) ? fma(-C.cuv, d1[c], bu[c]) : -C.cuv * d1[c];
       A.p[U0][c] = fma(C.pv, w[c + 4], A.p[U0][c]);
-      A.p[U2][c] = (S > 0) ? fma(-C.pv, w[c + 4], bp[c]) : -C.pv * w[c + 4];
+      A.p[U2][c] = (RT || S > 0) ? fma(-C.pv, w[c + 4], bp[c]) : -C.pv * w[c + 4];
     }
   }
-  if constexpr (S < 2) {
+  if (S < 2) {
     double* r = o.ring + ((PH + 2) % 3) * (3 * FS);
-    st_ring<NX, FS, CL>(r, woff + 2, A.u[U0], g, o);
-    st_ring<NX, FS, CL>(r + 2 * FS, woff + 2, A.p[U0], g, o);
+    st_ring<NX, FS, CL, BX>(r, woff + 2, A.u[U0], g, o);
+    st_ring<NX, FS, CL, BX>(r + 2 * FS, woff + 2, A.p[U0], g, o);
   } else {
     if (k - 1 >= 0 && k - 1 < o.TY) {
       double* gp = o.g + (long long)(k - 1) * NXT;
-      st_out<PEERS>(o, gp, A.u[U0]);
-      st_out<PEERS>(o, gp + 2 * o.n, A.p[U0]);
+      st_out<PEERS, BX>(o, gp, A.u[U0]);
+      st_out<PEERS, BX>(o, gp + 2 * o.n, A.p[U0]);
     }
   }
   // ---- u row k: x stencil (advection + the symmetric x damping at +-2 and the centre);
   //      u_x for p(k) and the mixed damping of v(k-1), v(k+1)
-  double t2[4];
-  ld_chunks<6>(w, in, woff);
-  xstencil(A.u[U1], d1, w, C.cxu[3], C.cxu[1], C.cxu[5], C);
+  double t2[BX];
+  ld_chunks<NCH>(w, in, woff);
+  xstencil<BX>(A.u[U1], d1, w, C.cxu[3], C.cxu[1], C.cxu[5], C);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < BX; ++c) {
     A.p[U1][c] = fma(C.pu, d1[c], A.p[U1][c]);
     t2[c] = C.cvu * d1[c];
   }
   // ---- p row k: x stencil; p_x for u(k), p_y for v(k-1), v(k+1)
-  ld_chunks<6>(w, in + 2 * FS, woff);
-  xstencil(A.p[U1], d1, w, C.cxp[3], C.cxp[1], C.cxp[5], C);
+  ld_chunks<NCH>(w, in + 2 * FS, woff);
+  xstencil<BX>(A.p[U1], d1, w, C.cxp[3], C.cxp[1], C.cxp[5], C);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < BX; ++c) {
     A.u[U1][c] = fma(C.pu, d1[c], A.u[U1][c]);  // pgx == pu
     t2[c] = fma(C.pv, w[c + 4], t2[c]);         // pgy == pv
     A.v[V1][c] += t2[c];
@@ -347,7 +383,7 @@ __device__ __forceinline__ void issue(double* ring, uint64_t* full, const Item& 
 
 // One tick: the CTA barrier, the q row two ticks ahead, then stage S's row k = t - lag.
 template <class K, int I, bool PEERS>
-__device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const Item& it, const FusedParams& P,
+__device__ __forceinline__ void tick(Acc<K::BX>& A, double* ring, uint64_t* full, const Item& it, const FusedParams& P,
                                      int S, int t, const int* woff, const Sink& o, bool producer, int g) {
   constexpr int NX = K::NX;
   if constexpr (K::CL > 1) cluster_sync();  // the neighbours' halo stores of the last tick
@@ -357,22 +393,36 @@ __device__ __forceinline__ void tick(Acc& A, double* ring, uint64_t* full, const
   double* r1 = ring + K::NQ * K::SLOT;
   double* r2 = r1 + K::N1 * K::SLOT;
   // k = t - lag with lag in {6, 9, 12}: k mod 3 = t mod 3 = I
-  if (S == 0) {
+  if constexpr (K::UNI) {  // one copy of the row code, the stage a warp-uniform value
+    const int k = t - 6 - 3 * S;
+    if (k < 2 * S - 6 || k > it.TY + 5 - 2 * S) return;
+    const double* in;
+    const double* qb = nullptr;
+    if (S == 0) {
+      const uint32_t s = qslot(it.seq, k);
+      mbar_wait(full + s, qpar(it.seq, k));
+      in = q + (size_t)s * K::SLOT;
+    } else {
+      in = (S == 1 ? r1 : r2) + (I * K::SLOT);
+      qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
+    }
+    row_step<NX, -1, I, PEERS, K::FS, K::CL, K::BX>(A, in, qb, woff, P.st[S], o, k, g, S);
+  } else if (S == 0) {
     const int k = t - 6;
     if (k > it.TY + 5) return;
     const uint32_t s = qslot(it.seq, k);
     mbar_wait(full + s, qpar(it.seq, k));
-    row_step<NX, 0, I, PEERS, K::FS, K::CL>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k, g);
+    row_step<NX, 0, I, PEERS, K::FS, K::CL, K::BX>(A, q + (size_t)s * K::SLOT, nullptr, woff, P.st[0], o, k, g);
   } else if (S == 1) {
     const int k = t - 9;
     if (k < -4 || k > it.TY + 3) return;
     const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
-    row_step<NX, 1, I, PEERS, K::FS, K::CL>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k, g);
+    row_step<NX, 1, I, PEERS, K::FS, K::CL, K::BX>(A, r1 + (I * K::SLOT), qb, woff, P.st[1], o, k, g);
   } else {
     const int k = t - 12;
     if (k < -2 || k > it.TY + 1) return;
     const double* qb = q + (size_t)qslot(it.seq, k + 1) * K::SLOT;
-    row_step<NX, 2, I, PEERS, K::FS, K::CL>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k, g);
+    row_step<NX, 2, I, PEERS, K::FS, K::CL, K::BX>(A, r2 + (I * K::SLOT), qb, woff, P.st[2], o, k, g);
   }
 }
 
@@ -401,16 +451,16 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
   const int g = tid - S * K::GS;
   // window chunk offsets: cols [4g - 4, 4g + 8) as 6 chunks; one CTA per row: wrapped
   // periodically; CL > 1: the outer chunks of the edge threads are the row's halos
-  int woff[6];
+  int woff[K::NCH];
 #pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    int c = 2 * g - 2 + j;
+  for (int j = 0; j < K::NCH; ++j) {
+    int c = (K::BX / 2) * g - 2 + j;
     if constexpr (CL == 1) {
       c += (c < 0) ? K::CH : 0;
       c -= (c >= K::CH) ? K::CH : 0;
-      woff[j] = 2 * swz(c);
+      woff[j] = 2 * swz<K::BX>(c);
     } else {
-      woff[j] = c < 0 ? K::HL + 2 * (c + 2) : (c >= K::CH ? K::HR + 2 * (c - K::CH) : 2 * swz(c));
+      woff[j] = c < 0 ? K::HL + 2 * (c + 2) : (c >= K::CH ? K::HR + 2 * (c - K::CH) : 2 * swz<K::BX>(c));
     }
   }
   const bool producer = (tid == 0);
@@ -475,14 +525,14 @@ __global__ void __launch_bounds__(K::NT, K::MINB) rk3_mtma_kernel(
       o.peer_delta = P.peer_delta;
     }
     o.g = (to_out ? out + (long long)b * ld_out : tmp + (long long)b * ld_tmp) + (long long)it.y0 * K::NXT +
-          (long long)crank * NX + 4 * g;
+          (long long)crank * NX + K::BX * g;
     if (producer) {  // prologue: q rows -6 and -5 (stage 1's ticks 0 and 1)
       issue<K>(ring, full, it, ny, -6);
       issue<K>(ring, full, it, ny, -5);
     }
-    Acc A;
+    Acc<K::BX> A;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < K::BX; ++c) {
 #pragma unroll
       for (int r = 0; r < 3; ++r) A.u[r][c] = A.p[r][c] = A.v[r][c] = 0.0;
       A.h[c] = 0.0;
@@ -527,16 +577,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // view {4, nx/4, ny, 3, batch} of a batch of states (ld doubles apart); box = {4, bx4, 1, bf, 1}
 // (one grid row of bx4 4-cell chunks of bf fields), 32-byte swizzle -- or none for the halo
 // boxes, which the edge threads read unswizzled
+// `inner` cells per innermost box row: 4 with the 32-byte swizzle (BX = 4), 8 with the 64-byte
+// swizzle (BX = 8); bx4 counts inner-sized column groups
 CUtensorMap row_map(const double* base, int nx, int ny, long long ld, int batch, int bx4 = 0, int bf = 3,
-                    bool swizzle = true) {
+                    bool swizzle = true, int inner = 4) {
   CUtensorMap m;
-  const cuuint64_t dims[5] = {4, (cuuint64_t)nx / 4, (cuuint64_t)ny, 3, (cuuint64_t)batch};
-  const cuuint64_t strides[4] = {32, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8, (cuuint64_t)ld * 8};
-  const cuuint32_t box[5] = {4, (cuuint32_t)(bx4 > 0 ? bx4 : nx / 4), 1, (cuuint32_t)bf, 1};
+  const cuuint64_t dims[5] = {(cuuint64_t)inner, (cuuint64_t)(nx / inner), (cuuint64_t)ny, 3, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)inner * 8, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8,
+                                 (cuuint64_t)ld * 8};
+  const cuuint32_t box[5] = {(cuuint32_t)inner, (cuuint32_t)(bx4 > 0 ? bx4 : nx / inner), 1, (cuuint32_t)bf, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 swizzle ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 !swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                          : (inner == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PW_CHECK(r == CUDA_SUCCESS, PW_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
@@ -568,10 +622,11 @@ void launch_cfg(Ctx& c, const FusedParams& fp, const double* in, double* out, do
   nseg = std::max(1, std::min(nseg, fp.ny / 16));
   // CL = 1: one box per row (3 fields); CL > 1: per field, the CTA's NX columns, plus
   // 4-cell halo boxes (no swizzle)
-  const int bx4 = K::NX / 4, bf = K::CL == 1 ? 3 : 1;
-  const CUtensorMap m_in = row_map(in, fp.nx, fp.ny, fp.ld_in, batch, bx4, bf);
-  const CUtensorMap m_out = row_map(out, fp.nx, fp.ny, fp.ld_out, batch, bx4, bf);
-  const CUtensorMap m_tmp = row_map(tmp, fp.nx, fp.ny, d, batch, bx4, bf);
+  constexpr int inner = K::BX == 4 ? 4 : 8;
+  const int bx4 = K::NX / inner, bf = K::CL == 1 ? 3 : 1;
+  const CUtensorMap m_in = row_map(in, fp.nx, fp.ny, fp.ld_in, batch, bx4, bf, true, inner);
+  const CUtensorMap m_out = row_map(out, fp.nx, fp.ny, fp.ld_out, batch, bx4, bf, true, inner);
+  const CUtensorMap m_tmp = row_map(tmp, fp.nx, fp.ny, d, batch, bx4, bf, true, inner);
   const CUtensorMap h_in = K::CL > 1 ? row_map(in, fp.nx, fp.ny, fp.ld_in, batch, 1, 1, false) : m_in;
   const CUtensorMap h_out = K::CL > 1 ? row_map(out, fp.nx, fp.ny, fp.ld_out, batch, 1, 1, false) : m_out;
   const CUtensorMap h_tmp = K::CL > 1 ? row_map(tmp, fp.nx, fp.ny, d, batch, 1, 1, false) : m_tmp;
@@ -611,6 +666,18 @@ bool mtma_supported(int nx, int ny, long long ld_in, long long ld_out, const voi
 
 void launch_rk3_mtma(Ctx& c, const FusedParams& fp, const double* in, double* out, double* tmp, int batch,
                      int nsteps, long long d, int* sync) {
+  // PW_MARCH_BX=8: 8 columns per thread (128-byte swizzle); nx = 128 has too few columns for it
+  if (env_int2("PW_MARCH_BX", 4) == 8) switch (fp.nx) {
+    case 256: return launch_cfg<TK<256, 1, 8>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 512: return launch_cfg<TK<512, 1, 8>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    default: break;
+  }
+  // PW_MARCH_UNI=1: 4 columns per thread with the one-copy row code (A/B runs)
+  if (env_int2("PW_MARCH_UNI", 0) == 1) switch (fp.nx) {
+    case 256: return launch_cfg<TK<256, 1, 4, true>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    case 512: return launch_cfg<TK<512, 1, 4, true>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
+    default: break;
+  }
   switch (fp.nx) {
     case 128: return launch_cfg<TK<128>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
     case 256: return launch_cfg<TK<256>>(c, fp, in, out, tmp, batch, nsteps, d, sync);
