@@ -177,15 +177,24 @@ class FusedShardedFine:
     (pw_prop_apply_to_peers).  The last RK3 step of the row-marching kernel stores
     each output row into this rank's gather buffer and into every peer's, over
     NVLink, while the other rows are still being computed.  There is no NCCL call
-    on the data path.  Two barriers per call order the buffer reuse: one before the
-    stores (everyone has read the previous contents) and one after (every rank's
-    stores have landed).
+    on the data path.
+
+    The gather buffer has two halves used by alternate calls, so ONE barrier per call
+    (after the stores: every rank's rows have landed everywhere) also orders the reuse:
+    a rank storing into half h at call k is past call k-1's barrier, which every peer
+    joined only after its stream had consumed half h at call k-2.  Under NCCL that
+    barrier is stream-ordered (a one-element all-reduce enqueued behind the kernel; the
+    host does not block); under gloo (CPU rendezvous, the one-GPU tests) it is a host
+    synchronise + barrier.
     """
 
     def __init__(self, prop, group=None):
         self.prop = prop
         self.group = group
         self._buf = None
+        self._cap = 0
+        self._calls = 0
+        self._token = None
 
     @property
     def world(self):
@@ -196,10 +205,11 @@ class FusedShardedFine:
         return tdist.get_rank(self.group) if tdist.is_initialized() else 0
 
     def _buffer(self, numel):
-        if self._buf is None or self._buf.numel < numel:
+        if self._buf is None or self._cap < numel:
             if self._buf is not None:
                 self._buf.close()
-            self._buf = PeerGather(self.prop.ctx, numel, self.group)
+            self._buf = PeerGather(self.prop.ctx, 2 * numel, self.group)  # collective (host rendezvous)
+            self._cap, self._calls = numel, 0
         return self._buf
 
     def close(self):
@@ -207,22 +217,31 @@ class FusedShardedFine:
             self._buf.close()
             self._buf = None
 
+    def _barrier(self, stream):
+        """Every rank's stores of this call are complete and visible on every rank."""
+        if tdist.get_backend(self.group) == "nccl":
+            if self._token is None:
+                self._token = torch.zeros(1, dtype=torch.float32, device=stream.device)
+            tdist.all_reduce(self._token, group=self.group)  # ordered on the current stream
+        else:
+            stream.synchronize()
+            tdist.barrier(group=self.group)
+
     def __call__(self, qk: torch.Tensor) -> torch.Tensor:
         world, rank = self.world, self.rank
         n, d = qk.shape
         if world == 1:
             return self.prop.apply(qk)
         buf = self._buffer(n * d)
+        base = (self._calls & 1) * self._cap
+        self._calls += 1
         lo, hi = shard_range(n, rank, world)
         stream = torch.cuda.current_stream(qk.device)
-        stream.synchronize()
-        tdist.barrier(group=self.group)
         if hi > lo:
-            out = buf.local[lo * d:hi * d].view(hi - lo, d)
-            self.prop.apply_to_peers(qk[lo:hi], out, [p + lo * d * 8 for p in buf.peer_ptrs])
-        stream.synchronize()
-        tdist.barrier(group=self.group)
-        return buf.local[: n * d].view(n, d).clone()
+            out = buf.local[base + lo * d:base + hi * d].view(hi - lo, d)
+            self.prop.apply_to_peers(qk[lo:hi], out, [p + (base + lo * d) * 8 for p in buf.peer_ptrs])
+        self._barrier(stream)
+        return buf.local[base:base + n * d].view(n, d).clone()
 
     def batch(self, states):
         t = torch.as_tensor(states)

@@ -131,7 +131,7 @@ def _gather_worker(rank, world, port, out_q):
         for nx, ny, n in ((256, 64, 5), (1024, 32, 3)):  # fused epilogue; copy fallback
             prop = fine_prop(nx, ny, 3)
             fused = FusedShardedFine(prop)
-            for seed in (1, 2):  # the second call reuses the mapped buffers
+            for seed in (1, 2, 3, 4):  # alternate halves of the gather buffer; calls 3 and 4 reuse them
                 x = states(nx, ny, n, seed)
                 got = fused(x)
                 want = prop.apply(x)
