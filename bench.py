@@ -26,6 +26,7 @@ scaling, no data-path collective -- slices are independent).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -249,7 +250,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def parareal_window(name="c3", warm=True, group=None):
+def parareal_window(name="c3", warm=True, group=None, repeats=None):
     """One KSE-Parareal window of config `name` (c3: 512^2, P=64, K=5; c4: 1024^2, P=256,
     K=4): per-iteration device time and phases.  Under torchrun (`group`) the fine sweep
     is slice-sharded over the ranks (dist.ShardedFine, NCCL all-gather of the end states)
@@ -265,6 +266,8 @@ def parareal_window(name="c3", warm=True, group=None):
     from paper_1510_02237_b200.physics import ModelSpec
 
     wl = harness.WORKLOADS[name]
+    if repeats is None:
+        repeats = 3 if name == "c3" else 1
     g = build_grid(wl.n, wl.n)
     vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
     fine = SlicePropagator(make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), g, 0.5),
@@ -275,25 +278,36 @@ def parareal_window(name="c3", warm=True, group=None):
     if warm:
         # warm-up: first-use module loads (cuSOLVER/cuBLAS lazy loading) and pool allocations
         kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True, group=group)
-    tm = Timings()
-    if group is not None:
-        torch.distributed.barrier(group)
-    torch.cuda.synchronize()
-    fine.ctx.mem_stats(reset=True)
-    torch.cuda.reset_peak_memory_stats()
-    t0 = time.perf_counter()
-    ends, res, sub = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm, return_device=True,
-                               group=group)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
+    # the window is timed `repeats` times (c3: 3 x 0.27 s; c4 once) and the fastest run is
+    # reported with every sample next to it: the wall clock around a window also sees the
+    # host (320 serial steps are enqueued from one thread), which varies from box to box
+    samples, best = [], None
     n_ranks = 1
-    if group is not None:
-        t = torch.tensor([wall], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=group)
-        wall = float(t.item())
-        n_ranks = torch.distributed.get_world_size(group)
+    for _ in range(repeats):
+        tm_i = Timings()
+        if group is not None:
+            torch.distributed.barrier(group)
+        torch.cuda.synchronize()
+        fine.ctx.mem_stats(reset=True)
+        torch.cuda.reset_peak_memory_stats()
+        t0 = time.perf_counter()
+        out_i = kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, timings=tm_i, return_device=True, group=group)
+        torch.cuda.synchronize()
+        wall_i = time.perf_counter() - t0
+        if group is not None:
+            t = torch.tensor([wall_i], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=group)
+            wall_i = float(t.item())
+            n_ranks = torch.distributed.get_world_size(group)
+        samples.append(wall_i)
+        if best is None or wall_i < best[0]:
+            # only the small results: a kept Subspace would pin its multi-GB basis buffers and
+            # send the next window to the driver for fresh memory (+60 ms at c3)
+            best = (wall_i, tm_i, [float(r) for r in out_i[1]], list(getattr(out_i[2], "ranks_history", None) or []))
+        del out_i
+        gc.collect()
+    wall, tm, res, ranks = best
     d = q0.numel()
-    ranks = getattr(sub, "ranks_history", None) or []
     # roofline per phase: fine 48 B per cell-update; the serial correction
     # streams D and Q (2 r d 8 B) plus g, c, y (3 d 8 B) per step -- the coarse G it
     # interleaves with is L2-resident and adds no HBM bytes
@@ -312,9 +326,9 @@ def parareal_window(name="c3", warm=True, group=None):
                                               "time (the latency-bound coarse G included)"}}
     extra = {"reference_window": c3_reference_window()} if name == "c3" else {}
     return {**extra, "workload": f"{name}: {wl.n}^2, P={wl.n_p}, K={wl.n_it} KSE-Parareal window",
-            "window_s": wall, "iteration_s": wall / wl.n_it,
+            "window_s": wall, "window_s_samples": samples, "iteration_s": wall / wl.n_it,
             "phases_s": {"coarse_and_correction": tm.coarse, "fine": tm.fine, "qr": tm.qr},
-            "ranks": getattr(sub, "ranks_history", None), "residuals": [float(r) for r in res],
+            "ranks": ranks or None, "residuals": res,
             "fine_cell_updates_per_s": wl.n_p * wl.n_it * fine.nsteps * d / 3 / tm.fine if tm.fine else None,
             "memory_gib": _memory_gib(fine.ctx),
             "roofline": roof, "warm": warm, "n_gpus": n_ranks,
@@ -549,30 +563,7 @@ def run_ours(args, rank, world, local_rank):
                   "note": "K1 is bound by on-chip (shared-memory) bandwidth, not by HBM: every stage re-reads "
                           "3x-overlapping x-windows from shared memory; see DESIGN.md K1"}
 
-    extra = {}
-    if world > 1 and args.parareal and not comm_selftest(dist):
-        extra["parareal"] = {"error": "row-shard collective self-test failed; Parareal windows skipped"}
-    elif world > 1 and args.parareal:
-        try:
-            extra["parareal"] = parareal_window("c3", group=dist.group.WORLD)
-        except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
-            extra["parareal"] = {"error": f"{type(e).__name__}: {e}"}
-        if args.c4:
-            del x, out, flush
-            torch.cuda.empty_cache()
-            try:
-                extra["parareal_c4"] = parareal_window("c4", group=dist.group.WORLD)
-            except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
-                extra["parareal_c4"] = {"error": f"{type(e).__name__}: {e}"}
-    if rank == 0 and world == 1 and args.parareal:
-        extra["parareal"] = parareal_c3(local_rank)
-        if args.c4:
-            del x, out, xd, yd, flush, pinned_in, pinned_out, copy
-            torch.cuda.empty_cache()
-            try:
-                extra["parareal_c4"] = parareal_window("c4")
-            except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
-                extra["parareal_c4"] = {"error": f"{type(e).__name__}: {e}"}
+    line = None
     if rank == 0:
         line = {
             "metric": "fine RK-3 fp64 cell-updates/s", "value": value, "unit": "cell-updates/s",
@@ -606,10 +597,59 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline()
-        line.update(extra)
-        print(json.dumps(line), flush=True)
+    # The headline line is complete here.  The Parareal windows that follow are extras: under
+    # torchrun (N > 1) they run collectives, and a rank that fails or stalls inside one would
+    # leave the others waiting -- so a watchdog prints the line without them and ends the
+    # process if they do not finish in time (PW_BENCH_WINDOW_TIMEOUT seconds, default 420).
+    import threading
+
+    emitted = threading.Lock()
+    windows_done = threading.Event()
+
+    def emit():
+        if rank == 0 and emitted.acquire(blocking=False):
+            line.update(extra)
+            print(json.dumps(line), flush=True)
+
+    extra = {}
+
+    def watchdog(limit):
+        if not windows_done.wait(limit):
+            extra.setdefault("parareal", {"error": f"multi-rank Parareal windows did not finish within {limit:.0f} s; "
+                                                   "headline printed without them"})
+            emit()
+            os._exit(0)
+
+    if world > 1 and args.parareal:
+        threading.Thread(target=watchdog, args=(float(os.environ.get("PW_BENCH_WINDOW_TIMEOUT", "420")),),
+                         daemon=True).start()
+    if world > 1 and args.parareal and not comm_selftest(dist):
+        extra["parareal"] = {"error": "row-shard collective self-test failed; Parareal windows skipped"}
+    elif world > 1 and args.parareal:
+        try:
+            extra["parareal"] = parareal_window("c3", group=dist.group.WORLD)
+        except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
+            extra["parareal"] = {"error": f"{type(e).__name__}: {e}"}
+        if args.c4:
+            del x, out, flush
+            torch.cuda.empty_cache()
+            try:
+                extra["parareal_c4"] = parareal_window("c4", group=dist.group.WORLD)
+            except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
+                extra["parareal_c4"] = {"error": f"{type(e).__name__}: {e}"}
+    if rank == 0 and world == 1 and args.parareal:
+        extra["parareal"] = parareal_c3(local_rank)
+        if args.c4:
+            del x, out, xd, yd, flush, pinned_in, pinned_out, copy
+            torch.cuda.empty_cache()
+            try:
+                extra["parareal_c4"] = parareal_window("c4")
+            except Exception as e:  # noqa: BLE001 - reported, not fatal for the headline line
+                extra["parareal_c4"] = {"error": f"{type(e).__name__}: {e}"}
+    windows_done.set()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    emit()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -226,7 +226,9 @@ def run_windowed(cfg: PitConfig, q0: State, t_end: float, t_start: float = 0.0,
     seed = _upload(ctx, q0)
     report.record_device(0, t_start, ctx, seed, grid, kind, state=q0)
     for w in range(1, n_windows + 1):
-        ends, residuals, _ = _run_window(cfg, cfg.mode, seed.reshape(-1), props, report.timings)
+        # [:2] drops the window's Subspace at once: kept in a name until the next call returns,
+        # it would pin its d x m basis buffers while the next window allocates its own
+        ends, residuals = _run_window(cfg, cfg.mode, seed.reshape(-1), props, report.timings)[:2]
         t = t_start + w * span
         states = _as_states(ends, grid, kind)
         report.window_endpoints.append(states)
