@@ -240,7 +240,7 @@ def run_reference(args, rank, world):
     line = {"metric": "fine RK-3 fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "impl": "reference", "dtype": "f64", "data": "synthetic",
-            "config": bench_config(1),
+            "config": bench_config(world),
             "implementation": "CPU port of the reference kernels (oracle/pw_oracle.c, reference operation "
                               "order, all host threads); the reference itself is Python and is not on the "
                               "GPU box",
