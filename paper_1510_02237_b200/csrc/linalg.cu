@@ -142,6 +142,137 @@ __global__ void __launch_bounds__(kQrThreads) pqr_kernel(double* A, int mr, int 
   }
 }
 
+// The same factorisation with ONE grid barrier per column (default; PW_PQR=2 selects the
+// two-barrier kernel above for A/B runs).  After the barrier that publishes the updated columns
+// and norms, EVERY block finds the pivot and forms the reflector of the pivot column itself
+// (warp 0, from the unscaled column in global memory into shared memory): the same
+// instruction sequence on the same operands in every block, so the blocks agree bit for bit
+// and the second barrier (pivot owner -> everyone) disappears.  The owner's in-place write of
+// the scaled reflector, beta, tau and the pivot index is deferred until after the next barrier,
+// when no block reads the unscaled column any more (the reflector buffer is double-buffered by
+// step parity).  Results are bitwise equal to pqr_kernel (tests/test_gpu_tsqr.py).
+constexpr int kQrMaxRows = 2048;
+__global__ void __launch_bounds__(kQrThreads) pqr1_kernel(double* A, int mr, int m, int* piv,
+                                                          double* tau, double* norms, double* diag) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned done[64];  // m <= 2048
+  __shared__ double red_v[kQrWarps];
+  __shared__ int red_i[kQrWarps];
+  __shared__ int s_p;
+  __shared__ double s_t[2], s_beta[2];
+  __shared__ double vbuf[2][kQrMaxRows];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gwarp = blockIdx.x * kQrWarps + warp;
+  const int nwarps = gridDim.x * kQrWarps;
+  const int steps = mr < m ? mr : m;
+  for (int k = threadIdx.x; k < 64; k += blockDim.x) done[k] = 0u;
+  for (int c = gwarp; c < m; c += nwarps) {
+    const double* col = A + (size_t)c * mr;
+    double s = 0.0;
+    for (int i = lane; i < mr; i += 32) s = fma(col[i], col[i], s);
+    s = warp_sum(s);
+    if (lane == 0) norms[c] = sqrt(s);
+  }
+  grid.sync();
+  int p_prev = -1;
+  for (int j = 0; j <= steps; ++j) {
+    // deferred in-place write of step j-1's reflector by its owner block (the column is done:
+    // nobody reads it any more)
+    if (j > 0 && (int)blockIdx.x == p_prev % (int)gridDim.x) {
+      double* col = A + (size_t)p_prev * mr;
+      const double* v = vbuf[(j - 1) & 1];
+      for (int i = j + threadIdx.x; i < mr; i += blockDim.x) col[i] = v[i];
+      if (threadIdx.x == 0) {
+        col[j - 1] = s_beta[(j - 1) & 1];
+        tau[j - 1] = s_t[(j - 1) & 1];
+        piv[j - 1] = p_prev;
+        diag[j - 1] = fabs(s_beta[(j - 1) & 1]);
+      }
+    }
+    if (j == steps) break;
+    // pivot: max remaining norm, lowest index on ties (idamax semantics)
+    double best = -1.0;
+    int bi = m;
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      if (done[c >> 5] & (1u << (c & 31))) continue;
+      const double v = norms[c];
+      if (v > best || (v == best && c < bi)) { best = v; bi = c; }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const double ov = __shfl_xor_sync(FULL, best, off);
+      const int oi = __shfl_xor_sync(FULL, bi, off);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[warp] = best; red_i[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = red_v[0];
+      int bidx = red_i[0];
+      for (int w = 1; w < kQrWarps; ++w)
+        if (red_v[w] > b || (red_v[w] == b && red_i[w] < bidx)) { b = red_v[w]; bidx = red_i[w]; }
+      s_p = bidx;
+      done[bidx >> 5] |= (1u << (bidx & 31));
+    }
+    __syncthreads();
+    const int p = s_p;
+    double* vj = vbuf[j & 1];
+    // Householder reflector of column p, rows j..mr-1 (dlarfg), formed by every block
+    if (warp == 0) {
+      const double* col = A + (size_t)p * mr;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < mr; i += 32) s = fma(col[i], col[i], s);
+      s = warp_sum(s);
+      const double alpha = col[j];
+      double t = 0.0, beta = alpha;
+      if (s != 0.0) {
+        const double xnorm = sqrt(s);
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        t = (beta - alpha) / beta;
+        const double scal = 1.0 / (alpha - beta);
+        for (int i = j + 1 + lane; i < mr; i += 32) vj[i] = col[i] * scal;
+      } else {
+        for (int i = j + 1 + lane; i < mr; i += 32) vj[i] = col[i];
+      }
+      if (lane == 0) {
+        s_t[j & 1] = t;
+        s_beta[j & 1] = beta;
+      }
+    }
+    __syncthreads();
+    // apply H_j to the remaining columns; recompute their trailing norms
+    const double t = s_t[j & 1];
+    for (int c = gwarp; c < m; c += nwarps) {
+      if (done[c >> 5] & (1u << (c & 31))) continue;
+      double* col = A + (size_t)c * mr;
+      double w = 0.0;
+      for (int i = j + 1 + lane; i < mr; i += 32) w = fma(vj[i], col[i], w);
+      w = warp_sum(w) + col[j];
+      const double tw = t * w;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < mr; i += 32) {
+        const double x = col[i] - tw * vj[i];
+        col[i] = x;
+        s = fma(x, x, s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        col[j] -= tw;
+        norms[c] = sqrt(s);
+      }
+    }
+    p_prev = p;
+    grid.sync();
+  }
+  // columns never pivoted (m > mr): record them after the pivoted ones
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int k = steps;
+    for (int c = 0; c < m && k < m; ++c)
+      if (!(done[c >> 5] & (1u << (c & 31)))) piv[k++] = c;
+  }
+}
+
 // Q2[:, c] = H_0 ... H_c e_c  (c < r), one warp per column, x staged in smem
 constexpr int kQ2Warps = 4;
 __global__ void __launch_bounds__(kQ2Warps * 32) form_q2_kernel(const double* A, int mr,
@@ -827,8 +958,10 @@ int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv
   int want = (m + kQrWarps - 1) / kQrWarps;
   int blocks = std::max(1, std::min(want, c.num_sms * std::min(g_pqr_blocks_per_sm, 1)));
   void* args[] = {&R, &mr, &m, &piv_dev, &tau_dev, &norms, &diag_dev};
-  PW_CUDA(cudaLaunchCooperativeKernel((void*)pqr_kernel, dim3(blocks), dim3(kQrThreads), args, 0,
-                                      c.stream));
+  const char* pe = getenv("PW_PQR");
+  const bool two_barriers = (pe && atoi(pe) == 2) || mr > kQrMaxRows;
+  PW_CUDA(cudaLaunchCooperativeKernel(two_barriers ? (void*)pqr_kernel : (void*)pqr1_kernel, dim3(blocks),
+                                      dim3(kQrThreads), args, 0, c.stream));
   c.launches += 1;
   // rank = #{ |R_jj| > tol |R_11| } (subspace.py:69-72): host side from the m diagonal values
   std::vector<double> dg(steps);

@@ -83,3 +83,27 @@ def test_geqrf_matches_lapack(dev, rows, cols, lda_pad, kind):
         assert np.abs(sg[:, None] * R - Rl).max() <= 1e-12 * np.abs(Rl).max()
         same = sg > 0
         np.testing.assert_allclose(tau[same], taul[:k][same], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("d,m,dup", [(4096, 40, 0), (5000, 96, 7), (700, 300, 25), (64, 64, 3), (33, 50, 0)])
+def test_pivoted_qr_one_barrier_kernel_is_bitwise_equal_to_the_two_barrier_kernel(dev, monkeypatch, d, m, dup):
+    """The small pivoted QR of R1 (pqr1_kernel: every block forms the pivot column's reflector,
+    one grid barrier per column) against the two-barrier kernel (PW_PQR=2): same pivots, same
+    rank, bitwise equal Q and images -- including near-duplicate snapshots (rank decisions) and
+    more snapshots than rows."""
+    from paper_1510_02237_b200.subspace import Subspace
+
+    rng = np.random.default_rng(d + m)
+    cols = [rng.standard_normal(d) for _ in range(m - dup)]
+    for k in range(dup):  # near-duplicates: a kept column plus a perturbation at the rank tolerance
+        cols.append(cols[k] * (1.0 + 1e-3 * k) + 1e-11 * rng.standard_normal(d))
+    imgs = [np.roll(c, 1) * 0.5 for c in cols]
+    out = {}
+    for variant in ("2", "1"):
+        monkeypatch.setenv("PW_PQR", variant)
+        sub = Subspace(d).update(cols[: m // 2], imgs[: m // 2]).update(cols[m // 2:], imgs[m // 2:])
+        out[variant] = (sub.rank, sub.q.copy(), sub.fq.copy())
+    assert out["1"][0] == out["2"][0]
+    assert out["1"][0] <= min(d, m)
+    np.testing.assert_array_equal(out["1"][1], out["2"][1])
+    np.testing.assert_array_equal(out["1"][2], out["2"][2])

@@ -123,3 +123,28 @@ def test_c4_window_matches_reference_run():
     9.45e-11 at iteration 1, cond(R11) ~ 7e9), so two QR algorithms legitimately differ at
     eps * cond ~ 1e-6; the bound is 10 x the reference's own numba-vs-numpy floor."""
     check_window("c4", bounds("c4"))
+
+
+def test_c3_original_parareal_window_matches_reference_run():
+    """c3 with the ORIGINAL Parareal sweep (parareal.py:68-97, no subspace) against the
+    reference's own run (tests/golden/make_parareal_window_golden.py).  No ill-conditioned
+    factorisation is involved, so the north star's 1e-10 per slice and iteration applies as is."""
+    from paper_1510_02237_b200.parareal import parareal_sweep
+
+    path = os.path.join(GOLDEN, "c3_parareal_reference.npz")
+    if not os.path.exists(path):
+        pytest.skip("c3_parareal_reference.npz not generated")
+    g = np.load(path)
+    wl, fine, coarse = props("c3")
+    q0 = torch.as_tensor(harness.initial_state("c3")).cuda()
+    idx = torch.as_tensor(g["idx"]).cuda()
+    worst = []
+    for k in range(1, len(g["res"]) + 1):
+        ends, res = parareal_sweep(q0, fine, coarse, wl.n_p, k, return_device=True)
+        st = (torch.stack(list(ends)) if isinstance(ends, (list, tuple)) else ends).reshape(wl.n_p, -1)
+        norms = torch.linalg.norm(st, dim=1).cpu().numpy()
+        samp = st[:, idx].cpu().numpy()
+        worst.append(_stat(norms, samp, g["norms"][k - 1], g["samples"][k - 1]))
+        np.testing.assert_allclose(res, g["res"][:k], rtol=1e-10)
+        assert worst[-1] <= 1e-10, (k, worst[-1])
+    print(f"c3 original Parareal: per-iteration max relative deviation vs the reference run: {worst}")
