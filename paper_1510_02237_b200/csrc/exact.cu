@@ -1591,8 +1591,10 @@ static int nf_variant() {
   // 0: the grid-barrier kernels; 2 / 3 / 4: substeps per phase (phase-A form); 6 / 10: phase A
   // folded into the first block (K = 3 / 2); 11 / 12: folded + register-resident columns
   // (K = 3 / 2; 12 is the default: 512^2 2-step call 160 us, 1024^2 623 us, from 200 / 698)
+  // -1 (default): 11 where one 60-row tile per SM covers the grid (512^2: 151 us per 2-step call
+  // against 155 with K = 2, both with resident tiles), else 12
   const char* e = getenv("PW_COARSE_NF");
-  return (e && *e) ? atoi(e) : 12;
+  return (e && *e) ? atoi(e) : -1;
 }
 
 // Row-sharded G: one state whose rows live in nsh row shards, shard s holding
@@ -1644,10 +1646,16 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
   if (nsteps <= 0 || batch <= 0) return;
   PW_CHECK((long long)p.nx * p.ny < (1LL << 31), PW_ERR_VALUE, "grid too large");
   if (!c.strict && batch == 1 && ld >= 3LL * p.nx * p.ny && p.nx % 32 == 0 && p.ny >= 64 &&
-      (long long)p.nx * p.ny >= 16384 && nf_variant() > 0) {
+      (long long)p.nx * p.ny >= 16384 && nf_variant() != 0) {
     const bool o1 = p.order == 1;
     bool ok = false;
-    switch (nf_variant()) {
+    int variant = nf_variant();
+    if (variant < 0) {
+      const int t60 = (p.nx / 32) * ((p.ny + 59) / 60);
+      const int sms = c.num_sms > 0 ? c.num_sms : 148;
+      variant = (t60 <= sms && 2 * t60 >= sms) ? 11 : 12;
+    }
+    switch (variant) {
       case 2: ok = o1 ? launch_nf<64, 2, 512, 1>(c, p, states, nsteps, h, nsub, work)
                       : launch_nf<64, 2, 512, 0>(c, p, states, nsteps, h, nsub, work); break;
       case 4: ok = o1 ? launch_nf<56, 4, 512, 1>(c, p, states, nsteps, h, nsub, work)
