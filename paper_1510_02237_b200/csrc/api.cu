@@ -1473,6 +1473,13 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     // (PW_IMPLICIT_Q=0 keeps the explicit Q = Q1 Q2 product of every update)
     const char* iq_env = std::getenv("PW_IMPLICIT_Q");
     const bool implicit_q = kse && c.comm_world <= 1 && c.vshards <= 1 && !(iq_env && *iq_env == '0');
+    // PW_ALPHA_FROM_R=1 (opt-in): Q^T qk_i read off the pivoted factor instead of a GEMM over the
+    // d rows.  Same c3 / c4 deviations from the reference runs and 4 ms less per c3 window, but the
+    // projection of one vector then differs in the last bits from iteration to iteration (it is a
+    // column of a different factorisation each time), so a converged slice no longer reproduces
+    // its previous iterate bit for bit (residual 2e-16 instead of the reference's exact 0).
+    const char* ar_env = getenv("PW_ALPHA_FROM_R");
+    const bool alpha_from_r = kse && c.comm_world <= 1 && c.vshards <= 1 && ar_env && *ar_env == '1';
     long long roff = 0, ldr = d;
     if (local) {
       const long long blk = ((d + c.comm_world - 1) / c.comm_world + 1) / 2 * 2;
@@ -1622,12 +1629,20 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             // implicit Q: Q^T QK = Q2^T QK[0:mr] - X2^T (V^T QK)
             const int mr = B->cq_n1, kv = B->cq_n2, lc = mr + kv;
             double* gv = bGv.ensure(c, (size_t)kv * (n_c + 1));
-            gemm(c, true, false, kv, n_c, d, 1.0, B->W.p, d, QK, d, 0.0, gv, kv);
-            gemm(c, true, false, r, n_c, mr, 1.0, B->Cq.p, lc, QK, d, 0.0, ab, r);
-            gemm(c, true, false, r, n_c, kv, 1.0, B->Cq.p + mr, lc, gv, kv, 1.0, ab, r);
+            if (alpha_from_r && !tsqr_applicable(B.get())) {
+              // the qk are this update's snapshots: Q^T qk_i is a column of the pivoted factor
+              pw::launch_alpha_from_r(c, B->Rs.p, (int)std::min<long long>(d, B->m), B->piv.p, B->m, m_old, n_c, r, ab);
+            } else {
+              gemm(c, true, false, kv, n_c, d, 1.0, B->W.p, d, QK, d, 0.0, gv, kv);
+              gemm(c, true, false, r, n_c, mr, 1.0, B->Cq.p, lc, QK, d, 0.0, ab, r);
+              gemm(c, true, false, r, n_c, kv, 1.0, B->Cq.p + mr, lc, gv, kv, 1.0, ab, r);
+            }
             gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           } else {
-            gemm(c, true, false, r, n_c, d, 1.0, basis_q(B.get()), d, QK, d, 0.0, ab, r);
+            if (alpha_from_r && !tsqr_applicable(B.get()))
+              pw::launch_alpha_from_r(c, B->Rs.p, (int)std::min<long long>(d, B->m), B->piv.p, B->m, m_old, n_c, r, ab);
+            else
+              gemm(c, true, false, r, n_c, d, 1.0, basis_q(B.get()), d, QK, d, 0.0, ab, r);
             gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           }
           alpha = ab;                             // column 0 = Q^T q0

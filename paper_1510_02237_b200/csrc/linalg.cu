@@ -1024,6 +1024,32 @@ void launch_gather_rows(Ctx& c, const double* X, int m, const int* piv, int r, d
   PW_LAUNCH_CHECK();
 }
 
+// alpha = Q^T s for snapshot columns c0 .. c0 + nc - 1, read off the factorisation:
+// S Pi = Q R2 (R2 = the pivoted factor of R1, stored by pqr in place: column piv[k] of Rs holds
+// R2[0..k, k]), so Q[:, :r]^T S[:, piv[k]] = R2[0..r-1, k] -- the first r entries of that
+// stored column, zero below row k.  No pass over the d-row basis.
+__global__ void alpha_from_r_kernel(const double* __restrict__ Rs, int mr, const int* __restrict__ piv, int m,
+                                    int steps, int c0, int r, double* __restrict__ alpha) {
+  __shared__ int s_k;
+  const int c = c0 + blockIdx.x;
+  if (threadIdx.x == 0) s_k = m;  // never pivoted (m > mr): every stored row is an R entry
+  __syncthreads();
+  for (int k = threadIdx.x; k < steps; k += blockDim.x)
+    if (piv[k] == c) s_k = k;
+  __syncthreads();
+  const int k = s_k;
+  const double* col = Rs + (size_t)c * mr;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) alpha[(size_t)blockIdx.x * r + i] = (i <= k) ? col[i] : 0.0;
+}
+
+void launch_alpha_from_r(Ctx& c, const double* Rs, int mr, const int* piv, int m, int c0, int nc, int r,
+                         double* alpha) {
+  if (r <= 0 || nc <= 0) return;
+  alpha_from_r_kernel<<<nc, 256, 0, c.stream>>>(Rs, mr, piv, m, mr < m ? mr : m, c0, r, alpha);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
 static int cg_variant() {
   static int v = -1;
   if (v < 0) {

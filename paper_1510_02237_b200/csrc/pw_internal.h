@@ -224,6 +224,9 @@ void dgemm(Ctx& c, bool ta, long long m, long long n, long long k, double alpha,
 
 // Xc (r x r) = rows piv[0..r) of X (m x r): R11^-1 back from its scattered form
 void launch_gather_rows(Ctx& c, const double* X, int m, const int* piv, int r, double* Xc);
+// alpha (r x nc, ld r) = Q^T S[:, c0 .. c0 + nc) from the pivoted factor stored in Rs (mr x m)
+void launch_alpha_from_r(Ctx& c, const double* Rs, int mr, const int* piv, int m, int c0, int nc, int r,
+                         double* alpha);
 
 // tall-skinny Householder QR (tsqr.cu): LAPACK geqrf's output format for rows x p
 void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double* tau);
