@@ -1157,6 +1157,9 @@ int pw_prop_create_pde(pw_ctx* ctx, const pw_pde_desc* desc, pw_prop** out) {
     };
     P->ex.inv_dx = pow2_inv(D.dx);
     P->ex.inv_dy = pow2_inv(D.dy);
+    P->ex.cvel = cst ? 1 : 0;
+    P->ex.uc = hu[0];
+    P->ex.vc = hv[0];
     if (D.scheme == PW_SCHEME_RK3 && cst) {
       pw::make_fused_params(P->fp, D.nx, D.ny, D.dx, D.dy, D.cs, D.order, hu[0], hv[0], D.a1,
                             D.a2, D.h);

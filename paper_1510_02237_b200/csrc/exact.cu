@@ -963,11 +963,13 @@ __device__ __forceinline__ double adv_smem(const ExactParams& p, const double* p
   const int gyp = gy + 1 < ny ? gy + 1 : 0;
   const double* r = pl + y * RX;
   auto fx = [&](int f, int gf) {  // face between region cells f-1 | f of row y
-    return face_flux(order, __ldg(p.uf + (size_t)gy * nx + gf), r[f - 3], r[f - 2], r[f - 1], r[f], r[f + 1], r[f + 2]);
+    const double uface = p.cvel ? p.uc : __ldg(p.uf + (size_t)gy * nx + gf);
+    return face_flux(order, uface, r[f - 3], r[f - 2], r[f - 1], r[f], r[f + 1], r[f + 2]);
   };
   auto gyf = [&](int f, int gf) {  // face between region rows f-1 | f of column x
     const double* c = pl + x;
-    return face_flux(order, __ldg(p.vf + (size_t)gf * nx + gx), c[(f - 3) * RX], c[(f - 2) * RX], c[(f - 1) * RX],
+    const double vface = p.cvel ? p.vc : __ldg(p.vf + (size_t)gf * nx + gx);
+    return face_flux(order, vface, c[(f - 3) * RX], c[(f - 2) * RX], c[(f - 1) * RX],
                      c[f * RX], c[(f + 1) * RX], c[(f + 2) * RX]);
   };
   const double fxi = fx(x, gx), fxp = fx(x + 1, gxp);

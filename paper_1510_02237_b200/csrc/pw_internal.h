@@ -66,6 +66,10 @@ struct ExactParams {
   // 1/dx, 1/dy when dx, dy are powers of two: x/dx == x*(1/dx) exactly then,
   // so the divisions of flux_divergence become multiplies without changing a bit
   double inv_dx = 0.0, inv_dy = 0.0;
+  // the face velocities when every face carries the same value (cvel = 1): the shared-memory
+  // tendency pass of the coarse G takes them from here instead of two global loads per face
+  int cvel = 0;
+  double uc = 0.0, vc = 0.0;
 };
 
 // Folded constant-velocity RK3 coefficients for one stage with factor beta
