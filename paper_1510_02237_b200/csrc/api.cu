@@ -1481,6 +1481,14 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     // projection of one vector then differs in the last bits from iteration to iteration (it is a
     // column of a different factorisation each time), so a converged slice no longer reproduces
     // its previous iterate bit for bit (residual 2e-16 instead of the reference's exact 0).
+    // Folded correction (single unsharded GPU; PW_FOLD_CORRECTION=0 restores the GEMM form):
+    // c_i keeps only F(qk_i) - G(qk_i) and the serial pass applies D (alpha(qn_i) - alpha(qk_i)) in
+    // one go, instead of subtracting D alpha(qk_i) from c_i by a d x P x r GEMM and adding
+    // D alpha(qn_i) in the pass: K(qn_i) - K(qk_i) with the two projections differenced before D.
+    // Same deviations from the reference runs (c3 3.7e-7, c4 2.0e-6), and a converged slice still
+    // reproduces its iterate exactly (alpha(qn_i) == alpha(qk_i) bit for bit gives D 0 = 0).
+    const char* fc_env = getenv("PW_FOLD_CORRECTION");
+    const bool fold_corr = kse && c.comm_world <= 1 && c.vshards <= 1 && !(fc_env && *fc_env == '0');
     const char* ar_env = getenv("PW_ALPHA_FROM_R");
     const bool alpha_from_r = kse && c.comm_world <= 1 && c.vshards <= 1 && ar_env && *ar_env == '1';
     long long roff = 0, ldr = d;
@@ -1640,13 +1648,13 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
               gemm(c, true, false, r, n_c, mr, 1.0, B->Cq.p, lc, QK, d, 0.0, ab, r);
               gemm(c, true, false, r, n_c, kv, 1.0, B->Cq.p + mr, lc, gv, kv, 1.0, ab, r);
             }
-            gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
+            if (!fold_corr) gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           } else {
             if (alpha_from_r && !tsqr_applicable(B.get()))
               pw::launch_alpha_from_r(c, B->Rs.p, (int)std::min<long long>(d, B->m), B->piv.p, B->m, m_old, n_c, r, ab);
             else
               gemm(c, true, false, r, n_c, d, 1.0, basis_q(B.get()), d, QK, d, 0.0, ab, r);
-            gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
+            if (!fold_corr) gemm(c, false, false, d, n_c, r, -1.0, B->Y.p, d, ab, r, 1.0, PRED, d);
           }
           alpha = ab;                             // column 0 = Q^T q0
           alpha_next = ab + (size_t)r * n_c;      // scratch pair after the block
@@ -1724,12 +1732,14 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             const int mr = B->cq_n1, kv = B->cq_n2;
             double* gv = bGv.p + (size_t)kv * n_c;
             pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B->Y.p, r, PRED + (size_t)i * d, a_cur,
-                                    B->W.p, kv, d, QN + (size_t)(i + 1) * d, gv, part);
+                                    B->W.p, kv, d, QN + (size_t)(i + 1) * d, gv, part, 0, 0,
+                                    fold_corr ? alpha + (size_t)i * r : nullptr);
             pw::launch_implicit_alpha(c, B->Cq.p, mr + kv, QN + (size_t)(i + 1) * d, mr, gv, kv, r, a_nxt);
           } else {
             pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B ? B->Y.p : nullptr, r,
                                     PRED + (size_t)i * d, a_cur, (B && r > 0) ? basis_q(B.get()) : nullptr, r, d,
-                                    QN + (size_t)(i + 1) * d, a_nxt, part);
+                                    QN + (size_t)(i + 1) * d, a_nxt, part, 0, 0,
+                                    (fold_corr && r > 0) ? alpha + (size_t)i * r : nullptr);
           }
           a_cur = a_nxt;
         }

@@ -422,13 +422,13 @@ template <int UNR, int MINB, bool V2>
 __global__ void __launch_bounds__(kCgThreads, MINB) combine_gemv_kernel(
     const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
     const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d, long long ld,
-    double* __restrict__ y_out, double* __restrict__ part) {
+    double* __restrict__ y_out, double* __restrict__ part, const double* __restrict__ alpha_sub) {
   // d rows starting at the given pointers; D and Q columns are ld apart (ld >= d: a row
   // block of a sharded basis passes its block's first-row pointers)
   extern __shared__ double sh[];
   double* a_s = sh;             // rd
   double* wpart = sh + rd;      // kCgWarps x rq
-  for (int k = threadIdx.x; k < rd; k += blockDim.x) a_s[k] = alpha[k];
+  for (int k = threadIdx.x; k < rd; k += blockDim.x) a_s[k] = alpha_sub ? alpha[k] - alpha_sub[k] : alpha[k];
   for (int k = threadIdx.x; k < kCgWarps * rq; k += blockDim.x) wpart[k] = 0.0;
   __syncthreads();
   const long long ntiles = (d + kCgRows - 1) / kCgRows;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
     const double* __restrict__ g, const double* __restrict__ D, int rd, const double* __restrict__ cvec,
     const double* __restrict__ alpha, const double* __restrict__ Q, int rq, long long d, long long ld,
     double* __restrict__ y_out, double* __restrict__ part, int nst, unsigned int* __restrict__ done,
-    double* __restrict__ alpha_next) {
+    double* __restrict__ alpha_next, const double* __restrict__ alpha_sub) {
   // nst ring stages (<= kTmaStages: fewer when rd + 8 rq doubles of bookkeeping must fit too).
   // The last CTA to finish sums the per-CTA partials into alpha_next (fixed order).
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -524,7 +524,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) combine_tma_kernel(
   double* a_s = reinterpret_cast<double*>(empty + nst);                   // rd
   double* wpart = a_s + rd;                                               // 8 warps x rq
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int k = tid; k < rd; k += blockDim.x) a_s[k] = alpha[k];
+  // alpha_sub: the pass applies D (alpha - alpha_sub) (the sweep's folded correction term)
+  for (int k = tid; k < rd; k += blockDim.x) a_s[k] = alpha_sub ? alpha[k] - alpha_sub[k] : alpha[k];
   for (int k = tid; k < kCgWarps * rq; k += blockDim.x) wpart[k] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -1071,7 +1072,7 @@ int combine_grid(const Ctx& c, long long d, int per_sm) {
 template <int UNR, int MINB, bool V2>
 static int launch_cg(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                       const double* cvec, const double* alpha, const double* Q, int rq, long long d,
-                      long long ld, double* y, double* part, int nblk) {
+                      long long ld, double* y, double* part, int nblk, const double* alpha_sub) {
   auto kern = combine_gemv_kernel<UNR, MINB, V2>;
   if (nblk <= 0) nblk = combine_grid(c, d, MINB);
   size_t smem = sizeof(double) * ((size_t)rd + (size_t)rq * kCgWarps + 1);
@@ -1080,14 +1081,14 @@ static int launch_cg(Ctx& c, cudaStream_t st, const double* g, const double* D, 
     PW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  kern<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part);
+  kern<<<nblk, kCgThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, alpha_sub);
   return nblk;
 }
 
 void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                          const double* cvec, const double* alpha, const double* Q, int rq,
                          long long d, double* y, double* alpha_next, double* part, int nblk,
-                         long long ld) {
+                         long long ld, const double* alpha_sub) {
   if (ld <= 0) ld = d;
   // 16-byte pairs need every column (and the row block) 16-byte aligned
   const bool v2 = (d % 2 == 0) && (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(D) |
@@ -1111,25 +1112,25 @@ void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double*
       PW_CUDA(cudaMemsetAsync(c.tma_done, 0, sizeof(unsigned int), st));
     }
     combine_tma_kernel<<<nblk, kTmaThreads, smem, st>>>(g, D, rd, cvec, alpha, Q, rq, d, ld, y, part,
-                                                        tma_nst, c.tma_done, alpha_next);
+                                                        tma_nst, c.tma_done, alpha_next, alpha_sub);
     c.launches += 1;
     PW_LAUNCH_CHECK();
     return;
   }
   switch (var) {
-    case 1: nblk = launch_cg<4, 2, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk); break;
-    case 2: nblk = launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk); break;
+    case 1: nblk = launch_cg<4, 2, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub); break;
+    case 2: nblk = launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub); break;
     case 3:
-      nblk = v2 ? launch_cg<4, 4, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk)
-                : launch_cg<4, 4, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk);
+      nblk = v2 ? launch_cg<4, 4, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub)
+                : launch_cg<4, 4, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub);
       break;
     case 4:
-      nblk = v2 ? launch_cg<8, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk)
-                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk);
+      nblk = v2 ? launch_cg<8, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub)
+                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub);
       break;
     default:
-      nblk = v2 ? launch_cg<4, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk)
-                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk);
+      nblk = v2 ? launch_cg<4, 3, true>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub)
+                : launch_cg<4, 3, false>(c, st, g, D, rd, cvec, alpha, Q, rq, d, ld, y, part, nblk, alpha_sub);
       break;
   }
   c.launches += 1;

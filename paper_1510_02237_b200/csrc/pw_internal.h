@@ -255,12 +255,12 @@ void form_q2(Ctx& c, const double* R, int mr, const int* piv, const double* tau,
              double* Q2);
 void tri_inverse_scatter(Ctx& c, const double* R, int mr, int m, const int* piv, int r,
                          double* X);
-// y = [g +] c + D alpha (rd cols) and alpha_next = Q^T y (rq cols); nblk <= 0: default grid
+// y = [g +] c + D (alpha [- alpha_sub]) (rd cols) and alpha_next = Q^T y (rq cols); nblk <= 0: default grid
 // d rows from the given pointers; D / Q columns ld apart (ld <= 0: ld = d)
 void launch_combine_gemv(Ctx& c, cudaStream_t st, const double* g, const double* D, int rd,
                          const double* cvec, const double* alpha, const double* Q, int rq,
                          long long d, double* y, double* alpha_next, double* part, int nblk = 0,
-                         long long ld = 0);
+                         long long ld = 0, const double* alpha_sub = nullptr);
 // alpha[j] = C[0:n1, j] . xt + C[n1:n1+n2, j] . g for j < r (C column-major, ld ldc): the
 // small step that turns the reflector products V^T x into Q^T x when Q is kept implicit
 void launch_implicit_alpha(Ctx& c, const double* C, int ldc, const double* xt, int n1, const double* g, int n2,
