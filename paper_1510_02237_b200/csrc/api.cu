@@ -1476,21 +1476,21 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
     // (PW_IMPLICIT_Q=0 keeps the explicit Q = Q1 Q2 product of every update)
     const char* iq_env = std::getenv("PW_IMPLICIT_Q");
     const bool implicit_q = kse && c.comm_world <= 1 && c.vshards <= 1 && !(iq_env && *iq_env == '0');
-    // PW_ALPHA_FROM_R=1 (opt-in): Q^T qk_i read off the pivoted factor instead of a GEMM over the
-    // d rows.  Same c3 / c4 deviations from the reference runs and 4 ms less per c3 window, but the
-    // projection of one vector then differs in the last bits from iteration to iteration (it is a
-    // column of a different factorisation each time), so a converged slice no longer reproduces
-    // its previous iterate bit for bit (residual 2e-16 instead of the reference's exact 0).
     // Folded correction (single unsharded GPU; PW_FOLD_CORRECTION=0 restores the GEMM form):
     // c_i keeps only F(qk_i) - G(qk_i) and the serial pass applies D (alpha(qn_i) - alpha(qk_i)) in
     // one go, instead of subtracting D alpha(qk_i) from c_i by a d x P x r GEMM and adding
     // D alpha(qn_i) in the pass: K(qn_i) - K(qk_i) with the two projections differenced before D.
-    // Same deviations from the reference runs (c3 3.7e-7, c4 2.0e-6), and a converged slice still
-    // reproduces its iterate exactly (alpha(qn_i) == alpha(qk_i) bit for bit gives D 0 = 0).
+    // Same deviations from the reference runs (c3 3.7e-7, c4 2.0e-6), and a converged first slice
+    // still reproduces its iterate exactly (alpha(qn_0) and alpha(qk_0) are the same vector).
     const char* fc_env = getenv("PW_FOLD_CORRECTION");
     const bool fold_corr = kse && c.comm_world <= 1 && c.vshards <= 1 && !(fc_env && *fc_env == '0');
+    // Q^T qk_i read off the pivoted factor instead of a GEMM over the d rows (PW_ALPHA_FROM_R=0
+    // restores the GEMM): the qk_i are this update's snapshots, so Q^T S = R2[:r, :] Pi^T holds their
+    // projections already.  Same c3 / c4 deviations from the reference runs.  (With the folded
+    // correction the first slice's projection cancels exactly whatever its bits, so a converged
+    // first slice still repeats bit for bit.)  The row-sharded paths keep the GEMM.
     const char* ar_env = getenv("PW_ALPHA_FROM_R");
-    const bool alpha_from_r = kse && c.comm_world <= 1 && c.vshards <= 1 && ar_env && *ar_env == '1';
+    const bool alpha_from_r = kse && c.comm_world <= 1 && c.vshards <= 1 && !(ar_env && *ar_env == '0');
     long long roff = 0, ldr = d;
     if (local) {
       const long long blk = ((d + c.comm_world - 1) / c.comm_world + 1) / 2 * 2;
