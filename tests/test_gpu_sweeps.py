@@ -229,6 +229,27 @@ def test_c1_kse_lean_mode_matches_reference(monkeypatch):
     assert sub.q.shape == (g["q0"].size, sub.rank)
 
 
+@pytest.mark.parametrize("fold,from_r,implicit", [("0", "0", "1"), ("0", "1", "1"), ("1", "0", "1"),
+                                                   ("1", "1", "0"), ("0", "0", "0")])
+def test_c1_kse_regrouped_correction_forms_match_reference(monkeypatch, fold, from_r, implicit):
+    """The serial correction's algebraic forms on one GPU: the folded correction
+    D (alpha(qn_i) - alpha(qk_i)) (PW_FOLD_CORRECTION), the snapshot projections read off the
+    pivoted factor (PW_ALPHA_FROM_R) and the implicit / explicit Q (PW_IMPLICIT_Q), in the
+    combinations other than the default -- each against the reference's golden c1 history."""
+    from paper_1510_02237_b200.parareal import kse_sweep
+
+    g = golden("c1_kse.npz")
+    wl, fine, coarse = c1_props()
+    monkeypatch.setenv("PW_FOLD_CORRECTION", fold)
+    monkeypatch.setenv("PW_ALPHA_FROM_R", from_r)
+    monkeypatch.setenv("PW_IMPLICIT_Q", implicit)
+    ends, res, sub = kse_sweep(g["q0"], fine, coarse, wl.n_p, wl.n_it)
+    assert sub.rank == g["kse_ranks"][-1]
+    worst = max(rel(ends[i], g["kse_hist"][-1][i]) for i in range(wl.n_p))
+    assert worst <= 1e-10, worst
+    np.testing.assert_allclose(res, g["kse_res"], rtol=1e-10)
+
+
 @pytest.mark.parametrize("nsh", [2, 3, 5])
 def test_c1_kse_row_sharded_serial_correction(dev, nsh):
     """The multi-GPU serial step (row shards of D and Q, partial alphas summed, rows
