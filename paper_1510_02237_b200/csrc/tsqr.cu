@@ -509,6 +509,69 @@ __global__ void __launch_bounds__(128) recon_solve_kernel(double* panel, long lo
 }
 
 
+
+// Trailing update of a sub-panel, C (rows x n, ld ldc) -= V (rows x TB, ld ldv) X (TB x n, ld TB):
+// the rank-32 GEMM the generic tiles run 3.5x off the HBM roofline (one 128 x 64 tile per CTA
+// with a 32-deep k loop is all prologue and epilogue).  Streaming form: a thread owns one row,
+// keeps its 32 entries of V in registers, and walks the columns of C (coalesced 256-byte column
+// segments per warp) with X broadcast from shared memory; 8 columns in flight per thread.
+// Bytes: rows x (2 n + TB) x 8; flops 2 x rows x n x TB on the DFMA pipe -- about balanced.
+constexpr int kRkThreads = 256;
+__global__ void __launch_bounds__(kRkThreads, 2) rank_tb_update_kernel(const double* __restrict__ V, long long ldv,
+                                                                       const double* __restrict__ X, int n,
+                                                                       double* __restrict__ C, long long ldc,
+                                                                       long long rows) {
+  extern __shared__ double xs[];  // TB x n, column-major (ld TB)
+  for (int e = threadIdx.x; e < TB * n; e += blockDim.x) xs[e] = X[e];
+  __syncthreads();
+  for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < rows;
+       row += (long long)gridDim.x * blockDim.x) {
+    double v[TB];
+#pragma unroll
+    for (int k = 0; k < TB; ++k) v[k] = V[row + k * ldv];
+    double* crow = C + row;
+    int j = 0;
+    for (; j + 8 <= n; j += 8) {
+      double cc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cc[u] = crow[(long long)(j + u) * ldc];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2* xc = reinterpret_cast<const double2*>(xs + (size_t)(j + u) * TB);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < TB / 2; ++k) {
+          const double2 x2 = xc[k];
+          acc = fma(v[2 * k], x2.x, acc);
+          acc = fma(v[2 * k + 1], x2.y, acc);
+        }
+        cc[u] -= acc;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) crow[(long long)(j + u) * ldc] = cc[u];
+    }
+    for (; j < n; ++j) {
+      const double* xc = xs + (size_t)j * TB;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < TB; ++k) acc = fma(v[k], xc[k], acc);
+      crow[(long long)j * ldc] -= acc;
+    }
+  }
+}
+
+void launch_rank_tb_update(Ctx& c, const double* V, long long ldv, const double* X, int n, double* C, long long ldc,
+                           long long rows) {
+  const size_t smem = sizeof(double) * TB * (size_t)n;
+  // set up once for the widest X (n <= 256: 64 KB), whatever this call's n
+  const int per_sm = kernel_setup(c, rank_tb_update_kernel, kRkThreads, sizeof(double) * TB * 256);
+  const long long want = (rows + kRkThreads - 1) / kRkThreads;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(want, (long long)std::max(c.num_sms, 1) * per_sm * 4));
+  rank_tb_update_kernel<<<grid, kRkThreads, smem, c.stream>>>(V, ldv, X, n, C, ldc, rows);
+  c.launches += 1;
+  PW_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 // geqrf of A (rows x p, ld lda) -> R / V in place, tau (min(rows, p)); see the header.
@@ -615,7 +678,14 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
       if (mrows > b) dgemm(c, true, b, nrest, mrows - b, 1.0, P + b, lda, Ar + b, lda, 1.0, Wt, b);
       dgemm(c, true, b, nrest, b, 1.0, T, b, Wt, b, 0.0, Xt, b);
       dgemm(c, false, b, nrest, b, -1.0, Vtop, b, Xt, b, 1.0, Ar, lda);
-      if (mrows > b) dgemm(c, false, mrows - b, nrest, b, -1.0, P + b, lda, Xt, b, 1.0, Ar + b, lda);
+      if (mrows > b) {
+        // b == TB except for a ragged last sub-panel (none follows it: nrest == 0 there)
+        static const bool generic = getenv("PW_TSQR_TRAIL_GEMM") && atoi(getenv("PW_TSQR_TRAIL_GEMM")) == 1;
+        if (b == TB && nrest <= 256 && !generic)
+          launch_rank_tb_update(c, P + b, lda, Xt, (int)nrest, Ar + b, lda, mrows - b);
+        else
+          dgemm(c, false, mrows - b, nrest, b, -1.0, P + b, lda, Xt, b, 1.0, Ar + b, lda);
+      }
     }
   }
   PW_CUDA(cudaFreeAsync(scr, c.stream));
