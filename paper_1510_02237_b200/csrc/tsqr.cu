@@ -424,6 +424,76 @@ __global__ void __launch_bounds__(32 * NW) tsqr_expand_kernel(TsqrArgs a) {
   }
 }
 
+// The leaf level of the explicit-Q pass, thread = row: X = [C; 0] - V (T (V_top^T C)) for the
+// 128-row leaf i, written over the leaf's reflectors.  A thread keeps its row of V in registers
+// (32 coalesced loads) and forms its 32 outputs against Y2 = T V_top^T C broadcast from shared
+// memory -- no staging of the 128 x 32 block through shared memory, six leaves per SM.  Every
+// element is accumulated in the order of tsqr_expand_kernel<true> (k ascending, the same fma),
+// so the two are bitwise equal (PW_TSQR_EXPAND=1 selects the staged kernel for A/B runs).
+__global__ void __launch_bounds__(32 * NWL) tsqr_expand_leaf_rows_kernel(TsqrArgs a) {
+  constexpr int TL = Blk<NWL>::TL, NT = Blk<NWL>::NT;
+  __shared__ double C[TB][TB + 1], Y[TB][TB + 1], T[TB][TB + 1], Vt[TB][TB + 1];
+  __shared__ __align__(16) double Y2t[TB][TB];  // [col][k]: the k pairs a thread walks are 16-byte loads
+  const int b = a.b;
+  const long long i = blockIdx.x;
+  const long long r0 = i * TL;
+  const int r = threadIdx.x;
+  double* const row = (r0 + r < a.rows) ? a.panel + r0 + r : nullptr;
+  double v[TB];
+#pragma unroll
+  for (int cc = 0; cc < TB; ++cc) v[cc] = (row && cc < b) ? row[cc * a.lda] : 0.0;
+  if (r < TB) {
+#pragma unroll
+    for (int cc = 0; cc < TB; ++cc) Vt[r][cc] = v[cc];
+  }
+  for (int e = threadIdx.x; e < TB * TB; e += NT) {
+    const int cc = e / TB, rr = e - cc * TB;
+    double x = 0.0, t = 0.0;
+    if (cc < b && rr < b) {
+      x = a.cin ? a.cin[(i / NWN) * (TB * TLN) + (long long)cc * TLN + (i % NWN) * b + rr] : (rr == cc ? 1.0 : 0.0);
+      t = a.tnode[i * TB * TB + rr + cc * b];
+    }
+    C[rr][cc] = x;
+    T[rr][cc] = t;
+  }
+  __syncthreads();
+  // Y = V_top^T C
+  for (int e = threadIdx.x; e < TB * TB; e += NT) {
+    const int yr = e / TB, c = e - yr * TB;
+    double acc = 0.0;
+    for (int kk = 0; kk < b; ++kk) acc = fma(Vt[kk][yr], C[kk][c], acc);
+    Y[yr][c] = acc;
+  }
+  __syncthreads();
+  // Y2 = T Y (T upper triangular), stored transposed
+  for (int e = threadIdx.x; e < TB * TB; e += NT) {
+    const int yr = e / TB, c = e - yr * TB;
+    double acc = 0.0;
+    for (int kk = yr; kk < b; ++kk) acc = fma(T[yr][kk], Y[kk][c], acc);
+    Y2t[c][yr] = acc;
+  }
+  __syncthreads();
+  if (!row) return;
+#pragma unroll 1
+  for (int c0 = 0; c0 < TB; c0 += 4) {
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = (r < TB) ? C[r][c0 + u] : 0.0;
+#pragma unroll
+    for (int k2 = 0; k2 < TB / 2; ++k2) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 y2 = *reinterpret_cast<const double2*>(&Y2t[c0 + u][2 * k2]);
+        x[u] = fma(-v[2 * k2], y2.x, x[u]);
+        x[u] = fma(-v[2 * k2 + 1], y2.y, x[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < b) row[(long long)(c0 + u) * a.lda] = x[u];
+  }
+}
+
 // Modified LU of Q_top - S (one warp; lane = row): U, s, L1 -> tau, T = -U S L1^-T, the
 // explicit unit-lower V_top for the trailing GEMMs, and the panel's top block
 // (strict lower = L1, upper = S R).  small: [U (b x b) | Vtop (b x b) | T (b x b)].
@@ -653,7 +723,12 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
       a.tnode = Tb + off[l] * TB * TB;
       a.cin = (l == L - 1) ? nullptr : Xb + voff[l + 1] * TB * TLN;
       if (l == 0) {
-        tsqr_expand_kernel<true, NWL><<<(unsigned)ml[0], Blk<NWL>::NT, Blk<NWL>::SMEM, c.stream>>>(a);
+        const char* se = getenv("PW_TSQR_EXPAND");
+        const bool staged = se && atoi(se) == 1;
+        if (staged)
+          tsqr_expand_kernel<true, NWL><<<(unsigned)ml[0], Blk<NWL>::NT, Blk<NWL>::SMEM, c.stream>>>(a);
+        else
+          tsqr_expand_leaf_rows_kernel<<<(unsigned)ml[0], Blk<NWL>::NT, 0, c.stream>>>(a);
       } else {
         a.vnode = Vb + voff[l] * TB * TLN;
         a.xout = Xb + voff[l] * TB * TLN;
@@ -680,7 +755,8 @@ void tsqr_geqrf(Ctx& c, long long rows, int p, double* A, long long lda, double*
       dgemm(c, false, b, nrest, b, -1.0, Vtop, b, Xt, b, 1.0, Ar, lda);
       if (mrows > b) {
         // b == TB except for a ragged last sub-panel (none follows it: nrest == 0 there)
-        static const bool generic = getenv("PW_TSQR_TRAIL_GEMM") && atoi(getenv("PW_TSQR_TRAIL_GEMM")) == 1;
+        const char* ge = getenv("PW_TSQR_TRAIL_GEMM");
+        const bool generic = ge && atoi(ge) == 1;
         if (b == TB && nrest <= 256 && !generic)
           launch_rank_tb_update(c, P + b, lda, Xt, (int)nrest, Ar + b, lda, mrows - b);
         else

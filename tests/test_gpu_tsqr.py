@@ -107,3 +107,26 @@ def test_pivoted_qr_one_barrier_kernel_is_bitwise_equal_to_the_two_barrier_kerne
     assert out["1"][0] <= min(d, m)
     np.testing.assert_array_equal(out["1"][1], out["2"][1])
     np.testing.assert_array_equal(out["1"][2], out["2"][2])
+
+
+@pytest.mark.parametrize("rows,cols,lda_pad", [(1000, 32, 3), (5000, 45, 0), (200000, 64, 0), (70001, 96, 1), (33, 40, 0)])
+def test_geqrf_leaf_expand_and_trailing_update_variants(dev, monkeypatch, rows, cols, lda_pad):
+    """The panel QR's two streaming kernels against the kernels they replaced: the row-per-thread
+    leaf pass of the explicit Q (tsqr_expand_leaf_rows_kernel) accumulates in the staged kernel's
+    order, so geqrf's output is bitwise equal (PW_TSQR_EXPAND=1); the rank-32 trailing update
+    (rank_tb_update_kernel) sums its 32 products in another order than the GEMM tiles
+    (PW_TSQR_TRAIL_GEMM=1), so that pair agrees to rounding."""
+    rng = np.random.default_rng(3 * rows + cols)
+    A = rng.standard_normal((rows, cols)) @ np.diag(np.logspace(0, -9, cols))
+    qr0, tau0 = geqrf(dev, A, lda_pad)
+    monkeypatch.setenv("PW_TSQR_EXPAND", "1")
+    qr1, tau1 = geqrf(dev, A, lda_pad)
+    np.testing.assert_array_equal(qr0, qr1)
+    np.testing.assert_array_equal(tau0, tau1)
+    monkeypatch.delenv("PW_TSQR_EXPAND")
+    monkeypatch.setenv("PW_TSQR_TRAIL_GEMM", "1")
+    qr2, tau2 = geqrf(dev, A, lda_pad)
+    k = min(rows, cols)
+    scale = np.abs(np.triu(qr0[:k, :])).max(axis=0)  # per column: R's largest entry
+    assert (np.abs(np.triu(qr2[:k, :]) - np.triu(qr0[:k, :])).max(axis=0) <= 1e-12 * scale + 1e-300).all()
+    np.testing.assert_allclose(tau2, tau0, rtol=0, atol=1e-12)
