@@ -1443,14 +1443,18 @@ struct StreamScope {
   }
 };
 struct SyncEvents {
-  cudaEvent_t snap = nullptr, fact = nullptr;
+  cudaEvent_t snap = nullptr, fact = nullptr, pass = nullptr, coef = nullptr;
   SyncEvents() {
     PW_CUDA(cudaEventCreateWithFlags(&snap, cudaEventDisableTiming));
     PW_CUDA(cudaEventCreateWithFlags(&fact, cudaEventDisableTiming));
+    PW_CUDA(cudaEventCreateWithFlags(&pass, cudaEventDisableTiming));
+    PW_CUDA(cudaEventCreateWithFlags(&coef, cudaEventDisableTiming));
   }
   ~SyncEvents() {
     cudaEventDestroy(snap);
     cudaEventDestroy(fact);
+    cudaEventDestroy(pass);
+    cudaEventDestroy(coef);
   }
 };
 }  // namespace
@@ -1723,6 +1727,9 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
           a_cur = a_nxt;
         }
       } else {
+        const char* co_env = getenv("PW_COEF_OVERLAP");
+        const bool coef_overlap = !(co_env && *co_env == '0');
+        bool coef_pending = false;
         for (int i = 0; i < n_c; ++i) {
           prop_apply(coarse, QN + (size_t)i * d, GN + (size_t)i * d, 1, d);
           double* a_nxt = (r > 0) ? a_buf[i % 2] : nullptr;
@@ -1731,10 +1738,27 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
             // alpha_{i+1} = Cq^T [qn_{i+1}[0:mr]; V^T qn_{i+1}]
             const int mr = B->cq_n1, kv = B->cq_n2;
             double* gv = bGv.p + (size_t)kv * n_c;
+            // the small step alpha_{i+1} = Cq^T [qn_{i+1}[0:mr]; gv] runs on the side stream beside the
+            // next G (whose persistent CTAs leave a few SMs free): the pass of step i+1 waits for it
+            if (coef_pending) {
+              PW_CUDA(cudaStreamWaitEvent(c.stream, sync.coef, 0));
+              coef_pending = false;
+            }
             pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B->Y.p, r, PRED + (size_t)i * d, a_cur,
                                     B->W.p, kv, d, QN + (size_t)(i + 1) * d, gv, part, 0, 0,
                                     fold_corr ? alpha + (size_t)i * r : nullptr);
-            pw::launch_implicit_alpha(c, B->Cq.p, mr + kv, QN + (size_t)(i + 1) * d, mr, gv, kv, r, a_nxt);
+            if (coef_overlap && c.side) {
+              PW_CUDA(cudaEventRecord(sync.pass, c.stream));
+              PW_CUDA(cudaStreamWaitEvent(c.side, sync.pass, 0));
+              {
+                StreamScope side(c, c.side);
+                pw::launch_implicit_alpha(c, B->Cq.p, mr + kv, QN + (size_t)(i + 1) * d, mr, gv, kv, r, a_nxt);
+              }
+              PW_CUDA(cudaEventRecord(sync.coef, c.side));
+              coef_pending = true;
+            } else {
+              pw::launch_implicit_alpha(c, B->Cq.p, mr + kv, QN + (size_t)(i + 1) * d, mr, gv, kv, r, a_nxt);
+            }
           } else {
             pw::launch_combine_gemv(c, c.stream, GN + (size_t)i * d, B ? B->Y.p : nullptr, r,
                                     PRED + (size_t)i * d, a_cur, (B && r > 0) ? basis_q(B.get()) : nullptr, r, d,
@@ -1743,6 +1767,7 @@ int pw_sweep(pw_ctx* ctx, int mode, pw_prop* fine, pw_prop* coarse, const double
           }
           a_cur = a_nxt;
         }
+        if (coef_pending) PW_CUDA(cudaStreamWaitEvent(c.stream, sync.coef, 0));  // join the side stream
       }
       pw::launch_residual(c, QK + d, d, QN + d, d, n_c, d, scr, res_dev + k);
       nv_phase.reset();
