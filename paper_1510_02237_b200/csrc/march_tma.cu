@@ -152,6 +152,44 @@ __device__ __forceinline__ void ld_chunks(double (&w)[2 * N], const double* row,
     w[2 * j + 1] = t.y;
   }
 }
+// A thread's x window (BX + 8 cells, w[1] .. w[BX + 6] are read) as 128-bit chunk loads (the
+// compiler narrows the two half-used edge chunks to 64-bit loads, which conflict 2-way at 32
+// bytes per lane whatever the swizzle: 14 % of the kernel's shared-memory wavefronts).
+// -DPW_K1_SHFL=1 takes the two edge cells from the neighbouring lanes' registers instead (they
+// are those lanes' w[BX + 1] and w[6]; 4 SHFL.32 = 4 passes of the pipe against 8; lanes 0 and 31
+// load theirs): same values, parity-tested, but measured SLOWER at c2 (59.4 vs 72.8 G/s: the
+// shuffles sit between the loads and the first taps, 168 registers and 20 bytes of spills).
+#ifndef PW_K1_SHFL
+#define PW_K1_SHFL 0
+#endif
+template <int BX>
+__device__ __forceinline__ void ld_window(double (&w)[BX + 8], const double* row, const int* off) {
+  constexpr int NCH = BX / 2 + 4;
+#if PW_K1_SHFL
+#pragma unroll
+  for (int j = 1; j < NCH - 1; ++j) {
+    const double2 t = *reinterpret_cast<const double2*>(row + off[j]);
+    w[2 * j] = t.x;
+    w[2 * j + 1] = t.y;
+  }
+  const int lane = threadIdx.x & 31;
+  double lo = __shfl_up_sync(0xffffffffu, w[BX + 1], 1);
+  double hi = __shfl_down_sync(0xffffffffu, w[6], 1);
+  if (lane == 0) lo = row[off[0] + 1];
+  if (lane == 31) hi = row[off[NCH - 1]];
+  w[0] = 0.0;
+  w[1] = lo;
+  w[BX + 6] = hi;
+  w[BX + 7] = 0.0;
+#else
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const double2 t = *reinterpret_cast<const double2*>(row + off[j]);
+    w[2 * j] = t.x;
+    w[2 * j + 1] = t.y;
+  }
+#endif
+}
 template <int BX>
 __device__ __forceinline__ void st4(double* row, const int* off, const double (&v)[BX]) {
 #pragma unroll
@@ -269,7 +307,7 @@ __device__ __forceinline__ void row_step(Acc<BX>& A, const double* in, const dou
   constexpr int V0 = (PH + 1) % 3, V1 = (PH + 2) % 3, V2 = PH;  // v: rows k-2 (-> k+1), k-1, k
   double w[BX + 8], d1[BX];
   // ---- v row k: x stencil of row k; completes v(k-2); births v(k+1); u_y-mixed / p_y terms
-  ld_chunks<NCH>(w, in + FS, woff);
+  ld_window<BX>(w, in + FS, woff);
   // v: cxv equals cxp off the centre; the +-2 taps are plain advection
   xstencil<BX>(A.v[V2], d1, w, C.cxv[3], C.cxp[1], C.cxp[5], C);
 #pragma unroll
@@ -324,7 +362,7 @@ __device__ __forceinline__ void row_step(Acc<BX>& A, const double* in, const dou
   // ---- u row k: x stencil (advection + the symmetric x damping at +-2 and the centre);
   //      u_x for p(k) and the mixed damping of v(k-1), v(k+1)
   double t2[BX];
-  ld_chunks<NCH>(w, in, woff);
+  ld_window<BX>(w, in, woff);
   xstencil<BX>(A.u[U1], d1, w, C.cxu[3], C.cxu[1], C.cxu[5], C);
 #pragma unroll
   for (int c = 0; c < BX; ++c) {
@@ -332,7 +370,7 @@ __device__ __forceinline__ void row_step(Acc<BX>& A, const double* in, const dou
     t2[c] = C.cvu * d1[c];
   }
   // ---- p row k: x stencil; p_x for u(k), p_y for v(k-1), v(k+1)
-  ld_chunks<NCH>(w, in + 2 * FS, woff);
+  ld_window<BX>(w, in + 2 * FS, woff);
   xstencil<BX>(A.p[U1], d1, w, C.cxp[3], C.cxp[1], C.cxp[5], C);
 #pragma unroll
   for (int c = 0; c < BX; ++c) {
