@@ -143,14 +143,6 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int N>
-__device__ __forceinline__ void ld_chunks(double (&w)[2 * N], const double* row, const int* off) {
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const double2 t = *reinterpret_cast<const double2*>(row + off[j]);
-    w[2 * j] = t.x;
-    w[2 * j + 1] = t.y;
-  }
 }
 // A thread's x window (BX + 8 cells, w[1] .. w[BX + 6] are read) as 128-bit chunk loads (the
 // compiler narrows the two half-used edge chunks to 64-bit loads, which conflict 2-way at 32
