@@ -143,7 +143,6 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-}
 // A thread's x window (BX + 8 cells, w[1] .. w[BX + 6] are read) as 128-bit chunk loads (the
 // compiler narrows the two half-used edge chunks to 64-bit loads, which conflict 2-way at 32
 // bytes per lane whatever the swizzle: 14 % of the kernel's shared-memory wavefronts).
