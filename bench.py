@@ -276,9 +276,10 @@ def parareal_window(name="c3", warm=True, group=None, repeats=None):
                                              4.0, 16), wl.slice_span)
     q0 = torch.as_tensor(harness.initial_state(name)).cuda()
     if warm:
-        # warm-up: first-use module loads and the stream-ordered pool's allocations.  The pool
-        # needs three c3 windows to settle (measured: 0.342, 0.257, then 0.246 s steadily), one c4
-        # window (4.96-4.97 s from the second on)
+        # warm-up: first-use module loads and the stream-ordered pool's allocations.  c3 windows
+        # keep getting faster for about three windows (one warm-up: 0.342, 0.257, then 0.246 s
+        # steadily; three: 0.295, 0.248, 0.248), so the fastest of the timed samples is the
+        # steady state; c4 is steady from its second window (4.96-4.97 s)
         for _ in range(3 if name == "c3" else 1):
             kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True, group=group)
             gc.collect()
