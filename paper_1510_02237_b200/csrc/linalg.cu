@@ -958,6 +958,7 @@ int pivoted_qr_small(Ctx& c, double* R, int mr, int m, double rank_tol, int* piv
   double* norms = c.red;
   int want = (m + kQrWarps - 1) / kQrWarps;
   int blocks = std::max(1, std::min(want, c.num_sms * std::min(g_pqr_blocks_per_sm, 1)));
+  if (const char* be = getenv("PW_PQR_BLOCKS")) blocks = std::max(1, std::min(blocks, atoi(be)));  // tuning hook
   void* args[] = {&R, &mr, &m, &piv_dev, &tau_dev, &norms, &diag_dev};
   const char* pe = getenv("PW_PQR");
   const bool two_barriers = (pe && atoi(pe) == 2) || mr > kQrMaxRows;
