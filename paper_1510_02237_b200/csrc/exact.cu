@@ -1594,7 +1594,9 @@ static int nf_variant() {
   // folded into the first block (K = 3 / 2); 11 / 12: folded + register-resident columns
   // (K = 3 / 2; 12 is the default: 512^2 2-step call 160 us, 1024^2 623 us, from 200 / 698)
   // -1 (default): 11 where one 60-row tile per SM covers the grid (512^2: 151 us per 2-step call
-  // against 155 with K = 2, both with resident tiles), else 12
+  // against 155 with K = 2, both with resident tiles), else K = 2 with 64-row (12) or 58-row (17)
+  // tiles, whichever needs fewer CTA rounds x tile rows (1024^2: 576 tiles of 57 rows are four
+  // 97 %-full rounds of 148 CTAs, 584 us against 606 with 512 tiles of 64 rows)
   const char* e = getenv("PW_COARSE_NF");
   return (e && *e) ? atoi(e) : -1;
 }
@@ -1655,7 +1657,12 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
     if (variant < 0) {
       const int t60 = (p.nx / 32) * ((p.ny + 59) / 60);
       const int sms = c.num_sms > 0 ? c.num_sms : 148;
-      variant = (t60 <= sms && 2 * t60 >= sms) ? 11 : 12;
+      // tiles outnumber the SMs: rounds of CTAs x rows per tile, for 64- and 58-row tiles
+      auto cost = [&](int tmy) {
+        const int ty = (p.ny + tmy - 1) / tmy, tiles = (p.nx / 32) * ty;
+        return (long long)((tiles + sms - 1) / sms) * ((p.ny + ty - 1) / ty);
+      };
+      variant = (t60 <= sms && 2 * t60 >= sms) ? 11 : (cost(58) < cost(64) ? 17 : 12);
     }
     switch (variant) {
       case 2: ok = o1 ? launch_nf<64, 2, 512, 1>(c, p, states, nsteps, h, nsub, work)
@@ -1679,6 +1686,9 @@ void launch_fefb_exact(Ctx& c, const ExactParams& p, double* states, int batch, 
                        : launch_nfm<60, 3, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
       case 12: ok = o1 ? launch_nfm<64, 2, 512, 1, 1, true>(c, p, states, nsteps, h, nsub, work)
                        : launch_nfm<64, 2, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
+      case 17:  // K = 2 with 58-row tiles: 1024^2 in 576 tiles of 57 rows (4 rounds of 148 CTAs, 97 % full)
+        ok = o1 ? launch_nfm<58, 2, 512, 1, 1, true>(c, p, states, nsteps, h, nsub, work)
+                : launch_nfm<58, 2, 512, 0, 1, true>(c, p, states, nsteps, h, nsub, work); break;
       case 13: ok = o1 ? launch_nfm<30, 2, 256, 1, 2, true>(c, p, states, nsteps, h, nsub, work)
                        : launch_nfm<30, 2, 256, 0, 2, true>(c, p, states, nsteps, h, nsub, work); break;
       default: ok = o1 ? launch_nf<60, 3, 512, 1>(c, p, states, nsteps, h, nsub, work)

@@ -59,7 +59,7 @@ def run_both(dev, spec, x, nsteps):
     return got, want
 
 
-@pytest.mark.parametrize("variant", ["2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12", "13"])
+@pytest.mark.parametrize("variant", ["2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12", "13", "17"])
 @pytest.mark.parametrize("nx,ny", [(512, 512), (256, 256), (512, 320), (1024, 1024), (128, 128), (256, 96)])
 def test_nf_coarse_bitwise(dev, monkeypatch, variant, nx, ny):
     monkeypatch.setenv("PW_COARSE_NF", variant)
@@ -67,7 +67,7 @@ def test_nf_coarse_bitwise(dev, monkeypatch, variant, nx, ny):
     assert torch.equal(got, want)
 
 
-@pytest.mark.parametrize("variant", ["3", "6", "10", "11", "12", "13"])
+@pytest.mark.parametrize("variant", ["3", "6", "10", "11", "12", "13", "17"])
 @pytest.mark.parametrize("case", ["odd_blocks", "order3", "no_damping", "upwind_negative", "c5_grid"])
 def test_nf_coarse_cases_bitwise(dev, monkeypatch, variant, case):
     monkeypatch.setenv("PW_COARSE_NF", variant)
