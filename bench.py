@@ -267,7 +267,7 @@ def parareal_window(name="c3", warm=True, group=None, repeats=None):
 
     wl = harness.WORKLOADS[name]
     if repeats is None:
-        repeats = 3 if name == "c3" else 1
+        repeats = 6 if name == "c3" else 1
     g = build_grid(wl.n, wl.n)
     vel = ConstantVelocity(harness.VEL_U, harness.VEL_V)
     fine = SlicePropagator(make_propagator(RK3, ModelSpec(ACOUSTIC, vel, 6, 1.0, 0.005, 1.0), g, 0.5),
@@ -283,7 +283,7 @@ def parareal_window(name="c3", warm=True, group=None, repeats=None):
         for _ in range(3 if name == "c3" else 1):
             kse_sweep(q0, fine, coarse, wl.n_p, wl.n_it, return_device=True, group=group)
             gc.collect()
-    # the window is timed `repeats` times (c3: 3 x 0.27 s; c4 once) and the fastest run is
+    # the window is timed `repeats` times (c3: 6 x 0.25 s; c4 once) and the fastest run is
     # reported with every sample next to it: the wall clock around a window also sees the
     # host (320 serial steps are enqueued from one thread), which varies from box to box
     samples, best = [], None
